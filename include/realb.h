@@ -1,0 +1,192 @@
+/*
+ * realb.h — C-ABI of the B200-native ReaLB MoE-layer hot path (sm_100a).
+ *
+ * Reference: arXiv 2604.19503 ("ReaLB"); reference package `moesim`
+ * (/root/reference/pkg/src/moesim). The reference is pure Python with no FFI,
+ * so every entry point below replaces a Python function or an analytic cost
+ * formula on the MoE-layer path; the replaced symbol is cited per function.
+ *
+ * Conventions (all functions):
+ *   - Plain pointers and sizes only. Every pointer argument named `d_*` is a
+ *     DEVICE pointer owned by the caller; nothing here allocates or frees
+ *     device memory (TMEM inside kernels excepted).
+ *   - `stream` is a cudaStream_t passed as void*. Every call is stream-ordered,
+ *     re-entrant, performs no host synchronisation and keeps no hidden state.
+ *   - Return value: REALB_OK (0) or a negative status. A human-readable
+ *     message for the last failure on the calling thread is available from
+ *     realb_last_error(). No C++ exception crosses this boundary.
+ *   - Data errors found on the device (non-finite quantiser input, mirroring
+ *     moesim.fp4.QuantizationDomainError, fp4.py:22) are reported through a
+ *     caller-provided int32 device flag, checked lazily by the caller.
+ */
+#ifndef REALB_H_
+#define REALB_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define REALB_API __attribute__((visibility("default")))
+#else
+#define REALB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REALB_ABI_VERSION 1
+
+#define REALB_OK 0
+#define REALB_EINVAL (-1)      /* bad argument (shape, alignment, range)      */
+#define REALB_ECUDA (-2)       /* CUDA runtime / launch failure               */
+#define REALB_EUNSUPPORTED (-3) /* shape outside what the kernels implement   */
+
+/* element types for `dtype` arguments */
+#define REALB_DT_BF16 0
+#define REALB_DT_F32 1
+#define REALB_DT_F64 2
+
+/* scale-factor layouts written by the quantisers */
+#define REALB_SF_FLAT 0    /* [rows][cols/16] row-major: moesim's (n,) order   */
+#define REALB_SF_MMA128x4 1 /* tcgen05 block-scale layout: 128-row x 4-SF
+                               512-byte atoms, byte = (r%32)*16+((r/32)%4)*4+k%4,
+                               atoms ordered (r/128, k/4) row-major            */
+
+/* router scoring functions (D1 contract) */
+#define REALB_SCORE_SOFTMAX_RENORM 0  /* Qwen3-VL-MoE: softmax, top-k, renorm   */
+#define REALB_SCORE_SIGMOID_RENORM 1  /* Kimi-VL (DeepSeek-V3 family): sigmoid,
+                                         top-k, renorm, x routed_scaling       */
+#define REALB_SCORE_SOFTMAX_CLAMPNORM 2 /* ERNIE-4.5-VL: softmax, top-k,
+                                           / max(sum, norm_min)                */
+
+/* precision codes: values of moesim.core.Precision (core.py:9-11) */
+#define REALB_PREC_W16A16 0
+#define REALB_PREC_W4A4 1
+
+REALB_API int realb_abi_version(void);
+REALB_API const char* realb_last_error(void);
+/* number of SMs of the current device, or <0 */
+REALB_API int realb_num_sms(void);
+
+/* ------------------------------------------------------------------------ *
+ * K3 / K4 — NVFP4 block quantiser.
+ * Replaces moesim.fp4.quantize_blocks (fp4.py:173-227), bit-exact, and its
+ * scalar twin quantize_block (fp4.py:108-122). Blocks are 16 consecutive
+ * elements along a row of x[rows][cols] (cols % 16 == 0).
+ *   d_codes : [rows][cols/2] bytes, element 2i in the low nibble (= pack_block
+ *             order, fp4.py:246-252, and the tcgen05 packed-E2M1 order)
+ *   d_sf    : E4M3 scale bytes, layout `sf_layout`; REALB_SF_MMA128x4 needs
+ *             rows % 128 == 0 and cols % 64 == 0.
+ *   d_nonfinite_flag : set to 1 when any element is non-finite
+ *             (QuantizationDomainError); may be NULL.
+ *   max_ctas: cap on CTAs (0 = auto) so the quantiser can run CTA-limited on
+ *             a side stream next to NCCL.
+ * ------------------------------------------------------------------------ */
+REALB_API int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, int64_t cols,
+                         uint8_t* d_codes, uint8_t* d_sf, int sf_layout,
+                         int32_t* d_nonfinite_flag, int max_ctas, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * K1 + K2 — router / top-k / modality statistics (new: the reference
+ * synthesises routing, tracegen.py:141-185; the counts it produces feed
+ * aggregate_rank_loads, core.py:106-130).
+ *   d_x        : bf16 [T][H] hidden states, H % 64 == 0
+ *   d_wg       : bf16 [E][H] router weight
+ *   d_bias     : fp32 [E] selection bias (e_score_correction_bias) or NULL
+ *   d_modality : uint8 [T], 1 = vision token, 0 = text
+ *   d_logits   : fp32 [T][E] logits written by the kernel (the D1 contract
+ *                selects on exactly these values)
+ *   d_topk_idx : int32 [T][k], experts in selection order (score desc, ties
+ *                to the lowest expert id)
+ *   d_topk_w   : fp32 [T][k] routing weights
+ *   d_chunk_counts : int32 [ceil(T/128)][E][2] per-128-token-chunk
+ *                (vision, text) pair counts (deterministic, atomic-free)
+ * E <= 256, 1 <= k <= 16.
+ * ------------------------------------------------------------------------ */
+REALB_API int realb_router_topk_stats(const void* d_x, const void* d_wg, const float* d_bias,
+                            const uint8_t* d_modality, int T, int H, int E, int k,
+                            int scoring, float routed_scaling, float norm_min,
+                            float* d_logits, int32_t* d_topk_idx, float* d_topk_w,
+                            int32_t* d_chunk_counts, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * Grouped-row layout ("align"): from the per-chunk counts, build the
+ * expert-sorted, 128-row-padded row space the grouped GEMMs run on.
+ * d_layout is an int32 workspace of realb_layout_words(E, nchunks) words:
+ *   [0] padded rows used   [1] #W16A16 groups   [2] #W4A4 groups
+ *   [8 + e]          row_start[e]    [8 + E + e]   row_count[e]
+ *   [8 + 2E + e]     expert (v,t) totals are in d_expert_vt instead
+ *   glist/prefix per precision and per-chunk offsets follow (internal).
+ * d_expert_prec : uint8 [E] REALB_PREC_* per expert (the precision plan
+ *                 expanded through the placement, balancers.py:113-118).
+ * d_expert_vt   : int32 [E][2] global (vision, text) pair counts (output).
+ * ------------------------------------------------------------------------ */
+REALB_API int64_t realb_layout_words(int E, int nchunks);
+REALB_API int realb_moe_align(const int32_t* d_chunk_counts, int nchunks, int E,
+                    const uint8_t* d_expert_prec, int32_t* d_layout,
+                    int32_t* d_expert_vt, void* stream);
+
+/* Local dispatch: scatter token rows into the grouped row space.
+ *   d_pair_pos : int32 [T][k] output row of every (token, slot) pair
+ *   d_a_bf16   : bf16 [rows_cap][H] rows of W16A16 experts (others untouched)
+ *   d_a_codes / d_a_sf : W4A4 experts' rows, quantised on the fly with the
+ *                reference block rule (fp4.py:108-122) into MMA layout;
+ *                may be NULL when no expert is W4A4.
+ * Padding rows of every group are zero-filled. */
+REALB_API int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx, int T, int H,
+                           int E, int k, const uint8_t* d_expert_prec,
+                           const int32_t* d_layout, int nchunks, int64_t rows_cap,
+                           int32_t* d_pair_pos, void* d_a_bf16, uint8_t* d_a_codes,
+                           uint8_t* d_a_sf, int32_t* d_nonfinite_flag, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * K5 — grouped BF16 expert GEMM on tcgen05 (kind::f16, TMA, TMEM).
+ *   out[r][n] = sum_k A[r][k] * W[g*N + n][k]  over the groups of precision
+ *   `prec` listed in d_layout.
+ *   epilogue REALB_EPI_STORE  : out bf16 [rows][N]
+ *   epilogue REALB_EPI_SWIGLU : W rows are gate/up interleaved in 128-row
+ *        halves (D4); out bf16 [rows][N/2] = silu(gate) * up,
+ *        and, when d_out_codes != NULL, also NVFP4-quantised (K4 fused).
+ * Replaces the compute term of moesim.costmodel.rank_compute_latency
+ * (costmodel.py:60-68).
+ * ------------------------------------------------------------------------ */
+#define REALB_EPI_STORE 0
+#define REALB_EPI_SWIGLU 1
+REALB_API int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t rows_cap,
+                            int N, int K, int E, const int32_t* d_layout, int prec,
+                            int epilogue, void* d_out, int max_ctas, void* stream);
+
+/* K6 — grouped NVFP4 x NVFP4 GEMM (tcgen05 kind::mxf4nvf4.block_scale,
+ * scale_vec::4X, UE4M3 scales in REALB_SF_MMA128x4 layout) over the W4A4
+ * groups of d_layout. Weight rows are indexed by global expert id
+ * (W row g*N + n), so only the W4A4 experts' rows need to be quantised.
+ * With REALB_EPI_SWIGLU and d_out_codes/d_out_sf non-NULL, the SwiGLU output
+ * is written directly as NVFP4 codes + MMA-layout scales for the next GEMM. */
+REALB_API int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t* d_a_sf,
+                             const uint8_t* d_w_codes, const uint8_t* d_w_sf,
+                             int64_t rows_cap, int N, int K, int E,
+                             const int32_t* d_layout, int epilogue,
+                             void* d_out, uint8_t* d_out_codes, uint8_t* d_out_sf,
+                             int max_ctas, void* stream);
+
+/* C3 (local part) — weighted top-k combine:
+ *   y[t][h] = sum_j topk_w[t][j] * rows[pair_pos[t][j]][h]   (fp32 acc, bf16 out) */
+REALB_API int realb_combine(const void* d_rows, const int32_t* d_pair_pos, const float* d_topk_w,
+                  int T, int H, int k, void* d_y, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * P1 — host precision policy, identical fp64 operation order to
+ * moesim.balancers.plan_realb (balancers.py:89-122). Host-only (no CUDA).
+ *   rank_vt : int64 [R][2] (vision, text) per rank (RankLoad, core.py:70-89)
+ *   out_prec: uint8 [R] REALB_PREC_*; out_flags: uint8 [R] bit0 hot,
+ *             bit1 vision-heavy.  Returns 1 if the plan is active, 0 if the
+ *             batch gate kept it inactive, <0 on error.
+ * ------------------------------------------------------------------------ */
+REALB_API int realb_plan(const int64_t* rank_vt, int R, double capacity_factor,
+               double modality_threshold, int64_t global_batch_threshold,
+               int modality_isolated, uint8_t* out_prec, uint8_t* out_flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REALB_H_ */

@@ -1,0 +1,117 @@
+// fp4_rule.cuh — the reference NVFP4 block rule, restated for the device with
+// exact arithmetic (no division on elements), bit-exact with
+// moesim.fp4.quantize_blocks (fp4.py:173-227) / quantize_block (fp4.py:108-122).
+//
+//   scale_bits = E4M3_RNE(amax / 6)   (encode_e4m3, fp4.py:36-56; sat 448 -> 0x7E)
+//   amax == 0  -> scale 0, all codes 0           (fp4.py:115-116)
+//   scale_bits == 0 for a nonzero block -> 1     (fp4.py:118-119)
+//   code = nearest E2M1 magnitude of v / scale, ties to the even index,
+//          no negative zero                      (fp4.py:69-82, :222-226)
+//
+// Element codes: instead of dividing, |v| is compared with the exact products
+// mid_i * scale (mid_i in {0.25,0.75,1.25,1.75,2.5,3.5,5}; scale has <= 4
+// significant bits so every product is exact in fp32/fp64). For even i the
+// test is strict (>), for odd i it is (>=): that is the reference's
+// searchsorted(side="left") plus its odd-index tie bump. The reference's own
+// fp64 quotient can never round onto a midpoint it does not equal (DESIGN.md
+// §Q), so the comparisons are equivalent.
+#pragma once
+#include <stdint.h>
+
+namespace realb {
+
+// E4M3 decode (decode_e4m3, fp4.py:59-66); exact in fp32.
+__device__ __forceinline__ float e4m3_decode(uint32_t bits) {
+  uint32_t e = bits >> 3, m = bits & 7u;
+  if (e == 0) return (float)m * 0.001953125f;  // m * 2^-9
+  // (1 + m/8) * 2^(e-7): build the fp32 directly
+  uint32_t fb = ((e - 7u + 127u) << 23) | (m << 20);
+  return __uint_as_float(fb);
+}
+
+// E4M3 round-to-nearest-even of a non-negative fp32 x, saturating at 448
+// (encode_e4m3, fp4.py:36-56), integer-exact.
+__device__ __forceinline__ uint32_t e4m3_encode_f32(float x) {
+  if (x >= 448.0f) return 0x7Eu;
+  if (x < 0.015625f) {  // subnormal: m = rint(x / 2^-9), exact scaling
+    float m = rintf(x * 512.0f);
+    return m >= 8.0f ? 0x08u : (uint32_t)m;
+  }
+  uint32_t b = __float_as_uint(x);
+  int e = (int)((b >> 23) & 0xFF) - 127;
+  uint32_t mant = b & 0x7FFFFFu;
+  uint32_t m = mant >> 20, rem = mant & 0xFFFFFu;
+  if (rem > 0x80000u || (rem == 0x80000u && (m & 1u))) m += 1;
+  if (m == 8u) { m = 0; e += 1; }
+  if (e > 8 || (e == 8 && m > 6u)) return 0x7Eu;
+  return ((uint32_t)(e + 7) << 3) | m;
+}
+
+// Same rule on an fp64 value (the reference computes in float64; used for
+// fp64 inputs whose amax is not exactly representable in fp32).
+__device__ __forceinline__ uint32_t e4m3_encode_f64(double x) {
+  if (x >= 448.0) return 0x7Eu;
+  if (x < 0.015625) {
+    double m = rint(x * 512.0);
+    return m >= 8.0 ? 0x08u : (uint32_t)m;
+  }
+  unsigned long long b = __double_as_longlong(x);
+  int e = (int)((b >> 52) & 0x7FF) - 1023;
+  unsigned long long mant = b & 0xFFFFFFFFFFFFFull;
+  uint32_t m = (uint32_t)(mant >> 49);
+  unsigned long long rem = mant & ((1ull << 49) - 1);
+  const unsigned long long half = 1ull << 48;
+  if (rem > half || (rem == half && (m & 1u))) m += 1;
+  if (m == 8u) { m = 0; e += 1; }
+  if (e > 8 || (e == 8 && m > 6u)) return 0x7Eu;
+  return ((uint32_t)(e + 7) << 3) | m;
+}
+
+// block scale bits from amax (fp32 path: amax exactly representable in fp32)
+__device__ __forceinline__ uint32_t block_scale_bits_f32(float amax) {
+  if (amax == 0.0f) return 0u;
+  uint32_t s = e4m3_encode_f32(__fdiv_rn(amax, 6.0f));  // IEEE division, DESIGN.md §Q
+  return s == 0u ? 1u : s;
+}
+__device__ __forceinline__ uint32_t block_scale_bits_f64(double amax) {
+  if (amax == 0.0) return 0u;
+  uint32_t s = e4m3_encode_f64(__ddiv_rn(amax, 6.0));
+  return s == 0u ? 1u : s;
+}
+
+// E2M1 code of v for a block with decoded scale `sc` (> 0).
+template <typename F>
+__device__ __forceinline__ uint32_t e2m1_code(F v, F sc) {
+  F mag = v < F(0) ? -v : v;
+  uint32_t idx = (uint32_t)(mag > F(0.25) * sc) + (uint32_t)(mag >= F(0.75) * sc) +
+                 (uint32_t)(mag > F(1.25) * sc) + (uint32_t)(mag >= F(1.75) * sc) +
+                 (uint32_t)(mag > F(2.5) * sc) + (uint32_t)(mag >= F(3.5) * sc) +
+                 (uint32_t)(mag > F(5.0) * sc);
+  return (v < F(0) && idx > 0u) ? (idx | 8u) : idx;
+}
+
+// Quantise 16 fp32 values (one block). Returns packed codes (element 2i in the
+// low nibble of byte i) as two 32-bit words; writes the scale bits.
+__device__ __forceinline__ uint2 quant_block16_f32(const float (&v)[16], uint32_t& sbits) {
+  float amax = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  sbits = block_scale_bits_f32(amax);
+  uint2 out = make_uint2(0u, 0u);
+  if (sbits != 0u) {
+    const float sc = e4m3_decode(sbits);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out.x |= e2m1_code<float>(v[i], sc) << (4 * i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out.y |= e2m1_code<float>(v[8 + i], sc) << (4 * i);
+  }
+  return out;
+}
+
+// byte offset of scale (row r, k-block kb) in the REALB_SF_MMA128x4 layout
+__host__ __device__ __forceinline__ int64_t sf_mma_offset(int64_t r, int64_t kb, int64_t nkb) {
+  const int64_t atom = (r >> 7) * (nkb >> 2) + (kb >> 2);
+  return atom * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (kb & 3);
+}
+
+}  // namespace realb

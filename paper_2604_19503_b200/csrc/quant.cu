@@ -1,0 +1,181 @@
+// quant.cu — K3: on-the-fly BF16 -> NVFP4 weight quantiser (also used for the
+// fp32/fp64 parity path). HBM-bound: 2.5625 B/element for bf16 input
+// (2 read + 0.5 codes + 0.0625 scale).
+//
+// Work unit = a 128-row x 4-block (64-column) tile: exactly one 512-byte
+// scale-factor atom of the tcgen05 block-scale layout, so the atom is written
+// as one contiguous, coalesced 512-byte run. Thread -> (row = b / 4,
+// kb = b % 4): four consecutive threads read one row's 128 contiguous input
+// bytes (bf16) and write its 32 contiguous code bytes.
+#include "common.cuh"
+#include "fp4_rule.cuh"
+
+namespace realb {
+
+template <typename T>
+struct Loader;
+
+template <>
+struct Loader<__nv_bfloat16> {
+  static __device__ __forceinline__ void load16(const __nv_bfloat16* p, float (&v)[16]) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 a = __ldg(q), b = __ldg(q + 1);
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+template <>
+struct Loader<float> {
+  static __device__ __forceinline__ void load16(const float* p, float (&v)[16]) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float4 t = __ldg(q + i);
+      v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+    }
+  }
+};
+
+__device__ __forceinline__ void flag_nonfinite(int32_t* flag) {
+  if (flag) atomicOr(flag, 1);
+}
+
+template <typename T, int LAYOUT>
+__global__ void __launch_bounds__(256) quant_kernel(const T* __restrict__ x, int64_t rows,
+                                                     int64_t cols, uint8_t* __restrict__ codes,
+                                                     uint8_t* __restrict__ sf, int32_t* flag) {
+  const int64_t nkb = cols >> 4;
+  const int64_t tiles_k = (nkb + 3) >> 2;
+  const int64_t tiles = ((rows + 127) >> 7) * tiles_k;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t tm = tile / tiles_k, tk = tile - tm * tiles_k;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int b = threadIdx.x + half * 256;
+      const int64_t r = tm * 128 + (b >> 2);
+      const int64_t kb = tk * 4 + (b & 3);
+      if (r >= rows || kb >= nkb) continue;
+      float v[16];
+      Loader<T>::load16(x + r * cols + kb * 16, v);
+      bool finite = true;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) finite &= isfinite(v[i]);
+      if (!finite) flag_nonfinite(flag);
+      uint32_t sbits;
+      uint2 c = quant_block16_f32(v, sbits);
+      *reinterpret_cast<uint2*>(codes + r * (cols >> 1) + kb * 8) = c;
+      const int64_t so = LAYOUT == REALB_SF_FLAT ? r * nkb + kb : sf_mma_offset(r, kb, nkb);
+      sf[so] = (uint8_t)sbits;
+    }
+  }
+}
+
+// fp64 input: the reference's own arithmetic width (parity path only).
+template <int LAYOUT>
+__global__ void __launch_bounds__(256) quant_kernel_f64(const double* __restrict__ x, int64_t rows,
+                                                         int64_t cols, uint8_t* __restrict__ codes,
+                                                         uint8_t* __restrict__ sf, int32_t* flag) {
+  const int64_t nkb = cols >> 4;
+  const int64_t tiles_k = (nkb + 3) >> 2;
+  const int64_t tiles = ((rows + 127) >> 7) * tiles_k;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t tm = tile / tiles_k, tk = tile - tm * tiles_k;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      const int b = threadIdx.x + half * 256;
+      const int64_t r = tm * 128 + (b >> 2);
+      const int64_t kb = tk * 4 + (b & 3);
+      if (r >= rows || kb >= nkb) continue;
+      const double2* q = reinterpret_cast<const double2*>(x + r * cols + kb * 16);
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double2 t = __ldg(q + i);
+        v[2 * i] = t.x; v[2 * i + 1] = t.y;
+      }
+      double amax = 0.0;
+      bool finite = true;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        finite &= isfinite(v[i]);
+        amax = fmax(amax, fabs(v[i]));
+      }
+      if (!finite) flag_nonfinite(flag);
+      const uint32_t sbits = block_scale_bits_f64(amax);
+      uint2 c = make_uint2(0u, 0u);
+      if (sbits) {
+        const double sc = (double)e4m3_decode(sbits);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c.x |= e2m1_code<double>(v[i], sc) << (4 * i);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c.y |= e2m1_code<double>(v[8 + i], sc) << (4 * i);
+      }
+      *reinterpret_cast<uint2*>(codes + r * (cols >> 1) + kb * 8) = c;
+      const int64_t so = LAYOUT == REALB_SF_FLAT ? r * nkb + kb : sf_mma_offset(r, kb, nkb);
+      sf[so] = (uint8_t)sbits;
+    }
+  }
+}
+
+template <typename T>
+static int launch_quant(void (*kernel)(const T*, int64_t, int64_t, uint8_t*, uint8_t*, int32_t*),
+                        const void* x, int64_t rows, int64_t cols, uint8_t* codes,
+                        uint8_t* sf, int32_t* flag, int max_ctas, cudaStream_t st) {
+  const int64_t tiles = ((rows + 127) / 128) * (((cols / 16) + 3) / 4);
+  int64_t grid = (int64_t)num_sms() * 8;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid > tiles) grid = tiles;
+  if (grid < 1) return REALB_OK;
+  kernel<<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, codes, sf, flag);
+  return check_launch("realb_quantize_nvfp4");
+}
+
+}  // namespace realb
+
+using namespace realb;
+
+extern "C" int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, int64_t cols,
+                                    uint8_t* d_codes, uint8_t* d_sf, int sf_layout,
+                                    int32_t* d_flag, int max_ctas, void* stream) {
+  if (!d_x || !d_codes || !d_sf || rows < 0 || cols <= 0 || cols % 16) {
+    set_error("realb_quantize_nvfp4: bad arguments (rows=%lld cols=%lld; cols must be a "
+              "positive multiple of 16)", (long long)rows, (long long)cols);
+    return REALB_EINVAL;
+  }
+  if (sf_layout != REALB_SF_FLAT && sf_layout != REALB_SF_MMA128x4) {
+    set_error("realb_quantize_nvfp4: unknown sf_layout %d", sf_layout);
+    return REALB_EINVAL;
+  }
+  if (sf_layout == REALB_SF_MMA128x4 && (rows % 128 || cols % 64)) {
+    set_error("realb_quantize_nvfp4: MMA scale layout needs rows%%128==0 and cols%%64==0 "
+              "(rows=%lld cols=%lld)", (long long)rows, (long long)cols);
+    return REALB_EINVAL;
+  }
+  if (rows == 0) return REALB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool flat = sf_layout == REALB_SF_FLAT;
+  switch (dtype) {
+    case REALB_DT_BF16:
+      return flat ? launch_quant(quant_kernel<__nv_bfloat16, REALB_SF_FLAT>, d_x, rows, cols,
+                                 d_codes, d_sf, d_flag, max_ctas, st)
+                  : launch_quant(quant_kernel<__nv_bfloat16, REALB_SF_MMA128x4>, d_x, rows, cols,
+                                 d_codes, d_sf, d_flag, max_ctas, st);
+    case REALB_DT_F32:
+      return flat ? launch_quant(quant_kernel<float, REALB_SF_FLAT>, d_x, rows, cols, d_codes,
+                                 d_sf, d_flag, max_ctas, st)
+                  : launch_quant(quant_kernel<float, REALB_SF_MMA128x4>, d_x, rows, cols, d_codes,
+                                 d_sf, d_flag, max_ctas, st);
+    case REALB_DT_F64:
+      return flat ? launch_quant(quant_kernel_f64<REALB_SF_FLAT>, d_x, rows, cols, d_codes, d_sf,
+                                 d_flag, max_ctas, st)
+                  : launch_quant(quant_kernel_f64<REALB_SF_MMA128x4>, d_x, rows, cols, d_codes,
+                                 d_sf, d_flag, max_ctas, st);
+    default:
+      set_error("realb_quantize_nvfp4: unknown dtype %d", dtype);
+      return REALB_EINVAL;
+  }
+}
