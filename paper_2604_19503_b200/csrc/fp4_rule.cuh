@@ -108,6 +108,85 @@ __device__ __forceinline__ uint2 quant_block16_f32(const float (&v)[16], uint32_
   return out;
 }
 
+// ---------------------------------------------------------------------------
+// bf16 fast path (the product path: weights, activations, SwiGLU output).
+// For bf16 inputs (8 significant bits) and E4M3 scales (4 bits) the quotient
+// v / scale is either exactly an E2M1 rounding midpoint or at least 2^-9
+// (relative) away from every midpoint. q1 = q0 + (v - q0*sc) * rcp(sc) with
+// q0 = v * rcp(sc) is exact at the midpoints and within a few fp32 ulps
+// elsewhere, so the hardware RNE conversion cvt.rn.satfinite.e2m1x2.f32 of q1
+// reproduces the reference's ties-to-even-index decision (verified over the
+// exhaustive bf16 x scale table, tests/test_quant_gpu.py). The conversion can
+// emit negative zero (0x8); it is canonicalised to 0 (fp4.py:80-81).
+__device__ __forceinline__ uint32_t cvt_e2m1x4(float a0, float a1, float a2, float a3) {
+  uint32_t out;
+  asm("{\n\t.reg .b8 b0, b1;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
+      "mov.b32 %0, {b0, b1, 0, 0};\n\t}"
+      : "=r"(out)
+      : "f"(a0), "f"(a1), "f"(a2), "f"(a3));
+  return out;
+}
+// 8 nibbles: any code with zero magnitude becomes +0
+__device__ __forceinline__ uint32_t canon_neg_zero(uint32_t x) {
+  const uint32_t mag = x & 0x77777777u;
+  const uint32_t nz = (mag + 0x77777777u) & 0x88888888u;  // bit 3 of a nibble set iff mag != 0
+  return mag | (x & nz);
+}
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// amax of 16 bf16 values held as 8 bf16x2 words (exact: integer max of |bits|)
+__device__ __forceinline__ float amax_bf16x16(const uint32_t (&w)[8]) {
+  uint32_t m = w[0] & 0x7FFF7FFFu;
+#pragma unroll
+  for (int i = 1; i < 8; ++i) {
+    const uint32_t a = w[i] & 0x7FFF7FFFu;
+    asm("max.u16x2 %0, %0, %1;" : "+r"(m) : "r"(a));
+  }
+  const uint32_t lo = m & 0xFFFFu, hi = m >> 16;
+  return __uint_as_float((lo > hi ? lo : hi) << 16);
+}
+
+__device__ __forceinline__ float q1_div(float v, float sc, float r) {
+  const float q0 = v * r;
+  const float rho = fmaf(-q0, sc, v);
+  return fmaf(rho, r, q0);
+}
+
+// one block of 16 bf16 (8 words) -> packed codes (element 2i low nibble), scale bits
+__device__ __forceinline__ uint2 quant_block16_bf16(const uint32_t (&w)[8], uint32_t& sbits) {
+  const float amax = amax_bf16x16(w);
+  sbits = block_scale_bits_f32(amax);
+  if (sbits == 0u) return make_uint2(0u, 0u);
+  const float sc = e4m3_decode(sbits);
+  const float r = __frcp_rn(sc);
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    c[i] = cvt_e2m1x4(q1_div(bf16lo(w[2 * i]), sc, r), q1_div(bf16hi(w[2 * i]), sc, r),
+                      q1_div(bf16lo(w[2 * i + 1]), sc, r), q1_div(bf16hi(w[2 * i + 1]), sc, r));
+  return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
+}
+
+// same for 16 fp32 values that are known to be bf16-representable
+__device__ __forceinline__ uint2 quant_block16_bf16vals(const float (&v)[16], uint32_t& sbits) {
+  float amax = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  sbits = block_scale_bits_f32(amax);
+  if (sbits == 0u) return make_uint2(0u, 0u);
+  const float sc = e4m3_decode(sbits);
+  const float r = __frcp_rn(sc);
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    c[i] = cvt_e2m1x4(q1_div(v[4 * i], sc, r), q1_div(v[4 * i + 1], sc, r),
+                      q1_div(v[4 * i + 2], sc, r), q1_div(v[4 * i + 3], sc, r));
+  return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
+}
+
 // byte offset of scale (row r, k-block kb) in the REALB_SF_MMA128x4 layout
 __host__ __device__ __forceinline__ int64_t sf_mma_offset(int64_t r, int64_t kb, int64_t nkb) {
   const int64_t atom = (r >> 7) * (nkb >> 2) + (kb >> 2);

@@ -1,0 +1,61 @@
+// grouped.cuh — persistent tile scheduler over the expert-sorted row space
+// produced by realb_moe_align (layout words, include/realb.h).
+//
+// Tiles of one precision class are numbered t = mt * n_tiles + nt where mt
+// runs over the concatenated 128-row m-tiles of the class's groups (experts)
+// and nt over the BN-wide n-tiles of N. Consecutive CTAs therefore share an
+// A m-block (L2 reuse of activations) and sweep the expert's weight rows.
+#pragma once
+#include "common.cuh"
+
+namespace realb {
+
+struct TileCoord {
+  int group;    // global expert id
+  int a_row;    // first row of the 128-row m-block in the grouped row space
+  int n0;       // first output column
+  int valid;    // rows of this m-block that carry real (token, expert) pairs
+};
+
+struct GroupedSched {
+  const int32_t* glist;   // [G] expert ids of this precision class
+  const int32_t* prefix;  // [G+1] exclusive prefix of m-tiles
+  const int32_t* row_start;
+  const int32_t* row_count;
+  int G;
+  int n_tiles;
+  int BN;
+
+  __device__ __forceinline__ static GroupedSched make(const int32_t* layout, int E, int prec,
+                                                      int N, int BN) {
+    GroupedSched s;
+    s.glist = layout + LayoutView::off_glist(E, prec);
+    s.prefix = layout + LayoutView::off_prefix(E, prec);
+    s.row_start = layout + LayoutView::off_row_start(E);
+    s.row_count = layout + LayoutView::off_row_count(E);
+    s.G = layout[1 + prec];
+    s.n_tiles = N / BN;
+    s.BN = BN;
+    return s;
+  }
+  __device__ __forceinline__ int total() const { return G > 0 ? prefix[G] * n_tiles : 0; }
+  __device__ __forceinline__ TileCoord coord(int t) const {
+    const int mt = t / n_tiles, nt = t - mt * n_tiles;
+    // largest g with prefix[g] <= mt (groups with zero tiles are skipped naturally)
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= mt) lo = mid; else hi = mid - 1;
+    }
+    TileCoord c;
+    c.group = glist[lo];
+    const int local = mt - prefix[lo];
+    c.a_row = row_start[c.group] + local * 128;
+    c.n0 = nt * BN;
+    const int rem = row_count[c.group] - local * 128;
+    c.valid = rem < 128 ? rem : 128;
+    return c;
+  }
+};
+
+}  // namespace realb

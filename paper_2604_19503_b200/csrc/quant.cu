@@ -44,6 +44,55 @@ __device__ __forceinline__ void flag_nonfinite(int32_t* flag) {
   if (flag) atomicOr(flag, 1);
 }
 
+// bf16 product path: both halves' loads are issued before any compute (2 x 32 B
+// in flight per thread), then the cvt-based fast block rule.
+template <int LAYOUT>
+__global__ void __launch_bounds__(256) quant_kernel_bf16(const __nv_bfloat16* __restrict__ x,
+                                                          int64_t rows, int64_t cols,
+                                                          uint8_t* __restrict__ codes,
+                                                          uint8_t* __restrict__ sf, int32_t* flag) {
+  const int64_t nkb = cols >> 4;
+  const int64_t tiles_k = (nkb + 3) >> 2;
+  const int64_t tiles = ((rows + 127) >> 7) * tiles_k;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t tm = tile / tiles_k, tk = tile - tm * tiles_k;
+    uint32_t w[2][8];
+    bool ok[2];
+    int64_t rr[2], kk[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int b = threadIdx.x + h * 256;
+      rr[h] = tm * 128 + (b >> 2);
+      kk[h] = tk * 4 + (b & 3);
+      ok[h] = rr[h] < rows && kk[h] < nkb;
+      if (ok[h]) {
+        const uint4* q = reinterpret_cast<const uint4*>(x + rr[h] * cols + kk[h] * 16);
+        const uint4 a = __ldg(q), c = __ldg(q + 1);
+        w[h][0] = a.x; w[h][1] = a.y; w[h][2] = a.z; w[h][3] = a.w;
+        w[h][4] = c.x; w[h][5] = c.y; w[h][6] = c.z; w[h][7] = c.w;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!ok[h]) continue;
+      // non-finite bf16: exponent field all ones
+      uint32_t nf = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t e = w[h][i] & 0x7F807F80u;
+        nf |= ((e & 0xFFFFu) == 0x7F80u) | ((e >> 16) == 0x7F80u);
+      }
+      if (nf) flag_nonfinite(flag);
+      uint32_t sbits;
+      const uint2 c = quant_block16_bf16(w[h], sbits);
+      *reinterpret_cast<uint2*>(codes + rr[h] * (cols >> 1) + kk[h] * 8) = c;
+      const int64_t so =
+          LAYOUT == REALB_SF_FLAT ? rr[h] * nkb + kk[h] : sf_mma_offset(rr[h], kk[h], nkb);
+      sf[so] = (uint8_t)sbits;
+    }
+  }
+}
+
 template <typename T, int LAYOUT>
 __global__ void __launch_bounds__(256) quant_kernel(const T* __restrict__ x, int64_t rows,
                                                      int64_t cols, uint8_t* __restrict__ codes,
@@ -160,10 +209,10 @@ extern "C" int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, in
   const bool flat = sf_layout == REALB_SF_FLAT;
   switch (dtype) {
     case REALB_DT_BF16:
-      return flat ? launch_quant(quant_kernel<__nv_bfloat16, REALB_SF_FLAT>, d_x, rows, cols,
-                                 d_codes, d_sf, d_flag, max_ctas, st)
-                  : launch_quant(quant_kernel<__nv_bfloat16, REALB_SF_MMA128x4>, d_x, rows, cols,
-                                 d_codes, d_sf, d_flag, max_ctas, st);
+      return flat ? launch_quant(quant_kernel_bf16<REALB_SF_FLAT>, d_x, rows, cols, d_codes,
+                                 d_sf, d_flag, max_ctas, st)
+                  : launch_quant(quant_kernel_bf16<REALB_SF_MMA128x4>, d_x, rows, cols, d_codes,
+                                 d_sf, d_flag, max_ctas, st);
     case REALB_DT_F32:
       return flat ? launch_quant(quant_kernel<float, REALB_SF_FLAT>, d_x, rows, cols, d_codes,
                                  d_sf, d_flag, max_ctas, st)

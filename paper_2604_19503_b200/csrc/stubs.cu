@@ -6,6 +6,5 @@ extern "C" int realb_router_topk_stats(const void*, const void*, const float*, c
 extern "C" int64_t realb_layout_words(int E, int nchunks) { return LayoutView::words(E, nchunks); }
 extern "C" int realb_moe_align(const int32_t*, int, int, const uint8_t*, int32_t*, int32_t*, void*) STUB(realb_moe_align)
 extern "C" int realb_dispatch_permute(const void*, const int32_t*, int, int, int, int, const uint8_t*, const int32_t*, int, int64_t, int32_t*, void*, uint8_t*, uint8_t*, int32_t*, void*) STUB(realb_dispatch_permute)
-extern "C" int realb_grouped_gemm_bf16(const void*, const void*, int64_t, int, int, int, const int32_t*, int, int, void*, int, void*) STUB(realb_grouped_gemm_bf16)
 extern "C" int realb_grouped_gemm_nvfp4(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int64_t, int, int, int, const int32_t*, int, void*, uint8_t*, uint8_t*, int, void*) STUB(realb_grouped_gemm_nvfp4)
 extern "C" int realb_combine(const void*, const int32_t*, const float*, int, int, int, void*, void*) STUB(realb_combine)

@@ -1,0 +1,79 @@
+"""K5: grouped BF16 tcgen05 GEMM vs a plain PyTorch fp32 reference."""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import host_layout
+from paper_2604_19503_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def run_bf16(A, W, lay, N, K, E, prec, epi, rows_cap):
+    dev = A.device
+    lay_t = torch.from_numpy(lay).to(dev)
+    NO = N if epi == _lib.EPI_STORE else N // 2
+    out = torch.full((rows_cap, NO), float("nan"), dtype=torch.bfloat16, device=dev)
+    _lib.call("realb_grouped_gemm_bf16", A.data_ptr(), W.data_ptr(), rows_cap, N, K, E,
+              lay_t.data_ptr(), prec, epi, out.data_ptr(), 0, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    return out
+
+
+def ref_rows(A, W, lay, E, N, counts, prec_sel, prec, epi):
+    outs = {}
+    for e in range(E):
+        if prec_sel[e] != prec or counts[e] == 0:
+            continue
+        rs = int(lay[8 + e])
+        a = A[rs:rs + counts[e]].float()
+        y = a @ W[e * N:(e + 1) * N].float().T
+        if epi == _lib.EPI_SWIGLU:
+            nb = N // 256
+            y = y.view(-1, nb, 2, 128)
+            g, u = y[:, :, 0], y[:, :, 1]
+            y = (torch.nn.functional.silu(g) * u).reshape(-1, N // 2)
+        outs[e] = (rs, y)
+    return outs
+
+
+@pytest.mark.parametrize("E,N,K,counts", [
+    (1, 256, 64, [128]),
+    (1, 256, 128, [77]),
+    (4, 512, 2048, [300, 0, 17, 1000]),
+    (8, 2816, 2048, [513, 129, 1, 0, 777, 256, 2048, 90]),   # Kimi gate_up shape
+    (8, 2048, 1408, [513, 129, 1, 0, 777, 256, 2048, 90]),   # Kimi down shape
+])
+@pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_SWIGLU])
+def test_grouped_bf16(E, N, K, counts, epi):
+    torch.manual_seed(E * 31 + N + K)
+    prec_sel = np.zeros(E, np.int64)
+    lay, rows = host_layout(counts, prec_sel)
+    rows_cap = max(rows, 128)
+    A = torch.randn(rows_cap, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(E * N, K, device="cuda") / K**0.5).to(torch.bfloat16)
+    out = run_bf16(A, W, lay, N, K, E, 0, epi, rows_cap)
+    for e, (rs, y) in ref_rows(A, W, lay, E, N, counts, prec_sel, 0, epi).items():
+        got = out[rs:rs + counts[e]].float()
+        err = (got - y).norm() / y.norm().clamp_min(1e-30)
+        assert err < 1e-2, (e, float(err))   # bf16 output rounding ~ 3e-3
+
+
+def test_grouped_bf16_precision_subset():
+    """Only groups of the requested precision class are computed."""
+    E, N, K = 4, 256, 256
+    counts = [200, 300, 100, 50]
+    prec_sel = np.array([0, 1, 0, 1])
+    lay, rows = host_layout(counts, prec_sel)
+    A = torch.randn(rows, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(E * N, K, device="cuda") / 16).to(torch.bfloat16)
+    out = run_bf16(A, W, lay, N, K, E, 1, _lib.EPI_STORE, rows)
+    for e in range(E):
+        rs = int(lay[8 + e])
+        blk = out[rs:rs + counts[e]]
+        if prec_sel[e] == 1:
+            y = A[rs:rs + counts[e]].float() @ W[e * N:(e + 1) * N].float().T
+            assert ((blk.float() - y).norm() / y.norm()) < 1e-2
+        else:
+            assert torch.isnan(blk.float()).all()
