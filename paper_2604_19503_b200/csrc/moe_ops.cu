@@ -1,0 +1,251 @@
+// moe_ops.cu — the data-movement kernels around the expert GEMMs:
+//   realb_moe_align        per-chunk counts -> expert totals (K2 reduction,
+//                          the device form of aggregate_rank_loads' inputs,
+//                          core.py:106-130), 128-row padded grouped row space,
+//                          per-precision group lists and m-tile prefixes
+//   realb_dispatch_permute tokens -> grouped rows (stable: by expert, then
+//                          token, then slot), bf16 copy or on-the-fly NVFP4
+//                          quantisation (K4, reference block rule) per expert
+//   realb_combine          y[t] = sum_j w[t,j] * rows[pos[t,j]]  (C3, local)
+// All three are HBM/latency-bound; none uses atomics on global memory, so the
+// grouped layout and pair positions are deterministic.
+#include "common.cuh"
+#include "fp4_rule.cuh"
+
+namespace realb {
+
+// ----------------------------------------------------------------- align
+__global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ cc, int nchunks,
+                                                    int E, const uint8_t* __restrict__ prec,
+                                                    int32_t* __restrict__ layout,
+                                                    int32_t* __restrict__ expert_vt) {
+  __shared__ int32_t s_cnt[256], s_start[256];
+  const int e = threadIdx.x;
+  if (e < E) {
+    int v = 0, t = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      v += cc[((int64_t)c * E + e) * 2];
+      t += cc[((int64_t)c * E + e) * 2 + 1];
+    }
+    expert_vt[2 * e] = v;
+    expert_vt[2 * e + 1] = t;
+    s_cnt[e] = v + t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < E; ++i) {
+      s_start[i] = run;
+      run += (s_cnt[i] + 127) / 128 * 128;
+    }
+    layout[0] = run;
+    for (int p = 0; p < 2; ++p) {
+      int32_t* gl = layout + LayoutView::off_glist(E, p);
+      int32_t* pf = layout + LayoutView::off_prefix(E, p);
+      int g = 0, mt = 0;
+      for (int i = 0; i < E; ++i) {
+        if ((int)prec[i] != p) continue;
+        gl[g] = i;
+        pf[g] = mt;
+        mt += (s_cnt[i] + 127) / 128;
+        ++g;
+      }
+      pf[g] = mt;
+      layout[1 + p] = g;
+    }
+  }
+  __syncthreads();
+  if (e < E) {
+    layout[LayoutView::off_row_start(E) + e] = s_start[e];
+    layout[LayoutView::off_row_count(E) + e] = s_cnt[e];
+    int32_t* co = layout + LayoutView::off_chunk(E);
+    int run = s_start[e];
+    for (int c = 0; c < nchunks; ++c) {
+      co[(int64_t)c * E + e] = run;
+      run += cc[((int64_t)c * E + e) * 2] + cc[((int64_t)c * E + e) * 2 + 1];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- dispatch
+// One CTA per 128-token chunk (the router's chunking). Pair ranks inside the
+// chunk are computed per warp with __match_any_sync, then offset by a per-warp
+// exclusive prefix: pairs of one expert keep (token, slot) order.
+constexpr int kPermWarps = 8;
+
+__global__ void __launch_bounds__(256) permute_kernel(
+    const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ topk_idx, int T, int H, int E,
+    int k, const uint8_t* __restrict__ prec, const int32_t* __restrict__ layout,
+    int32_t* __restrict__ pair_pos, __nv_bfloat16* __restrict__ a_bf16,
+    uint8_t* __restrict__ a_codes, uint8_t* __restrict__ a_sf, int32_t* flag) {
+  extern __shared__ int32_t sm[];
+  int32_t* s_base = sm;                       // [E]
+  int32_t* s_cnt = s_base + E;                // [kPermWarps][E]
+  int32_t* s_pos = s_cnt + kPermWarps * E;    // [128*k]
+  const int chunk = blockIdx.x;
+  const int t0 = chunk * 128;
+  const int ntok = min(128, T - t0);
+  const int P = ntok * k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* co = layout + LayoutView::off_chunk(E) + (int64_t)chunk * E;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_base[i] = co[i];
+  for (int i = threadIdx.x; i < kPermWarps * E; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+
+  // phase 1: warp-local stable ranks
+  const int seg = (P + kPermWarps - 1) / kPermWarps;
+  const int p_lo = warp * seg, p_hi = min(P, p_lo + seg);
+  for (int p0 = p_lo; p0 < p_hi; p0 += 32) {
+    const int p = p0 + lane;
+    const bool act = p < p_hi;
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (!act) continue;
+    const int e = topk_idx[(int64_t)t0 * k + p];
+    const unsigned grp = __match_any_sync(am, e);
+    const int before = __popc(grp & ((1u << lane) - 1u));
+    const int base = s_cnt[warp * E + e];
+    s_pos[p] = base + before;  // rank within this warp's segment
+    __syncwarp(am);
+    if (before == 0) s_cnt[warp * E + e] = base + __popc(grp);
+    __syncwarp(am);
+  }
+  __syncthreads();
+  // phase 2: exclusive prefix over warps, per expert (+ chunk base)
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    int run = s_base[i];
+    for (int w = 0; w < kPermWarps; ++w) {
+      const int c = s_cnt[w * E + i];
+      s_cnt[w * E + i] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // phase 3: final positions
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    const int e = topk_idx[(int64_t)t0 * k + p];
+    const int pos = s_cnt[(p / seg) * E + e] + s_pos[p];
+    s_pos[p] = pos;
+    pair_pos[(int64_t)t0 * k + p] = pos;
+  }
+  __syncthreads();
+  // phase 4: move rows, one warp per pair
+  const int nkb = H / 16;
+  for (int p = warp; p < P; p += kPermWarps) {
+    const int t = t0 + p / k;
+    const int e = topk_idx[(int64_t)t0 * k + p];
+    const int64_t pos = s_pos[p];
+    const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
+    if (prec[e] == REALB_PREC_W16A16) {
+      uint4* dst = reinterpret_cast<uint4*>(a_bf16 + pos * H);
+      for (int i = lane; i < H / 8; i += 32) dst[i] = __ldg(src + i);
+    } else {
+      // lane handles 4 consecutive 16-blocks = one 32-bit word of the SF atom
+      for (int g = lane; g < nkb / 4; g += 32) {
+        uint32_t sfw = 0;
+        uint2 cw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint4 u0 = __ldg(src + (g * 4 + b) * 2), u1 = __ldg(src + (g * 4 + b) * 2 + 1);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          uint32_t nf = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t ex = w[i] & 0x7F807F80u;
+            nf |= ((ex & 0xFFFFu) == 0x7F80u) | ((ex >> 16) == 0x7F80u);
+          }
+          if (nf && flag) atomicOr(flag, 1);
+          uint32_t sb;
+          cw[b] = quant_block16_bf16(w, sb);
+          sfw |= sb << (8 * b);
+        }
+        uint4* cdst = reinterpret_cast<uint4*>(a_codes + pos * (H / 2) + g * 32);
+        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
+        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
+        *reinterpret_cast<uint32_t*>(a_sf + sf_mma_offset(pos, (int64_t)g * 4, nkb)) = sfw;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- combine
+__global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ rows,
+                                                      const int32_t* __restrict__ pos,
+                                                      const float* __restrict__ w, int T, int H,
+                                                      int k, __nv_bfloat16* __restrict__ y) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  int64_t p[8];
+  float wt[8];
+  for (int j = 0; j < k; ++j) {
+    p[j] = pos[(int64_t)t * k + j];
+    wt[j] = w[(int64_t)t * k + j];
+  }
+  for (int c = lane; c < H / 8; c += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(rows + p[j] * H) + c);
+      const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] = fmaf(wt[j], bf16lo(v[i]), acc[2 * i]);
+        acc[2 * i + 1] = fmaf(wt[j], bf16hi(v[i]), acc[2 * i + 1]);
+      }
+    }
+    reinterpret_cast<uint4*>(y + (int64_t)t * H)[c] =
+        make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                   pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+  }
+}
+
+}  // namespace realb
+
+using namespace realb;
+
+extern "C" int64_t realb_layout_words(int E, int nchunks) {
+  if (E < 1 || nchunks < 0) return REALB_EINVAL;
+  return LayoutView::words(E, nchunks);
+}
+
+extern "C" int realb_moe_align(const int32_t* d_cc, int nchunks, int E, const uint8_t* d_prec,
+                               int32_t* d_layout, int32_t* d_expert_vt, void* stream) {
+  if (!d_cc || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 || nchunks < 0) {
+    set_error("realb_moe_align: bad arguments (E=%d nchunks=%d; E <= 256)", E, nchunks);
+    return REALB_EINVAL;
+  }
+  align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
+                                                    d_expert_vt);
+  return check_launch("realb_moe_align");
+}
+
+extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx, int T, int H,
+                                      int E, int k, const uint8_t* d_prec,
+                                      const int32_t* d_layout, int nchunks, int64_t rows_cap,
+                                      int32_t* d_pair_pos, void* d_a_bf16, uint8_t* d_a_codes,
+                                      uint8_t* d_a_sf, int32_t* d_flag, void* stream) {
+  if (!d_x || !d_topk_idx || !d_prec || !d_layout || !d_pair_pos || !d_a_bf16 || T < 0 ||
+      H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || nchunks != (T + 127) / 128) {
+    set_error("realb_dispatch_permute: bad arguments (T=%d H=%d E=%d k=%d nchunks=%d)", T, H, E,
+              k, nchunks);
+    return REALB_EINVAL;
+  }
+  if (T == 0) return REALB_OK;
+  const int smem = (E + kPermWarps * E + 128 * k) * 4;
+  permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, T, H, E, k, d_prec, d_layout,
+      d_pair_pos, reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag);
+  return check_launch("realb_dispatch_permute");
+}
+
+extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const float* d_w, int T,
+                             int H, int k, void* d_y, void* stream) {
+  if (!d_rows || !d_pos || !d_w || !d_y || T < 0 || H <= 0 || H % 8 || k < 1 || k > 8) {
+    set_error("realb_combine: bad arguments (T=%d H=%d k=%d)", T, H, k);
+    return REALB_EINVAL;
+  }
+  if (T == 0) return REALB_OK;
+  combine_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_rows), d_pos, d_w, T, H, k,
+      reinterpret_cast<__nv_bfloat16*>(d_y));
+  return check_launch("realb_combine");
+}

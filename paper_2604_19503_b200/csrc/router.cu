@@ -1,0 +1,257 @@
+// router.cu — K1 + K2: gating GEMM, top-k selection, routing weights and
+// per-chunk (vision, text) pair statistics in ONE kernel.
+//
+// One CTA per 128-token chunk. logits[128, E] = X[128, H] . Wg[E, H]^T runs on
+// tcgen05 (kind::f16, M=128, N=E padded to 16) with TMA-fed smem stages; the
+// epilogue thread that owns token row r streams its E fp32 logits out of TMEM
+// (tcgen05.ld 32x32b) and performs, in registers:
+//   - write logits[r, :]                (the D1 contract selects on these)
+//   - top-k on s = logit + bias, strict ">" insertion in expert order, i.e.
+//     descending score with ties to the lowest expert id (the reference's only
+//     top-k convention, balancers.py:161-165)
+//   - routing weights per scoring family
+//   - (vision, text) counts of its k pairs into a shared-memory histogram
+// and the chunk histogram is written once, without global atomics, to
+// chunk_counts[c][E][2] (deterministic; summed by realb_moe_align).
+// Roofline: HBM-bound (2H bytes/token read, E <= 256 < ridge), DESIGN.md §K1.
+#include "common.cuh"
+
+namespace realb {
+
+constexpr int kRBK = 64;
+constexpr int kRStages = 4;
+constexpr int kKMax = 8;
+
+template <int EPAD>
+struct RouterSmem {
+  static constexpr int A_BYTES = 128 * kRBK * 2;
+  static constexpr int B_BYTES = EPAD * kRBK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int HIST_OFF = kRStages * STAGE;
+  static constexpr int BAR_OFF = HIST_OFF + 256 * 2 * 4;
+  static constexpr int TOTAL = BAR_OFF + 128 + 1024;
+  static constexpr uint32_t TMEM_COLS = EPAD <= 32 ? 32 : EPAD <= 64 ? 64 : EPAD <= 128 ? 128 : 256;
+};
+
+template <int EPAD, int KK>
+__global__ void __launch_bounds__(256, 1)
+    router_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                  const float* __restrict__ bias, const uint8_t* __restrict__ modality, int T,
+                  int H, int E, int scoring, float routed_scaling, float norm_min,
+                  float* __restrict__ logits, int32_t* __restrict__ topk_idx,
+                  float* __restrict__ topk_w, int32_t* __restrict__ chunk_counts) {
+  using S = RouterSmem<EPAD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  int32_t* hist = reinterpret_cast<int32_t*>(smem + S::HIST_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* empty = full + kRStages;
+  uint64_t* done = empty + kRStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int chunk = blockIdx.x;
+  const int nkb = H / kRBK;
+
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) hist[i] = 0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < kRStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * S::STAGE;
+        mbar_arrive_expect_tx(&full[stage], S::STAGE);
+        tma_load_2d(sa, &tmX, &full[stage], kb * kRBK, chunk * 128);
+        tma_load_2d(sa + S::A_BYTES, &tmW, &full[stage], kb * kRBK, 0);
+        if (++stage == kRStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, EPAD);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + stage * S::STAGE);
+        const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sa + S::A_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < kRBK / 16; ++kk)
+          umma_bf16(tmem_base, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                    (kb | kk) != 0);
+        tc_commit(&empty[stage]);
+        if (++stage == kRStages) { stage = 0; phase ^= 1; }
+      }
+      tc_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int t = chunk * 128 + row;
+    const bool valid = t < T;
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16);
+
+    constexpr int k = KK;
+    float sval[KK], lsel[KK];
+    int sid[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) { sval[j] = -INFINITY; lsel[j] = 0.f; sid[j] = 0; }
+    float run_max = -INFINITY, run_sum = 0.f;  // online softmax over all E logits
+    float* lrow = logits + (int64_t)t * E;
+#pragma unroll 1
+    for (int c0 = 0; c0 < EPAD; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tb + c0, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int e = c0 + i;
+        if (e >= E) break;
+        const float l = __uint_as_float(v[i]);
+        if (valid) lrow[e] = l;
+        const float s = bias ? l + __ldg(bias + e) : l;
+        if (scoring != REALB_SCORE_SIGMOID_RENORM) {
+          const float m = fmaxf(run_max, l);
+          run_sum = run_sum * __expf(run_max - m) + __expf(l - m);
+          run_max = m;
+        }
+        if (s > sval[k - 1]) {  // strict: an equal score keeps the lower expert id
+          bool placed = false;
+#pragma unroll
+          for (int j = KK - 1; j >= 0; --j) {
+            if (placed) continue;
+            if (j > 0 && sval[j - 1] < s) {
+              sval[j] = sval[j - 1]; lsel[j] = lsel[j - 1]; sid[j] = sid[j - 1];
+            } else {
+              sval[j] = s; lsel[j] = l; sid[j] = e; placed = true;
+            }
+          }
+        }
+      }
+    }
+    // routing weights from the selected logits
+    float w[KK];
+    float wsum = 0.f;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      float p;
+      if (scoring == REALB_SCORE_SIGMOID_RENORM)
+        p = 1.0f / (1.0f + __expf(-lsel[j]));
+      else
+        p = __expf(lsel[j] - run_max) / run_sum;  // softmax probability
+      w[j] = p;
+      wsum += p;
+    }
+    float scale;
+    if (scoring == REALB_SCORE_SOFTMAX_RENORM) scale = 1.0f / wsum;
+    else if (scoring == REALB_SCORE_SIGMOID_RENORM) scale = routed_scaling / wsum;
+    else scale = 1.0f / fmaxf(wsum, norm_min);
+    if (valid) {
+      const int vis = modality[t] ? 0 : 1;  // hist[e][0] vision, [e][1] text
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        topk_idx[(int64_t)t * k + j] = sid[j];
+        topk_w[(int64_t)t * k + j] = w[j] * scale;
+        atomicAdd(&hist[2 * sid[j] + vis], 1);
+      }
+    }
+    tc_fence_before();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    int32_t* out = chunk_counts + (int64_t)chunk * E * 2;
+    for (int i = row; i < 2 * E; i += 128) out[i] = hist[i];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<S::TMEM_COLS>(tmem_base);
+}
+
+template <int EPAD, int KK>
+static int launch_router(const void* x, const void* wg, const float* bias, const uint8_t* mod,
+                         int T, int H, int E, int k, int scoring, float rs, float nm, float* logits,
+                         int32_t* idx, float* w, int32_t* cc, cudaStream_t st) {
+  CUtensorMap tx, tw;
+  int rc = make_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, H, T, (uint64_t)H * 2, kRBK, 128,
+                        CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, wg, H, E, (uint64_t)H * 2, kRBK, EPAD,
+                    CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  auto kern = router_kernel<EPAD, KK>;
+  const int smem = RouterSmem<EPAD>::TOTAL;
+  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                   "router smem attribute");
+  if (rc) return rc;
+  const int grid = (T + 127) / 128;
+  kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc);
+  return check_launch("realb_router_topk_stats");
+}
+
+}  // namespace realb
+
+using namespace realb;
+
+extern "C" int realb_router_topk_stats(const void* d_x, const void* d_wg, const float* d_bias,
+                                       const uint8_t* d_modality, int T, int H, int E, int k,
+                                       int scoring, float routed_scaling, float norm_min,
+                                       float* d_logits, int32_t* d_topk_idx, float* d_topk_w,
+                                       int32_t* d_chunk_counts, void* stream) {
+  if (!d_x || !d_wg || !d_modality || !d_logits || !d_topk_idx || !d_topk_w || !d_chunk_counts ||
+      T < 0 || E < 1 || E > 256 || k < 1 || k > kKMax || k > E || H <= 0 || scoring < 0 ||
+      scoring > 2) {
+    set_error("realb_router_topk_stats: bad arguments (T=%d H=%d E=%d k=%d scoring=%d)", T, H, E,
+              k, scoring);
+    return REALB_EINVAL;
+  }
+  if (H % kRBK) {
+    set_error("realb_router_topk_stats: H must be a multiple of 64 (H=%d)", H);
+    return REALB_EUNSUPPORTED;
+  }
+  if (T == 0) return REALB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int epad = (E + 15) / 16 * 16;
+  if (k != 1 && k != 2 && k != 4 && k != 6 && k != 8) {
+    set_error("realb_router_topk_stats: top-k must be one of 1,2,4,6,8 (k=%d)", k);
+    return REALB_EUNSUPPORTED;
+  }
+#define REALB_ROUTER_K(P, KK)                                                                      \
+  if (k == KK)                                                                                     \
+    return launch_router<P, KK>(d_x, d_wg, d_bias, d_modality, T, H, E, k, scoring, routed_scaling, \
+                                norm_min, d_logits, d_topk_idx, d_topk_w, d_chunk_counts, st);
+#define REALB_ROUTER_CASE(P) \
+  if (epad <= P) {           \
+    REALB_ROUTER_K(P, 1)     \
+    REALB_ROUTER_K(P, 2)     \
+    REALB_ROUTER_K(P, 4)     \
+    REALB_ROUTER_K(P, 6)     \
+    REALB_ROUTER_K(P, 8)     \
+  }
+  REALB_ROUTER_CASE(16)
+  REALB_ROUTER_CASE(64)
+  REALB_ROUTER_CASE(128)
+  REALB_ROUTER_CASE(256)
+#undef REALB_ROUTER_CASE
+#undef REALB_ROUTER_K
+  return REALB_EUNSUPPORTED;
+}

@@ -1,0 +1,332 @@
+"""One ReaLB MoE layer on one GPU (one EP rank, or all ranks of a 1-GPU run).
+
+This module takes the slot of ``moesim.engine.simulate_layer`` (engine.py:120-159):
+instead of evaluating cost formulas it executes the layer with the sm_100a
+kernels of the C-ABI library and reports the same per-rank phase schema
+(``RankPhases``/``LayerTiming``, engine.py:55-86) filled from CUDA events.
+
+Per layer:
+  K1+K2 router_topk_stats            main stream   logits, top-k, (v,t) chunk counts
+  align                              main stream   expert totals + grouped row space
+  policy  plan_realb on the host     one 1-KB D2H  (policy.py; balancers.py:89-122)
+  K3 quantise W4A4 experts' weights  SIDE stream   overlapped with dispatch
+  dispatch_permute (+K4 act quant)   main stream
+  K5 / K6 grouped GEMMs (+SwiGLU)    main stream   (K6 waits on the side stream)
+  combine                            main stream
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .policy import (ClusterConfig, Precision, PrecisionPlan, RealbParams, place_experts_static,
+                     plan_baseline, plan_for, rank_loads_from_counts)
+
+
+# ----------------------------------------------------------------- shapes
+@dataclass(frozen=True)
+class MoEShape:
+    """MoE-layer shape of a model family (SURVEY.md §8 config shorthand)."""
+
+    name: str
+    num_experts: int
+    top_k: int
+    hidden: int
+    intermediate: int
+    scoring: int
+    routed_scaling: float = 1.0
+    norm_min: float = 1e-12
+    modality_isolated: bool = False
+
+
+SHAPES = {
+    # 8 experts top-2, H=512 (BASELINE.json configs[0]); I=1024 recorded choice
+    "tiny": MoEShape("tiny-mmoe", 8, 2, 512, 1024, _lib.SCORE_SOFTMAX_RENORM),
+    # Kimi-VL-A3B (DeepSeek-V3 family router: sigmoid, renorm, x routed_scaling)
+    "kimi": MoEShape("kimi-vl-a3b", 64, 6, 2048, 1408, _lib.SCORE_SIGMOID_RENORM, 2.446),
+    # Qwen3-VL-30B-A3B (softmax, top-k, renorm)
+    "qwen": MoEShape("qwen3-vl-30b-a3b", 128, 8, 2048, 768, _lib.SCORE_SOFTMAX_RENORM),
+    # ERNIE-4.5-VL-A3B modality-split MoE: vision group (ReaLB applies, isolated)
+    "ernie_vision": MoEShape("ernie-4.5-vl-a3b-vision", 64, 6, 2560, 512,
+                             _lib.SCORE_SOFTMAX_CLAMPNORM, modality_isolated=True),
+    "ernie_text": MoEShape("ernie-4.5-vl-a3b-text", 64, 6, 2560, 1536, _lib.SCORE_SOFTMAX_CLAMPNORM),
+}
+
+
+# ----------------------------------------------------------------- timing schema
+class PipelineMode(enum.Enum):
+    SEQUENTIAL = "sequential"
+    OVERLAPPED = "overlapped"
+
+
+@dataclass(frozen=True)
+class RankPhases:
+    """Per-rank phase times in ns (engine.py:55-76), here measured with CUDA events."""
+
+    schedule_ns: int
+    transform_ns: int
+    dispatch_ns: int
+    compute_ns: int
+    combine_ns: int
+
+    def total(self, mode: PipelineMode, accelerated: bool) -> int:
+        if mode is PipelineMode.OVERLAPPED and accelerated:
+            return max(self.dispatch_ns, self.schedule_ns + self.transform_ns) + self.compute_ns + self.combine_ns
+        return self.schedule_ns + self.transform_ns + self.dispatch_ns + self.compute_ns + self.combine_ns
+
+
+@dataclass(frozen=True)
+class LayerTiming:
+    per_rank: tuple[RankPhases, ...]
+    per_rank_total_ns: tuple[int, ...]
+    layer_latency_ns: int
+    compute_only_ns: int
+    critical_rank: int
+    pipeline_mode: PipelineMode
+
+
+# ----------------------------------------------------------------- weights
+@dataclass
+class MoEWeights:
+    """Layer weights on the device in kernel layout.
+
+    router   bf16 [E, H]
+    bias     fp32 [E] selection bias (e_score_correction_bias) or None
+    w_gu     bf16 [E*2I, H]: per expert, gate/up rows interleaved in 128-row
+             halves (block b: gate[128b:128b+128], up[128b:128b+128]) so the
+             SwiGLU epilogue sees gate and up of the same outputs in one tile
+             (D4)
+    w_d      bf16 [E*H, I]
+    """
+
+    shape: MoEShape
+    router: torch.Tensor
+    bias: torch.Tensor | None
+    w_gu: torch.Tensor
+    w_d: torch.Tensor
+
+    @staticmethod
+    def interleave_gate_up(gate_up_hf: torch.Tensor) -> torch.Tensor:
+        """HF layout gate_up_proj [E, 2I, H] (gate rows first) -> kernel layout [E*2I, H]."""
+        E, I2, H = gate_up_hf.shape
+        I = I2 // 2
+        g = gate_up_hf[:, :I].reshape(E, I // 128, 128, H)
+        u = gate_up_hf[:, I:].reshape(E, I // 128, 128, H)
+        return torch.stack([g, u], dim=2).reshape(E * I2, H).contiguous()
+
+    @classmethod
+    def from_hf(cls, shape: MoEShape, router, gate_up_proj, down_proj, bias=None, device="cuda"):
+        """router [E,H], gate_up_proj [E,2I,H], down_proj [E,H,I] (HF conventions)."""
+        E, H, I = shape.num_experts, shape.hidden, shape.intermediate
+        assert tuple(gate_up_proj.shape) == (E, 2 * I, H) and tuple(down_proj.shape) == (E, H, I)
+        bf = torch.bfloat16
+        return cls(
+            shape=shape,
+            router=router.to(device=device, dtype=bf).contiguous(),
+            bias=None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous(),
+            w_gu=cls.interleave_gate_up(gate_up_proj.to(device=device, dtype=bf)),
+            w_d=down_proj.to(device=device, dtype=bf).reshape(E * H, I).contiguous(),
+        )
+
+
+# ----------------------------------------------------------------- the layer
+@dataclass
+class LayerResult:
+    y: torch.Tensor
+    plan: PrecisionPlan
+    expert_vt: np.ndarray
+    timing: LayerTiming | None = None
+    events: dict = field(default_factory=dict)
+
+
+class MoELayer:
+    """Executes one MoE layer for ``T`` local tokens with preallocated workspaces.
+
+    ``cluster`` describes the EP topology the precision plan is computed over. On
+    one GPU ``cluster.num_ranks`` may exceed 1 ("virtual EP": all experts are local,
+    the plan is evaluated per group of experts_per_rank experts exactly as the
+    reference would for that many ranks); with R = 1 the plan is never active
+    (balancers.py:103-104).
+    """
+
+    def __init__(self, weights: MoEWeights, max_tokens: int, cluster: ClusterConfig | None = None,
+                 device="cuda", quant_max_ctas: int = 0, timing: bool = False):
+        s = weights.shape
+        self.w, self.shape = weights, s
+        self.E, self.k, self.H, self.I = s.num_experts, s.top_k, s.hidden, s.intermediate
+        if self.I % 128 or self.H % 256 or (2 * self.I) % 256:
+            raise ValueError("shape must satisfy I % 128 == 0 and H % 256 == 0")
+        self.cluster = cluster or ClusterConfig(1, 1, self.E, 1, s.modality_isolated)
+        if self.cluster.total_experts != self.E:
+            raise ValueError("cluster.total_experts must equal the number of experts")
+        self.placement = place_experts_static(self.cluster)
+        self.max_tokens = max_tokens
+        self.device = torch.device(device)
+        self.quant_max_ctas = quant_max_ctas
+        self.timing = timing
+        E, k, H, I = self.E, self.k, self.H, self.I
+        T = max_tokens
+        self.nchunks_max = (T + 127) // 128
+        self.rows_cap = ((T * k + E * 127) + 127) // 128 * 128
+        dev, bf, u8, i32, f32 = self.device, torch.bfloat16, torch.uint8, torch.int32, torch.float32
+        self.logits = torch.empty(T, E, dtype=f32, device=dev)
+        self.topk_idx = torch.empty(T, k, dtype=i32, device=dev)
+        self.topk_w = torch.empty(T, k, dtype=f32, device=dev)
+        self.chunk_counts = torch.empty(self.nchunks_max, E, 2, dtype=i32, device=dev)
+        self.layout = torch.zeros(int(_lib.load().realb_layout_words(E, self.nchunks_max)), dtype=i32, device=dev)
+        self.expert_vt = torch.empty(E, 2, dtype=i32, device=dev)
+        self.expert_vt_host = torch.empty(E, 2, dtype=i32, pin_memory=True)
+        self.pair_pos = torch.empty(T, k, dtype=i32, device=dev)
+        self.prec_dev = torch.zeros(E, dtype=u8, device=dev)
+        self.prec_host = torch.zeros(E, dtype=u8, pin_memory=True)
+        R = self.rows_cap
+        self.a_bf16 = torch.empty(R, H, dtype=bf, device=dev)
+        self.h_bf16 = torch.empty(R, I, dtype=bf, device=dev)
+        self.rows_out = torch.empty(R, H, dtype=bf, device=dev)
+        self.flag = torch.zeros(1, dtype=i32, device=dev)
+        self._fp4 = None  # lazily allocated W4A4 workspaces
+        self.side = torch.cuda.Stream(device=dev, priority=0)
+
+    # -- W4A4 workspaces (activations + quantised weights of every expert)
+    def _fp4_ws(self):
+        if self._fp4 is None:
+            E, H, I, R = self.E, self.H, self.I, self.rows_cap
+            dev, u8 = self.device, torch.uint8
+            self._fp4 = dict(
+                a_codes=torch.empty(R, H // 2, dtype=u8, device=dev),
+                a_sf=torch.empty(R * H // 16, dtype=u8, device=dev),
+                h_codes=torch.empty(R, I // 2, dtype=u8, device=dev),
+                h_sf=torch.empty(R * I // 16, dtype=u8, device=dev),
+                wgu_codes=torch.empty(E * 2 * I, H // 2, dtype=u8, device=dev),
+                wgu_sf=torch.empty(E * 2 * I * H // 16, dtype=u8, device=dev),
+                wd_codes=torch.empty(E * H, I // 2, dtype=u8, device=dev),
+                wd_sf=torch.empty(E * H * I // 16, dtype=u8, device=dev),
+            )
+        return self._fp4
+
+    def quantize_experts(self, experts, stream=None):
+        """K3: quantise the listed experts' BF16 weights into the W4A4 workspace
+        (contiguous runs of experts become one launch each)."""
+        ws = self._fp4_ws()
+        E, H, I = self.E, self.H, self.I
+        sp = _lib.stream_ptr(stream)
+        runs = []
+        for e in sorted(experts):
+            if runs and runs[-1][1] == e:
+                runs[-1][1] = e + 1
+            else:
+                runs.append([e, e + 1])
+        for lo, hi in runs:
+            r0, r1 = lo * 2 * I, hi * 2 * I
+            _lib.call("realb_quantize_nvfp4", self.w.w_gu[r0:r1].data_ptr(), _lib.DT_BF16, r1 - r0, H,
+                      ws["wgu_codes"][r0:r1].data_ptr(), ws["wgu_sf"][r0 * H // 16:].data_ptr(),
+                      _lib.SF_MMA128x4, self.flag.data_ptr(), self.quant_max_ctas, sp)
+            d0, d1 = lo * H, hi * H
+            _lib.call("realb_quantize_nvfp4", self.w.w_d[d0:d1].data_ptr(), _lib.DT_BF16, d1 - d0, I,
+                      ws["wd_codes"][d0:d1].data_ptr(), ws["wd_sf"][d0 * I // 16:].data_ptr(),
+                      _lib.SF_MMA128x4, self.flag.data_ptr(), self.quant_max_ctas, sp)
+
+    # -- individual device steps (all on the current stream)
+    def route(self, x: torch.Tensor, modality: torch.Tensor):
+        T = x.shape[0]
+        s = self.shape
+        _lib.call("realb_router_topk_stats", x.data_ptr(), self.w.router.data_ptr(),
+                  _lib.ptr(self.w.bias), modality.data_ptr(), T, self.H, self.E, self.k, s.scoring,
+                  float(s.routed_scaling), float(s.norm_min), self.logits.data_ptr(),
+                  self.topk_idx.data_ptr(), self.topk_w.data_ptr(), self.chunk_counts.data_ptr(),
+                  _lib.stream_ptr())
+
+    def align(self, T: int):
+        _lib.call("realb_moe_align", self.chunk_counts.data_ptr(), (T + 127) // 128, self.E,
+                  self.prec_dev.data_ptr(), self.layout.data_ptr(), self.expert_vt.data_ptr(),
+                  _lib.stream_ptr())
+
+    def plan(self, strategy: str, params: RealbParams | None) -> PrecisionPlan:
+        """D2H of the [E,2] counts (one small sync) then the reference policy."""
+        self.expert_vt_host.copy_(self.expert_vt, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loads = rank_loads_from_counts(self.expert_vt_host.numpy(), self.cluster)
+        return plan_for(strategy, loads, self.cluster, params)
+
+    def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
+                params: RealbParams | None = None, plan: PrecisionPlan | None = None) -> LayerResult:
+        T = x.shape[0]
+        if T > self.max_tokens:
+            raise ValueError("more tokens than the layer was sized for")
+        E, k, H, I = self.E, self.k, self.H, self.I
+        nch = (T + 127) // 128
+        main = torch.cuda.current_stream()
+        ev = {n: torch.cuda.Event(enable_timing=True) for n in
+              ("start", "routed", "planned", "dispatched", "computed", "end", "q0", "q1")} if self.timing else {}
+        rec = (lambda n, s=None: ev[n].record(s or main)) if self.timing else (lambda n, s=None: None)
+        rec("start")
+        self.route(x, modality)
+        self.prec_dev.zero_()
+        self.align(T)
+        rec("routed")
+        if plan is None:
+            if strategy in ("baseline", "eplb", "async-eplb"):
+                plan = plan_baseline([None] * self.cluster.num_ranks)
+                vt = None
+            else:
+                plan = self.plan(strategy, params)
+                vt = self.expert_vt_host.numpy().copy()
+        else:
+            vt = None
+        prec = plan.expert_precision(self.placement)
+        fp4_experts = np.flatnonzero(prec == _lib.PREC_W4A4)
+        if len(fp4_experts):
+            self.prec_host.numpy()[:] = prec
+            self.prec_dev.copy_(self.prec_host, non_blocking=True)
+            self.align(T)  # rebuild the per-precision group lists
+            ws = self._fp4_ws()
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                rec("q0", self.side)
+                self.quantize_experts(fp4_experts.tolist(), self.side)
+                rec("q1", self.side)
+        rec("planned")
+        ws = self._fp4 if len(fp4_experts) else None
+        _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
+                  self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
+                  self.pair_pos.data_ptr(), self.a_bf16.data_ptr(),
+                  _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
+                  self.flag.data_ptr(), _lib.stream_ptr())
+        rec("dispatched")
+        sp = _lib.stream_ptr()
+        lay = self.layout.data_ptr()
+        if len(fp4_experts) < E:
+            _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
+                      self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                      self.h_bf16.data_ptr(), 0, sp)
+        if ws is not None:
+            main.wait_stream(self.side)
+            _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
+                      ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, E,
+                      lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
+        if len(fp4_experts) < E:
+            _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
+                      self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
+                      self.rows_out.data_ptr(), 0, sp)
+        if ws is not None:
+            _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+                      ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
+                      _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+        rec("computed")
+        y = torch.empty(T, H, dtype=torch.bfloat16, device=x.device)
+        _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
+                  self.topk_w.data_ptr(), T, H, k, y.data_ptr(), sp)
+        rec("end")
+        return LayerResult(y=y, plan=plan, expert_vt=vt, events=ev)
+
+    def check_flag(self):
+        from .quant import QuantizationDomainError
+
+        if int(self.flag.item()):
+            self.flag.zero_()
+            raise QuantizationDomainError("non-finite value reached the NVFP4 quantiser")
