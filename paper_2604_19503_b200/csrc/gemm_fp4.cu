@@ -1,0 +1,312 @@
+// gemm_fp4.cu — K6: grouped NVFP4 x NVFP4 expert GEMM on tcgen05
+// (kind::mxf4nvf4.block_scale.scale_vec::4X: E2M1 operands, one UE4M3 scale
+// per 16 elements along K for both A and W, FP32 accumulation in TMEM).
+//
+// Persistent, warp-specialised, one CTA per SM, 384 threads:
+//   warp 0     TMA producer: A 128x256 and W 256x256 E2M1 tiles (128-B rows,
+//              SWIZZLE_128B) + their scale-factor atoms (cp.async.bulk; the
+//              quantisers write scales directly in the 128x4-atom layout, so a
+//              stage's scales are contiguous 2 KB runs)
+//   warp 1     MMA issuer: tcgen05.cp (smem -> TMEM, 32x128b.warpx4) of the
+//              stage's scale atoms, then 4 x tcgen05.mma (M=128, N=256, K=64)
+//   warp 2     TMEM allocator (512 columns: 256 accumulator + 2 x 48 scale)
+//   warps 4-11 epilogue: the 8 warps copy the whole accumulator into registers
+//              (quadrant = warp % 4, column half = (warp - 4) / 4), release TMEM
+//              to the MMA warp at once, then run SwiGLU (+ NVFP4 re-quantisation
+//              of the bf16 result with the reference block rule, K4 fused) or the
+//              bf16 store from registers while the next tile's mainloop runs.
+// Roofline: tensor-bound at the dense FP4 rate (4x BF16 per MMA cycle).
+#include <cstdlib>
+
+#include "common.cuh"
+#include "fp4_rule.cuh"
+#include "grouped.cuh"
+
+namespace realb {
+
+constexpr int kF4BM = 128, kF4BN = 256;
+constexpr int kF4BKB = 128;               // bytes of K per stage = 256 E2M1 values
+constexpr int kF4Stages = 4;
+constexpr int kF4Threads = 384;
+
+struct SmemFp4 {
+  static constexpr int A_BYTES = kF4BM * kF4BKB;    // 16 KB
+  static constexpr int B_BYTES = kF4BN * kF4BKB;    // 32 KB
+  static constexpr int SFA_BYTES = 4 * 512;         // 128 rows x 16 scales
+  static constexpr int SFB_BYTES = 2 * 4 * 512;     // 256 rows x 16 scales
+  static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
+  static constexpr int BAR_OFF = kF4Stages * STAGE;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+constexpr uint32_t kTmemAcc = 0, kTmemSf = 256, kTmemSfStride = 48;
+
+struct Fp4Args {
+  const uint8_t* a_sf;
+  const uint8_t* w_sf;
+  const int32_t* layout;
+  int E, N, K;
+  __nv_bfloat16* out;   // STORE: bf16 [rows][N]
+  uint8_t* out_codes;   // SWIGLU: E2M1 [rows][N/4]
+  uint8_t* out_sf;      // SWIGLU: MMA-layout scales of the [rows][N/2] result
+  uint32_t sf_lbo, sf_sbo;
+};
+
+__device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(lbo >> 4) << 16;
+  d |= (uint64_t)(sbo >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kF4Threads, 1)
+    grouped_gemm_fp4_kernel(const __grid_constant__ CUtensorMap tmA,
+                            const __grid_constant__ CUtensorMap tmB, const Fp4Args args) {
+  using S = SmemFp4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* empty = full + kF4Stages;
+  uint64_t* tfull = empty + kF4Stages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int N = args.N, K = args.K;
+  const GroupedSched sched = GroupedSched::make(args.layout, args.E, REALB_PREC_W4A4, N, kF4BN);
+  const int total = sched.total();
+  const int kbytes = K / 2;
+  const int nkb = (kbytes + kF4BKB - 1) / kF4BKB;
+  const int atoms_per_row_tile = K / 64;  // 4-scale atoms per 128-row tile
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kF4Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord c = sched.coord(t);
+        const int brow = c.group * N + c.n0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int kval = min(kF4BKB, kbytes - kb * kF4BKB);  // bytes of K in this stage
+          const int nmma = kval / 32;
+          const uint32_t sfbytes = (uint32_t)nmma * 512;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::STAGE;
+          uint8_t* sb = sa + S::A_BYTES;
+          uint8_t* ssfa = sb + S::B_BYTES;
+          uint8_t* ssfb = ssfa + S::SFA_BYTES;
+          mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES + 3 * sfbytes);
+          tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, c.a_row);
+          tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
+          const int64_t atom_k = (int64_t)kb * 4;
+          bulk_load(ssfa, args.a_sf + ((int64_t)(c.a_row >> 7) * atoms_per_row_tile + atom_k) * 512,
+                    sfbytes, &full[stage]);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            bulk_load(ssfb + i * 2048,
+                      args.w_sf + ((int64_t)((brow >> 7) + i) * atoms_per_row_tile + atom_k) * 512,
+                      sfbytes, &full[stage]);
+          if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
+      int stage = 0;
+      uint32_t phase = 0, sfsel = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        mbar_wait(tempty, (it & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int kval = min(kF4BKB, kbytes - kb * kF4BKB);
+          const int nmma = kval / 32;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * S::STAGE);
+          const uint32_t sb = sa + S::A_BYTES, ssfa = sb + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
+          const uint32_t tsf = tmem_base + kTmemSf + sfsel * kTmemSfStride;
+          for (int j = 0; j < nmma; ++j) {
+            utccp_32x128b_warpx4(tsf + 4 * j, sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
+            utccp_32x128b_warpx4(tsf + 16 + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
+            utccp_32x128b_warpx4(tsf + 20 + 8 * j,
+                                 sf_desc(ssfb + 2048 + 512 * j, args.sf_lbo, args.sf_sbo));
+          }
+          const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sb);
+          for (int j = 0; j < nmma; ++j)
+            umma_nvfp4(tmem_base + kTmemAcc, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2),
+                       idesc, tsf + 4 * j, tsf + 16 + 8 * j, (kb | j) != 0);
+          tc_commit(&empty[stage]);
+          sfsel ^= 1;
+          if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(tfull);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (8 warps)
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int row_in_tile = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const TileCoord c = sched.coord(t);
+      mbar_wait(tfull, it & 1);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + kTmemAcc + ((uint32_t)(q * 32) << 16);
+      uint32_t v[4][32];
+      if constexpr (EPI == REALB_EPI_SWIGLU) {
+        tmem_ld32(tb + half * 64, v[0]);
+        tmem_ld32(tb + half * 64 + 32, v[1]);
+        tmem_ld32(tb + 128 + half * 64, v[2]);
+        tmem_ld32(tb + 128 + half * 64 + 32, v[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tmem_ld32(tb + half * 128 + 32 * i, v[i]);
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);  // accumulator free: next mainloop may start
+      const int64_t r = (int64_t)c.a_row + row_in_tile;
+      if constexpr (EPI == REALB_EPI_SWIGLU) {
+        // outputs [n0/2 + half*64, +64): h = bf16(silu(g) * u), then NVFP4
+        const int I = N / 2;
+        const int ocol = c.n0 / 2 + half * 64;
+        uint32_t sfw = 0;
+        uint2 cw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          float h[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = b * 16 + i;  // 0..63
+            const float g = __uint_as_float(v[col >> 5][col & 31]);
+            const float u = __uint_as_float(v[2 + (col >> 5)][col & 31]);
+            h[i] = __bfloat162float(__float2bfloat16_rn(g / (1.0f + __expf(-g)) * u));
+          }
+          uint32_t sb;
+          cw[b] = quant_block16_bf16vals(h, sb);
+          sfw |= sb << (8 * b);
+        }
+        uint4* cdst = reinterpret_cast<uint4*>(args.out_codes + r * (I / 2) + ocol / 2);
+        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
+        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
+        *reinterpret_cast<uint32_t*>(args.out_sf + sf_mma_offset(r, ocol / 16, I / 16)) = sfw;
+      } else {
+        __nv_bfloat16* orow = args.out + r * N + c.n0 + half * 128;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t* p = &v[i][8 * j];
+            st_global_v4(orow + 32 * i + 8 * j,
+                         pack_bf16x2(__uint_as_float(p[0]), __uint_as_float(p[1])),
+                         pack_bf16x2(__uint_as_float(p[2]), __uint_as_float(p[3])),
+                         pack_bf16x2(__uint_as_float(p[4]), __uint_as_float(p[5])),
+                         pack_bf16x2(__uint_as_float(p[6]), __uint_as_float(p[7])));
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+static uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* s = getenv(name);
+  return s ? (uint32_t)strtoul(s, nullptr, 0) : dflt;
+}
+
+template <int EPI>
+static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, const uint8_t* w_sf,
+                      int64_t rows_cap, int N, int K, int E, const int32_t* layout, void* out,
+                      uint8_t* out_codes, uint8_t* out_sf, int max_ctas, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, a, (uint64_t)K / 2, rows_cap,
+                        (uint64_t)K / 2, kF4BKB, kF4BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, (uint64_t)K / 2, (uint64_t)E * N,
+                    (uint64_t)K / 2, kF4BKB, kF4BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  Fp4Args args;
+  args.a_sf = a_sf;
+  args.w_sf = w_sf;
+  args.layout = layout;
+  args.E = E;
+  args.N = N;
+  args.K = K;
+  args.out = reinterpret_cast<__nv_bfloat16*>(out);
+  args.out_codes = out_codes;
+  args.out_sf = out_sf;
+  args.sf_lbo = env_u32("REALB_DBG_SF_LBO", 128);
+  args.sf_sbo = env_u32("REALB_DBG_SF_SBO", 128);
+  auto kern = grouped_gemm_fp4_kernel<EPI>;
+  const int smem = SmemFp4::TOTAL;
+  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                   "grouped_gemm_nvfp4: smem attribute");
+  if (rc) return rc;
+  int grid = num_sms();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  kern<<<grid, kF4Threads, smem, st>>>(ta, tb, args);
+  return check_launch("realb_grouped_gemm_nvfp4");
+}
+
+}  // namespace realb
+
+using namespace realb;
+
+extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t* d_a_sf,
+                                        const uint8_t* d_w_codes, const uint8_t* d_w_sf,
+                                        int64_t rows_cap, int N, int K, int E,
+                                        const int32_t* d_layout, int epilogue, void* d_out,
+                                        uint8_t* d_out_codes, uint8_t* d_out_sf, int max_ctas,
+                                        void* stream) {
+  if (!d_a_codes || !d_a_sf || !d_w_codes || !d_w_sf || !d_layout || rows_cap <= 0 ||
+      rows_cap % 128 || E <= 0) {
+    set_error("realb_grouped_gemm_nvfp4: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (N % kF4BN || K % 64) {
+    set_error("realb_grouped_gemm_nvfp4: needs N %% 256 == 0 and K %% 64 == 0 (N=%d K=%d)", N, K);
+    return REALB_EUNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (epilogue == REALB_EPI_STORE) {
+    if (!d_out) { set_error("realb_grouped_gemm_nvfp4: STORE needs d_out"); return REALB_EINVAL; }
+    return launch_fp4<REALB_EPI_STORE>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
+                                       d_layout, d_out, nullptr, nullptr, max_ctas, st);
+  }
+  if (epilogue == REALB_EPI_SWIGLU) {
+    if (!d_out_codes || !d_out_sf || (N / 2) % 64) {
+      set_error("realb_grouped_gemm_nvfp4: SWIGLU needs d_out_codes/d_out_sf and (N/2) %% 64 == 0");
+      return REALB_EINVAL;
+    }
+    return launch_fp4<REALB_EPI_SWIGLU>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
+                                        d_layout, nullptr, d_out_codes, d_out_sf, max_ctas, st);
+  }
+  set_error("realb_grouped_gemm_nvfp4: unknown epilogue %d", epilogue);
+  return REALB_EINVAL;
+}

@@ -1,0 +1,93 @@
+"""K6: grouped NVFP4 tcgen05 GEMM vs fp32 matmul of the reference-rule
+dequantised operands (the FP4-emulating oracle), and the fused SwiGLU + NVFP4
+re-quantisation epilogue vs the oracle block rule."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from helpers import host_layout
+from paper_2604_19503_b200 import _lib
+from paper_2604_19503_b200.quant import quantize_nvfp4, sf_mma_to_flat, unpack_codes
+
+pytestmark = pytest.mark.gpu
+
+MAGS = np.array([0, 0.5, 1, 1.5, 2, 3, 4, 6, -0.0, -0.5, -1, -1.5, -2, -3, -4, -6], np.float64)
+
+
+def decode_e4m3(b):
+    b = np.asarray(b, np.int64)
+    e, m = b >> 3, b & 7
+    return np.where(e == 0, m * 2.0**-9, (1 + m / 8) * 2.0 ** (e - 7))
+
+
+def dequant(codes_packed, sf_mma, rows, cols):
+    c = unpack_codes(codes_packed.cpu().numpy()).reshape(rows, cols)
+    s = sf_mma_to_flat(sf_mma.cpu().numpy(), rows, cols)
+    return MAGS[c] * np.repeat(decode_e4m3(s), 16, axis=1)
+
+
+def make_problem(E, N, K, counts, seed, a_scale=1.0):
+    torch.manual_seed(seed)
+    lay, rows = host_layout(counts, np.ones(E, np.int64))
+    rows = max(rows, 128)
+    A = (torch.randn(rows, K, device="cuda") * a_scale).to(torch.bfloat16)
+    W = (torch.randn(E * N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    ac, asf = quantize_nvfp4(A)
+    wc, wsf = quantize_nvfp4(W)
+    return lay, rows, A, W, ac, asf, wc, wsf
+
+
+@pytest.mark.parametrize("E,N,K,counts", [
+    (1, 256, 256, [128]),
+    (1, 256, 64, [100]),
+    (3, 512, 2048, [300, 0, 700]),
+    (4, 2048, 1408, [513, 129, 1, 260]),     # Kimi down: K tail (1408 = 5.5 x 256)
+    (4, 2816, 2048, [513, 129, 1, 260]),     # Kimi gate_up
+])
+def test_fp4_store_vs_dequant_oracle(E, N, K, counts):
+    lay, rows, A, W, ac, asf, wc, wsf = make_problem(E, N, K, counts, seed=E + N + K)
+    out = torch.full((rows, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    lt = torch.from_numpy(lay).cuda()
+    _lib.call("realb_grouped_gemm_nvfp4", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(),
+              rows, N, K, E, lt.data_ptr(), _lib.EPI_STORE, out.data_ptr(), None, None, 0, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    Ad = dequant(ac, asf, rows, K)
+    Wd = dequant(wc, wsf, E * N, K)
+    for e in range(E):
+        if counts[e] == 0:
+            continue
+        rs = int(lay[8 + e])
+        ref = Ad[rs:rs + counts[e]] @ Wd[e * N:(e + 1) * N].T
+        got = out[rs:rs + counts[e]].float().cpu().numpy()
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert err < 5e-3, (e, err)  # fp32 accumulation order + bf16 output rounding
+
+
+def test_fp4_swiglu_requant_epilogue():
+    E, N, K, counts = 2, 512, 512, [200, 77]
+    lay, rows, A, W, ac, asf, wc, wsf = make_problem(E, N, K, counts, seed=5, a_scale=4.0)
+    I = N // 2
+    hc = torch.zeros(rows, I // 2, dtype=torch.uint8, device="cuda")
+    hsf = torch.zeros(rows * I // 16, dtype=torch.uint8, device="cuda")
+    lt = torch.from_numpy(lay).cuda()
+    _lib.call("realb_grouped_gemm_nvfp4", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(),
+              rows, N, K, E, lt.data_ptr(), _lib.EPI_SWIGLU, None, hc.data_ptr(), hsf.data_ptr(), 0,
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    Ad = dequant(ac, asf, rows, K)
+    Wd = dequant(wc, wsf, E * N, K)
+    hq = dequant(hc, hsf, rows, I)
+    from oracle.moe_ref import bf16_round, silu
+
+    for e in range(E):
+        rs = int(lay[8 + e])
+        y = Ad[rs:rs + counts[e]] @ Wd[e * N:(e + 1) * N].T          # interleaved halves
+        y = y.reshape(counts[e], N // 256, 2, 128)
+        h = bf16_round((silu(y[:, :, 0]) * y[:, :, 1]).reshape(counts[e], I).astype(np.float32))
+        href = oracle.fake_quant(h)
+        got = hq[rs:rs + counts[e]]
+        err = np.linalg.norm(got - href) / np.linalg.norm(href)
+        assert err < 2e-2, err
+        assert (got == href).mean() > 0.97
