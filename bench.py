@@ -1,0 +1,355 @@
+"""MoE-layer prefill benchmark (BASELINE.json metric): tokens/s of one ReaLB MoE
+layer and its speedup over an all-BF16 EP run of the same kernels.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  (N > 1: launched by torchrun, one rank per GPU, expert parallelism over NCCL)
+
+One step = one full MoE-layer forward (router -> stats -> policy -> [K3 on the
+side stream] -> dispatch -> grouped GEMMs -> combine) over the rank's local
+tokens. Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE-layer prefill tokens/s and speedup vs all-BF16 EP at 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="kimi", choices=["tiny", "kimi", "qwen", "ernie_vision"])
+    p.add_argument("--tokens", type=int, default=8192, help="local tokens per GPU")
+    p.add_argument("--vision-frac", type=float, default=0.7)
+    p.add_argument("--cpu-sample-tokens", type=int, default=256)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-virtual-ep", action="store_true")
+    return p.parse_args()
+
+
+def measured_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- ours
+def build_layer(args, torch, rank=0, world=1):
+    from paper_2604_19503_b200 import _lib
+    from paper_2604_19503_b200.moe import SHAPES, MoELayer, MoEWeights
+    from paper_2604_19503_b200.policy import ClusterConfig
+    from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts
+
+    shape = SHAPES[args.config]
+    spec = WorkloadSpec(tokens=args.tokens, vision_frac=args.vision_frac,
+                        num_ranks=8 if shape.num_experts % 8 == 0 else 1, rank=rank)
+    x, mod, router, _ = make_batch(shape, spec)
+    gu, dn = make_experts(shape)
+    bias = torch.zeros(shape.num_experts, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
+    w = MoEWeights.from_hf(shape, router, gu, dn, bias=bias)
+    del gu, dn
+    cluster = ClusterConfig(world, 1, shape.num_experts // world, 1, shape.modality_isolated)
+    return shape, w, x, mod, cluster
+
+
+def time_steps(torch, fn, steps, warmup, flush):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        flush()  # untimed: L2 flushed between timed steps
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        times.append((s, e))
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in times]
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2604_19503_b200 import _lib
+    from paper_2604_19503_b200.moe import MoELayer
+    from paper_2604_19503_b200.policy import RealbParams
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_2604_19503_b200 import ep
+
+        return ep.run_bench(args)
+    torch.cuda.set_device(0)
+    shape, w, x, mod, cluster = build_layer(args, torch)
+    T = args.tokens
+    layer = MoELayer(w, max_tokens=T, cluster=cluster)
+    params = RealbParams()
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    flush = lambda: flush_buf.zero_()
+
+    # --- headline: ReaLB strategy (R = 1: plan provably inactive for C >= 1)
+    _lib.launch_count = 0
+    with ClockSampler(0) as clk:
+        t_realb = time_steps(torch, lambda: layer.forward(x, mod, "realb", params), args.steps, args.warmup, flush)
+    launches_per_step = _lib.launch_count / (args.steps + args.warmup)
+    t_bf16 = time_steps(torch, lambda: layer.forward(x, mod, "baseline"), args.steps, args.warmup, flush)
+    ms = float(np.mean(t_realb))
+    ms_bf16 = float(np.mean(t_bf16))
+    value = T / (ms / 1e3)
+
+    # --- e2e through the public API with host buffers (H2D of x and modality, D2H of y)
+    xh = x.cpu().pin_memory()
+    mh = mod.cpu().pin_memory()
+    yh = torch.empty(T, shape.hidden, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        xd = xh.to("cuda", non_blocking=True)
+        md = mh.to("cuda", non_blocking=True)
+        r = layer.forward(xd, md, "realb", params)
+        yh.copy_(r.y, non_blocking=True)
+
+    t_e2e = time_steps(torch, e2e_step, args.steps, args.warmup, flush)
+    ms_e2e = float(np.mean(t_e2e))
+
+    # --- roofline of the dominant kernel (K5 gate_up grouped GEMM), events on its stream
+    roof = roofline_gate_up(torch, layer, x, mod, shape, args)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16 (nvfp4 on W4A4 ranks)", "data": "synthetic",
+        "config": {"workload": f"{shape.name} MoE layer prefill, {T} tokens/GPU, {args.vision_frac:.0%} vision, "
+                               f"E={shape.num_experts} top-{shape.top_k} H={shape.hidden} I={shape.intermediate}",
+                   "strategy": "realb", "ep_ranks": 1, "tokens_per_gpu": T,
+                   "l2": "flushed between timed steps (256 MB write, untimed); weights 1.1 GB > L2"},
+        "speedup_vs_bf16": ms_bf16 / ms, "ms_per_step_bf16": ms_bf16,
+        "e2e": {"value": T / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(xh.numel() * 2 + mh.numel()),
+                "d2h_bytes_per_step": int(yh.numel() * 2)},
+        "roofline": roof,
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "clocks": clk.summary(),
+    }
+    if not args.no_virtual_ep:
+        try:
+            from paper_2604_19503_b200.virtual_ep import virtual_ep_report
+
+            out["virtual_ep8"] = virtual_ep_report(args, torch)
+        except Exception as e:  # reported, never silently dropped
+            out["virtual_ep8"] = {"error": repr(e)[:300]}
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, sample=args.cpu_sample_tokens)
+    print(json.dumps(out), flush=True)
+
+
+def roofline_gate_up(torch, layer, x, mod, shape, args):
+    """achieved = algorithmic flops of the K5 gate_up launch (2 * pairs * 2I * H)
+    / its CUDA-event duration on the launching (current) stream."""
+    from paper_2604_19503_b200 import _lib
+
+    peaks, src = measured_peaks()
+    T = x.shape[0]
+    layer.forward(x, mod, "baseline")
+    torch.cuda.synchronize()
+    E, H, I = shape.num_experts, shape.hidden, shape.intermediate
+    pairs = T * shape.top_k
+    sp = _lib.stream_ptr()
+    durs = []
+    for _ in range(max(5, args.steps)):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        _lib.call("realb_grouped_gemm_bf16", layer.a_bf16.data_ptr(), layer.w.w_gu.data_ptr(), layer.rows_cap,
+                  2 * I, H, E, layer.layout.data_ptr(), _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                  layer.h_bf16.data_ptr(), 0, sp)
+        e.record()
+        e.synchronize()
+        durs.append(s.elapsed_time(e))
+    t = sorted(durs)[len(durs) // 2] / 1e3
+    flops = 2.0 * pairs * (2 * I) * H
+    achieved = flops / t / 1e12
+    peak = float(peaks.get("bf16_tflops", 1641.1))
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"gate_up_{args.config}_{T}")
+        except Exception:
+            traffic = None
+    return {"kernel": "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)", "bound": "tensor",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": f"{src} bf16_tflops (burst)",
+            "algorithmic_flops_per_launch": flops, "launch_ms": t * 1e3}
+
+
+# ----------------------------------------------------------------------------- CPU arms
+class CpuOracleArm:
+    """The CPU oracle port of the whole path (oracle/moe_ref.py + the C quantiser),
+    on a bounded token sample of the same workload. Weights are built once."""
+
+    def __init__(self, args, sample: int):
+        import numpy as np
+        import torch
+
+        from paper_2604_19503_b200.moe import SHAPES
+        from paper_2604_19503_b200.policy import ClusterConfig
+        from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts
+
+        self.threads = os.cpu_count() or 1
+        torch.set_num_threads(self.threads)
+        self.shape = shape = SHAPES[args.config]
+        self.sample = sample
+        spec = WorkloadSpec(tokens=sample, vision_frac=args.vision_frac,
+                            num_ranks=8 if shape.num_experts % 8 == 0 else 1)
+        x, mod, router, _ = make_batch(shape, spec, device="cpu")
+        gu, dn = make_experts(shape, device="cpu")
+        self.x, self.mod, self.router = x.float().numpy(), mod.numpy(), router.float().numpy()
+        self.gu, self.dn = gu.float().numpy(), dn.float().numpy()
+        self.wbits = gu[0].contiguous().view(torch.int16).numpy().view(np.uint16)
+        R = max(1, int(os.environ.get("WORLD_SIZE", "1")))
+        self.R = R
+        self.cluster = ClusterConfig(R, 1, shape.num_experts // R, 1, shape.modality_isolated)
+
+    def step(self) -> float:
+        from oracle import moe_ref
+        from paper_2604_19503_b200.policy import RealbParams, place_experts_static, plan_for, \
+            rank_loads_from_counts
+
+        s = self.shape
+        t0 = time.perf_counter()
+        logits, idx, _ = moe_ref.route(self.x, self.router, s.top_k, s.scoring, routed_scaling=s.routed_scaling)
+        vt = moe_ref.expert_counts(idx, self.mod, s.num_experts)
+        plan = plan_for("realb", rank_loads_from_counts(vt, self.cluster), self.cluster, RealbParams())
+        prec = plan.expert_precision(place_experts_static(self.cluster))
+        moe_ref.moe_layer(self.x, self.mod, self.router, self.gu, self.dn, s.top_k, s.scoring,
+                          expert_prec=prec, routed_scaling=s.routed_scaling, logits=logits)
+        return time.perf_counter() - t0
+
+    def quantiser_mbps(self) -> float:
+        import oracle
+
+        t = time.perf_counter()
+        oracle.quantize_bf16(self.wbits)
+        return self.wbits.nbytes / (time.perf_counter() - t) / 1e6
+
+    def describe(self, value: float) -> dict:
+        return {"value": value, "unit": "tokens/s", "cores": self.threads, "kind": "port",
+                "sample": f"{self.sample} tokens of the {self.shape.name} workload through the full CPU oracle "
+                          f"layer (numpy fp32, {self.threads} BLAS threads), plan over R={self.R}"}
+
+
+def cpu_baseline(args, sample: int):
+    arm = CpuOracleArm(args, sample)
+    dt = min(arm.step() for _ in range(2))
+    d = arm.describe(sample / dt)
+    d["quantiser_MBps_bf16_in"] = arm.quantiser_mbps()
+    d["quantiser_cores"] = 1
+    return d
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path. The
+    reference (moesim) is an analytic simulator with no executable MoE layer, so
+    this arm runs the CPU oracle port of it (oracle/), on rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    arm = CpuOracleArm(args, args.cpu_sample_tokens)
+    for _ in range(args.warmup):
+        arm.step()
+    secs = [arm.step() for _ in range(args.steps)]
+    v = args.cpu_sample_tokens / float(np.mean(secs))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"{arm.shape.name} MoE layer prefill (CPU oracle port, bounded sample)",
+                      "tokens_per_step": args.cpu_sample_tokens},
+           "cpu_baseline": arm.describe(v),
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

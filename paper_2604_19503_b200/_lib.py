@@ -59,6 +59,13 @@ SIGNATURES: dict[str, tuple] = {
 
 _lib: C.CDLL | None = None
 
+# entry points that launch exactly one kernel per successful call
+LAUNCHES_KERNEL = {
+    "realb_quantize_nvfp4", "realb_router_topk_stats", "realb_moe_align", "realb_dispatch_permute",
+    "realb_grouped_gemm_bf16", "realb_grouped_gemm_nvfp4", "realb_combine",
+}
+launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
+
 
 def load() -> C.CDLL:
     """Load (once) and type the library. Raises RealbUnavailable if absent."""
@@ -82,10 +89,13 @@ def load() -> C.CDLL:
 
 
 def call(name: str, *args) -> int:
+    global launch_count
     lib = load()
     st = getattr(lib, name)(*args)
     if st < 0:
         raise RealbError(name, st, lib.realb_last_error().decode(errors="replace"))
+    if name in LAUNCHES_KERNEL:
+        launch_count += 1
     return st
 
 

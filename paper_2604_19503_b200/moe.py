@@ -324,6 +324,32 @@ class MoELayer:
         rec("end")
         return LayerResult(y=y, plan=plan, expert_vt=vt, events=ev)
 
+    def expert_compute(self, T: int, prec: np.ndarray) -> None:
+        """Re-run only the expert GEMMs of the experts whose code in ``prec`` is
+        0 (W16A16) or 1 (W4A4); code 2 excludes an expert. Operates on the rows the
+        last forward() dispatched (the codes of included experts must match it).
+        Used to time one (virtual) EP rank's compute in isolation."""
+        E, H, I = self.E, self.H, self.I
+        self.prec_host.numpy()[:] = prec
+        self.prec_dev.copy_(self.prec_host, non_blocking=True)
+        self.align(T)
+        sp, lay = _lib.stream_ptr(), self.layout.data_ptr()
+        if (prec == 0).any():
+            _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
+                      self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                      self.h_bf16.data_ptr(), 0, sp)
+            _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
+                      self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
+                      self.rows_out.data_ptr(), 0, sp)
+        if (prec == 1).any():
+            ws = self._fp4_ws()
+            _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
+                      ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, E,
+                      lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
+            _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+                      ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
+                      _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+
     def check_flag(self):
         from .quant import QuantizationDomainError
 

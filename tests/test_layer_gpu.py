@@ -149,3 +149,35 @@ def test_layer_bf16_vs_oracle(name, E, T):
     y = res.y.float().cpu().numpy()
     err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
     assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("name,E,T,strategy,R", [("tiny", None, 1024, "fp4all", 2),
+                                                  ("kimi", 16, 512, "fp4all", 8),
+                                                  ("kimi", 64, 2048, "realb", 8),
+                                                  ("qwen", 32, 512, "realb", 8)])
+def test_layer_w4a4_vs_oracle(name, E, T, strategy, R):
+    """Mixed-precision layer: W4A4 experts run the NVFP4 path (K3 weights, K4
+    activations + SwiGLU output, K6 GEMMs) and match the FP4-emulating oracle."""
+    shape = small(SHAPES[name], E)
+    layer, x, mod, router, gu, dn, _ = build_layer(shape, T, R=R)
+    params = RealbParams(global_batch_threshold=0)
+    res = layer.forward(x, mod, strategy=strategy, params=params)
+    torch.cuda.synchronize()
+    layer.check_flag()
+    prec = res.plan.expert_precision(layer.placement)
+    if strategy == "realb":
+        assert res.plan.active and prec.any() and not prec.all(), res.plan
+    ref = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                            gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k,
+                            shape.scoring, expert_prec=prec, routed_scaling=shape.routed_scaling,
+                            logits=layer.logits[:T].cpu().numpy())
+    y = res.y.float().cpu().numpy()
+    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
+    assert err < 2e-2, err
+    # and the FP4 path is genuinely different from all-BF16 (documented accuracy delta)
+    ref16 = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                              gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k,
+                              shape.scoring, routed_scaling=shape.routed_scaling,
+                              logits=layer.logits[:T].cpu().numpy())
+    d16 = np.linalg.norm(y - ref16["y"]) / np.linalg.norm(ref16["y"])
+    assert d16 > err
