@@ -86,6 +86,16 @@ REALB_API int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, int
                          uint8_t* d_codes, uint8_t* d_sf, int sf_layout,
                          int32_t* d_nonfinite_flag, int max_ctas, void* stream);
 
+/* K3 driven by the device-side plan: quantise the bf16 weight rows of every
+ * expert whose d_expert_prec code is W4A4 (rows of expert e are
+ * [e*rows_per_expert, (e+1)*rows_per_expert); rows_per_expert % 128 == 0),
+ * MMA scale layout, other experts untouched. */
+REALB_API int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows_per_expert,
+                                           int64_t cols, const uint8_t* d_expert_prec,
+                                           uint8_t* d_codes, uint8_t* d_sf,
+                                           int32_t* d_nonfinite_flag, int max_ctas,
+                                           void* stream);
+
 /* ------------------------------------------------------------------------ *
  * K1 + K2 — router / top-k / modality statistics (new: the reference
  * synthesises routing, tracegen.py:141-185; the counts it produces feed
@@ -125,6 +135,21 @@ REALB_API int64_t realb_layout_words(int E, int nchunks);
 REALB_API int realb_moe_align(const int32_t* d_chunk_counts, int nchunks, int E,
                     const uint8_t* d_expert_prec, int32_t* d_layout,
                     int32_t* d_expert_vt, void* stream);
+
+/* realb_moe_align with the P1 policy evaluated ON THE DEVICE (no host sync):
+ * expert totals -> per-rank (v,t) over the contiguous placement of R ranks
+ * (place_experts_static, core.py:92-97; aggregate_rank_loads, core.py:106-130)
+ * -> plan_for(strategy) (balancers.py:202-219; plan_realb :89-122 with the
+ * reference's fp64 operation order) -> d_expert_prec (output), then the layout.
+ *   strategy   : 0 baseline, 1 fp4all, 2 realb / realb-seq
+ *   d_plan_out : int32 [3 + R] or NULL: [0] active, [1] #W4A4 ranks, [2] R,
+ *                [3 + r] flags (bit0 hot, bit1 vision-heavy, bit2 W4A4) */
+REALB_API int realb_moe_align_plan(const int32_t* d_chunk_counts, int nchunks, int E, int R,
+                                   int strategy, double capacity_factor,
+                                   double modality_threshold, int64_t global_batch_threshold,
+                                   int modality_isolated, uint8_t* d_expert_prec,
+                                   int32_t* d_plan_out, int32_t* d_layout,
+                                   int32_t* d_expert_vt, void* stream);
 
 /* Local dispatch: scatter token rows into the grouped row space.
  *   d_pair_pos : int32 [T][k] output row of every (token, slot) pair

@@ -47,6 +47,8 @@ SIGNATURES: dict[str, tuple] = {
     "realb_router_topk_stats": (
         _i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _f32, _vp, _vp, _vp, _vp, _vp]),
     "realb_layout_words": (_i64, [_i32, _i32]),
+    "realb_moe_align_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _f64, _f64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "realb_quantize_experts_nvfp4": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
     "realb_moe_align": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "realb_dispatch_permute": (
         _i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -59,10 +61,12 @@ SIGNATURES: dict[str, tuple] = {
 
 _lib: C.CDLL | None = None
 
-# entry points that launch exactly one kernel per successful call
+# kernels launched per successful call (realb_dispatch_permute: positions + rows)
 LAUNCHES_KERNEL = {
-    "realb_quantize_nvfp4", "realb_router_topk_stats", "realb_moe_align", "realb_dispatch_permute",
-    "realb_grouped_gemm_bf16", "realb_grouped_gemm_nvfp4", "realb_combine",
+    "realb_dispatch_permute": 2,
+    "realb_quantize_nvfp4": 1, "realb_router_topk_stats": 1, "realb_moe_align": 1,
+    "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
+    "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_nvfp4": 1, "realb_combine": 1,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 
@@ -94,8 +98,7 @@ def call(name: str, *args) -> int:
     st = getattr(lib, name)(*args)
     if st < 0:
         raise RealbError(name, st, lib.realb_last_error().decode(errors="replace"))
-    if name in LAUNCHES_KERNEL:
-        launch_count += 1
+    launch_count += LAUNCHES_KERNEL.get(name, 0)
     return st
 
 

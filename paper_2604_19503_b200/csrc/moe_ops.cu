@@ -14,11 +14,54 @@
 
 namespace realb {
 
-// ----------------------------------------------------------------- align
+// ----------------------------------------------------------------- align (+ P1 on device)
+struct PlanParams {
+  int enabled;       // 0: use the caller's d_prec; 1: evaluate the strategy below
+  int strategy;      // 0 baseline, 1 fp4all, 2 realb (plan_for, balancers.py:202-219)
+  int R;             // EP ranks of the contiguous placement (place_experts_static)
+  int isolated;      // ClusterConfig.modality_isolated
+  double C, Md;      // RealbParams.capacity_factor / modality_threshold
+  long long thr;     // RealbParams.global_batch_threshold
+};
+
+// plan_realb (balancers.py:89-122) on the device: one thread, the reference's
+// fp64 operation order (identical to realb_plan in runtime.cu).
+__device__ void plan_on_device(const int32_t* ev, int E, const PlanParams& pp, uint8_t* prec,
+                               int32_t* plan_out) {
+  const int R = pp.R, epr = E / R;
+  long long rv[256], rt[256];
+  long long total = 0;
+  for (int r = 0; r < R; ++r) {
+    long long v = 0, t = 0;
+    for (int e = r * epr; e < (r + 1) * epr; ++e) { v += ev[2 * e]; t += ev[2 * e + 1]; }
+    rv[r] = v; rt[r] = v + t;
+    total += v + t;
+  }
+  int active = 0, nacc = 0;
+  for (int r = 0; r < R; ++r) {
+    uint32_t flags = 0;
+    if (pp.strategy == 1) {
+      flags = 7u;
+    } else if (pp.strategy == 2 && !(total < pp.thr || total == 0)) {
+      const double ideal = (double)total / (double)R;
+      const bool hot = (double)rt[r] / ideal > pp.C;
+      const bool vis = pp.isolated ? rt[r] > 0 : (rt[r] > 0 && (double)rv[r] / (double)rt[r] > pp.Md);
+      flags = (hot ? 1u : 0u) | (vis ? 2u : 0u) | ((hot && vis) ? 4u : 0u);
+    }
+    if (flags & 4u) ++nacc;
+    if (plan_out) plan_out[3 + r] = (int32_t)flags;
+    for (int e = r * epr; e < (r + 1) * epr; ++e) prec[e] = (flags & 4u) ? REALB_PREC_W4A4 : REALB_PREC_W16A16;
+  }
+  if (pp.strategy == 1) active = 1;
+  else if (pp.strategy == 2) active = !(total < pp.thr || total == 0);
+  if (plan_out) { plan_out[0] = active; plan_out[1] = nacc; plan_out[2] = R; }
+}
+
 __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ cc, int nchunks,
-                                                    int E, const uint8_t* __restrict__ prec,
+                                                    int E, uint8_t* __restrict__ prec,
                                                     int32_t* __restrict__ layout,
-                                                    int32_t* __restrict__ expert_vt) {
+                                                    int32_t* __restrict__ expert_vt,
+                                                    PlanParams pp, int32_t* plan_out) {
   __shared__ int32_t s_cnt[256], s_start[256];
   const int e = threadIdx.x;
   if (e < E) {
@@ -33,6 +76,7 @@ __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (pp.enabled) plan_on_device(expert_vt, E, pp, prec, plan_out);
     int run = 0;
     for (int i = 0; i < E; ++i) {
       s_start[i] = run;
@@ -74,10 +118,8 @@ __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ 
 constexpr int kPermWarps = 8;
 
 __global__ void __launch_bounds__(256) permute_kernel(
-    const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ topk_idx, int T, int H, int E,
-    int k, const uint8_t* __restrict__ prec, const int32_t* __restrict__ layout,
-    int32_t* __restrict__ pair_pos, __nv_bfloat16* __restrict__ a_bf16,
-    uint8_t* __restrict__ a_codes, uint8_t* __restrict__ a_sf, int32_t* flag) {
+    const int32_t* __restrict__ topk_idx, int T, int E, int k,
+    const int32_t* __restrict__ layout, int32_t* __restrict__ pair_pos) {
   extern __shared__ int32_t sm[];
   int32_t* s_base = sm;                       // [E]
   int32_t* s_cnt = s_base + E;                // [kPermWarps][E]
@@ -128,13 +170,23 @@ __global__ void __launch_bounds__(256) permute_kernel(
     pair_pos[(int64_t)t0 * k + p] = pos;
   }
   __syncthreads();
-  // phase 4: move rows, one warp per pair
+}
+
+// Row movement for every (token, slot) pair, one warp per pair over the whole
+// grid (the position kernel above is chunk-parallel only).
+__global__ void __launch_bounds__(256) gather_rows_kernel(
+    const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ topk_idx,
+    const int32_t* __restrict__ pair_pos, int64_t P, int H, int k,
+    const uint8_t* __restrict__ prec, __nv_bfloat16* __restrict__ a_bf16,
+    uint8_t* __restrict__ a_codes, uint8_t* __restrict__ a_sf, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
   const int nkb = H / 16;
-  for (int p = warp; p < P; p += kPermWarps) {
-    const int t = t0 + p / k;
-    const int e = topk_idx[(int64_t)t0 * k + p];
-    const int64_t pos = s_pos[p];
-    const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = p / k;
+    const int e = topk_idx[p];
+    const int64_t pos = pair_pos[p];
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
     if (prec[e] == REALB_PREC_W16A16) {
       uint4* dst = reinterpret_cast<uint4*>(a_bf16 + pos * H);
       for (int i = lane; i < H / 8; i += 32) dst[i] = __ldg(src + i);
@@ -213,9 +265,32 @@ extern "C" int realb_moe_align(const int32_t* d_cc, int nchunks, int E, const ui
     set_error("realb_moe_align: bad arguments (E=%d nchunks=%d; E <= 256)", E, nchunks);
     return REALB_EINVAL;
   }
-  align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
-                                                    d_expert_vt);
+  PlanParams pp{};
+  align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, const_cast<uint8_t*>(d_prec),
+                                                    d_layout, d_expert_vt, pp, nullptr);
   return check_launch("realb_moe_align");
+}
+
+extern "C" int realb_moe_align_plan(const int32_t* d_cc, int nchunks, int E, int R, int strategy,
+                                    double capacity_factor, double modality_threshold,
+                                    int64_t global_batch_threshold, int modality_isolated,
+                                    uint8_t* d_prec, int32_t* d_plan_out, int32_t* d_layout,
+                                    int32_t* d_expert_vt, void* stream) {
+  if (!d_cc || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 || nchunks < 0 || R < 1 ||
+      R > 256 || E % R || strategy < 0 || strategy > 2) {
+    set_error("realb_moe_align_plan: bad arguments (E=%d R=%d strategy=%d)", E, R, strategy);
+    return REALB_EINVAL;
+  }
+  if (!(capacity_factor > 0.0) || !(modality_threshold >= 0.0 && modality_threshold <= 1.0) ||
+      global_batch_threshold < 0) {
+    set_error("realb_moe_align_plan: invalid RealbParams");
+    return REALB_EINVAL;
+  }
+  PlanParams pp{1, strategy, R, modality_isolated, capacity_factor, modality_threshold,
+                (long long)global_batch_threshold};
+  align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
+                                                    d_expert_vt, pp, d_plan_out);
+  return check_launch("realb_moe_align_plan");
 }
 
 extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx, int T, int H,
@@ -231,10 +306,17 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
   }
   if (T == 0) return REALB_OK;
   const int smem = (E + kPermWarps * E + 128 * k) * 4;
-  permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, T, H, E, k, d_prec, d_layout,
-      d_pair_pos, reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag);
-  return check_launch("realb_dispatch_permute");
+  permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout,
+                                                                d_pair_pos);
+  int rc = check_launch("realb_dispatch_permute (positions)");
+  if (rc) return rc;
+  const int64_t P = (int64_t)T * k;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  gather_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, d_prec,
+      reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag);
+  return check_launch("realb_dispatch_permute (rows)");
 }
 
 extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const float* d_w, int T,

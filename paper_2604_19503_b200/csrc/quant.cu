@@ -93,6 +93,60 @@ __global__ void __launch_bounds__(256) quant_kernel_bf16(const __nv_bfloat16* __
   }
 }
 
+// K3 on the device-side plan: quantise only the rows of experts whose
+// precision code is W4A4 (rows_per_expert % 128 == 0, so a tile never straddles
+// two experts); MMA scale layout. The tiles of one expert are contiguous, so
+// whole experts are skipped by a single compare per tile.
+__global__ void __launch_bounds__(256) quant_experts_kernel(
+    const __nv_bfloat16* __restrict__ x, int64_t rows_per_expert, int64_t cols, int E,
+    const uint8_t* __restrict__ prec, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
+    int32_t* flag) {
+  const int64_t nkb = cols >> 4;
+  const int64_t tiles_k = nkb >> 2;
+  const int64_t tiles_per_expert = (rows_per_expert >> 7) * tiles_k;
+  // enumerate only the W4A4 experts' tiles: tile -> (j-th W4A4 expert, local tile)
+  __shared__ int s_list[256];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int e = 0; e < E; ++e)
+      if (prec[e] == REALB_PREC_W4A4) s_list[n++] = e;
+    s_n = n;
+  }
+  __syncthreads();
+  const int64_t tiles = (int64_t)s_n * tiles_per_expert;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t j = tile / tiles_per_expert, lt = tile - j * tiles_per_expert;
+    const int64_t tm = s_list[j] * (rows_per_expert >> 7) + lt / tiles_k, tk = lt % tiles_k;
+    uint32_t w[2][8];
+    int64_t rr[2], kk[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int b = threadIdx.x + h * 256;
+      rr[h] = tm * 128 + (b >> 2);
+      kk[h] = tk * 4 + (b & 3);
+      const uint4* q = reinterpret_cast<const uint4*>(x + rr[h] * cols + kk[h] * 16);
+      const uint4 a = __ldg(q), c = __ldg(q + 1);
+      w[h][0] = a.x; w[h][1] = a.y; w[h][2] = a.z; w[h][3] = a.w;
+      w[h][4] = c.x; w[h][5] = c.y; w[h][6] = c.z; w[h][7] = c.w;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t nf = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t ex = w[h][i] & 0x7F807F80u;
+        nf |= ((ex & 0xFFFFu) == 0x7F80u) | ((ex >> 16) == 0x7F80u);
+      }
+      if (nf) flag_nonfinite(flag);
+      uint32_t sbits;
+      const uint2 c = quant_block16_bf16(w[h], sbits);
+      *reinterpret_cast<uint2*>(codes + rr[h] * (cols >> 1) + kk[h] * 8) = c;
+      sf[sf_mma_offset(rr[h], kk[h], nkb)] = (uint8_t)sbits;
+    }
+  }
+}
+
 template <typename T, int LAYOUT>
 __global__ void __launch_bounds__(256) quant_kernel(const T* __restrict__ x, int64_t rows,
                                                      int64_t cols, uint8_t* __restrict__ codes,
@@ -227,4 +281,22 @@ extern "C" int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, in
       set_error("realb_quantize_nvfp4: unknown dtype %d", dtype);
       return REALB_EINVAL;
   }
+}
+
+extern "C" int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows_per_expert,
+                                            int64_t cols, const uint8_t* d_expert_prec,
+                                            uint8_t* d_codes, uint8_t* d_sf, int32_t* d_flag,
+                                            int max_ctas, void* stream) {
+  if (!d_w || !d_expert_prec || !d_codes || !d_sf || E < 1 || E > 256 || rows_per_expert <= 0 ||
+      rows_per_expert % 128 || cols <= 0 || cols % 64) {
+    set_error("realb_quantize_experts_nvfp4: bad arguments (E=%d rows/expert=%lld cols=%lld)", E,
+              (long long)rows_per_expert, (long long)cols);
+    return REALB_EINVAL;
+  }
+  int grid = num_sms() * 8;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  quant_experts_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_w), rows_per_expert, cols, E, d_expert_prec,
+      d_codes, d_sf, d_flag);
+  return check_launch("realb_quantize_experts_nvfp4");
 }

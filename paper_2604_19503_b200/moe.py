@@ -5,27 +5,29 @@ instead of evaluating cost formulas it executes the layer with the sm_100a
 kernels of the C-ABI library and reports the same per-rank phase schema
 (``RankPhases``/``LayerTiming``, engine.py:55-86) filled from CUDA events.
 
-Per layer:
+Per layer, all stream-ordered with NO host synchronisation:
   K1+K2 router_topk_stats            main stream   logits, top-k, (v,t) chunk counts
-  align                              main stream   expert totals + grouped row space
-  policy  plan_realb on the host     one 1-KB D2H  (policy.py; balancers.py:89-122)
-  K3 quantise W4A4 experts' weights  SIDE stream   overlapped with dispatch
+  align_plan                         main stream   expert totals, P1 plan_realb ON THE
+                                                   DEVICE (balancers.py:89-122 op order),
+                                                   grouped row space per precision
+  K3 quantise W4A4 experts' weights  SIDE stream   reads the device plan; overlaps dispatch
   dispatch_permute (+K4 act quant)   main stream
   K5 / K6 grouped GEMMs (+SwiGLU)    main stream   (K6 waits on the side stream)
   combine                            main stream
+The plan and counts are copied back asynchronously and exposed lazily on the
+returned LayerResult (valid until the next forward() of the same layer).
 """
 
 from __future__ import annotations
 
 import enum
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
-from .policy import (ClusterConfig, Precision, PrecisionPlan, RealbParams, place_experts_static,
-                     plan_baseline, plan_for, rank_loads_from_counts)
+from .policy import ClusterConfig, Precision, PrecisionPlan, RealbParams, place_experts_static
 
 
 # ----------------------------------------------------------------- shapes
@@ -135,13 +137,38 @@ class MoEWeights:
 
 
 # ----------------------------------------------------------------- the layer
-@dataclass
+_STRATEGY_CODE = {"baseline": 0, "eplb": 0, "async-eplb": 0, "fp4all": 1, "realb": 2, "realb-seq": 2}
+
+
 class LayerResult:
-    y: torch.Tensor
-    plan: PrecisionPlan
-    expert_vt: np.ndarray
-    timing: LayerTiming | None = None
-    events: dict = field(default_factory=dict)
+    """Output of one layer call. ``plan`` and ``expert_vt`` are read back lazily
+    (an event-guarded pinned copy), so the step itself never synchronises."""
+
+    def __init__(self, y, layer, plan_host, vt_host, event, placement, cluster):
+        self.y = y
+        self._plan_host, self._vt_host, self._event = plan_host, vt_host, event
+        self._placement, self._cluster = placement, cluster
+        self._plan = None
+
+    @property
+    def expert_vt(self) -> np.ndarray:
+        self._event.synchronize()
+        return self._vt_host.numpy().copy()
+
+    @property
+    def plan(self) -> PrecisionPlan:
+        if self._plan is None:
+            self._event.synchronize()
+            po = self._plan_host.numpy()
+            R = self._cluster.num_ranks
+            flags = po[3:3 + R]
+            active = bool(po[0])
+            self._plan = PrecisionPlan(
+                tuple(Precision.W4A4 if f & 4 else Precision.W16A16 for f in flags),
+                frozenset(int(r) for r in np.flatnonzero(flags & 1)),
+                frozenset(int(r) for r in np.flatnonzero(flags & 2)),
+                active)
+        return self._plan
 
 
 class MoELayer:
@@ -155,7 +182,7 @@ class MoELayer:
     """
 
     def __init__(self, weights: MoEWeights, max_tokens: int, cluster: ClusterConfig | None = None,
-                 device="cuda", quant_max_ctas: int = 0, timing: bool = False):
+                 device="cuda", quant_max_ctas: int = 0):
         s = weights.shape
         self.w, self.shape = weights, s
         self.E, self.k, self.H, self.I = s.num_experts, s.top_k, s.hidden, s.intermediate
@@ -168,7 +195,6 @@ class MoELayer:
         self.max_tokens = max_tokens
         self.device = torch.device(device)
         self.quant_max_ctas = quant_max_ctas
-        self.timing = timing
         E, k, H, I = self.E, self.k, self.H, self.I
         T = max_tokens
         self.nchunks_max = (T + 127) // 128
@@ -184,6 +210,8 @@ class MoELayer:
         self.pair_pos = torch.empty(T, k, dtype=i32, device=dev)
         self.prec_dev = torch.zeros(E, dtype=u8, device=dev)
         self.prec_host = torch.zeros(E, dtype=u8, pin_memory=True)
+        self.plan_dev = torch.zeros(3 + self.cluster.num_ranks, dtype=i32, device=dev)
+        self.plan_host = torch.zeros(3 + self.cluster.num_ranks, dtype=i32, pin_memory=True)
         R = self.rows_cap
         self.a_bf16 = torch.empty(R, H, dtype=bf, device=dev)
         self.h_bf16 = torch.empty(R, I, dtype=bf, device=dev)
@@ -246,83 +274,80 @@ class MoELayer:
                   self.prec_dev.data_ptr(), self.layout.data_ptr(), self.expert_vt.data_ptr(),
                   _lib.stream_ptr())
 
-    def plan(self, strategy: str, params: RealbParams | None) -> PrecisionPlan:
-        """D2H of the [E,2] counts (one small sync) then the reference policy."""
-        self.expert_vt_host.copy_(self.expert_vt, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        loads = rank_loads_from_counts(self.expert_vt_host.numpy(), self.cluster)
-        return plan_for(strategy, loads, self.cluster, params)
+    def align_plan(self, T: int, strategy: str, params: RealbParams):
+        """Expert totals + the precision plan evaluated on the device (no sync)."""
+        c = self.cluster
+        _lib.call("realb_moe_align_plan", self.chunk_counts.data_ptr(), (T + 127) // 128, self.E,
+                  c.num_ranks, _STRATEGY_CODE[strategy], float(params.capacity_factor),
+                  float(params.modality_threshold), int(params.global_batch_threshold),
+                  int(bool(c.modality_isolated)), self.prec_dev.data_ptr(), self.plan_dev.data_ptr(),
+                  self.layout.data_ptr(), self.expert_vt.data_ptr(), _lib.stream_ptr())
 
     def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
-                params: RealbParams | None = None, plan: PrecisionPlan | None = None) -> LayerResult:
+                params: RealbParams | None = None) -> LayerResult:
+        """One MoE layer over the local tokens; stream-ordered, no host sync.
+
+        strategy "baseline" (and the EPLB tags) runs the all-BF16 comparator with
+        exactly the same kernels minus the NVFP4 ones; "realb"/"fp4all" evaluate
+        the plan on the device and launch the W4A4 machinery (K3 on the side
+        stream, K4 in dispatch, K6), which is a no-op for experts the plan keeps
+        at W16A16."""
+        if strategy not in _STRATEGY_CODE:
+            raise ValueError(f"unknown strategy {strategy!r}")
+        params = params or RealbParams()
         T = x.shape[0]
         if T > self.max_tokens:
             raise ValueError("more tokens than the layer was sized for")
         E, k, H, I = self.E, self.k, self.H, self.I
         nch = (T + 127) // 128
         main = torch.cuda.current_stream()
-        ev = {n: torch.cuda.Event(enable_timing=True) for n in
-              ("start", "routed", "planned", "dispatched", "computed", "end", "q0", "q1")} if self.timing else {}
-        rec = (lambda n, s=None: ev[n].record(s or main)) if self.timing else (lambda n, s=None: None)
-        rec("start")
+        sp = _lib.stream_ptr(main)
         self.route(x, modality)
-        self.prec_dev.zero_()
-        self.align(T)
-        rec("routed")
-        if plan is None:
-            if strategy in ("baseline", "eplb", "async-eplb"):
-                plan = plan_baseline([None] * self.cluster.num_ranks)
-                vt = None
-            else:
-                plan = self.plan(strategy, params)
-                vt = self.expert_vt_host.numpy().copy()
-        else:
-            vt = None
-        prec = plan.expert_precision(self.placement)
-        fp4_experts = np.flatnonzero(prec == _lib.PREC_W4A4)
-        if len(fp4_experts):
-            self.prec_host.numpy()[:] = prec
-            self.prec_dev.copy_(self.prec_host, non_blocking=True)
-            self.align(T)  # rebuild the per-precision group lists
+        self.align_plan(T, strategy, params)
+        mixed = _STRATEGY_CODE[strategy] != 0
+        if mixed:
             ws = self._fp4_ws()
             self.side.wait_stream(main)
             with torch.cuda.stream(self.side):
-                rec("q0", self.side)
-                self.quantize_experts(fp4_experts.tolist(), self.side)
-                rec("q1", self.side)
-        rec("planned")
-        ws = self._fp4 if len(fp4_experts) else None
+                ssp = _lib.stream_ptr(self.side)
+                _lib.call("realb_quantize_experts_nvfp4", self.w.w_gu.data_ptr(), E, 2 * I, H,
+                          self.prec_dev.data_ptr(), ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
+                          self.flag.data_ptr(), self.quant_max_ctas, ssp)
+                _lib.call("realb_quantize_experts_nvfp4", self.w.w_d.data_ptr(), E, H, I,
+                          self.prec_dev.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
+                          self.flag.data_ptr(), self.quant_max_ctas, ssp)
+        else:
+            ws = None
         _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
                   self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
                   self.pair_pos.data_ptr(), self.a_bf16.data_ptr(),
                   _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
-                  self.flag.data_ptr(), _lib.stream_ptr())
-        rec("dispatched")
-        sp = _lib.stream_ptr()
+                  self.flag.data_ptr(), sp)
         lay = self.layout.data_ptr()
-        if len(fp4_experts) < E:
-            _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
-                      self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
-                      self.h_bf16.data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
+                  self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                  self.h_bf16.data_ptr(), 0, sp)
         if ws is not None:
             main.wait_stream(self.side)
             _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
                       ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, E,
                       lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
-        if len(fp4_experts) < E:
-            _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
-                      self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
-                      self.rows_out.data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
+                  self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
+                  self.rows_out.data_ptr(), 0, sp)
         if ws is not None:
             _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
-        rec("computed")
         y = torch.empty(T, H, dtype=torch.bfloat16, device=x.device)
         _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
                   self.topk_w.data_ptr(), T, H, k, y.data_ptr(), sp)
-        rec("end")
-        return LayerResult(y=y, plan=plan, expert_vt=vt, events=ev)
+        # lazy, asynchronous read-back of the plan and the counts (pinned, event-guarded)
+        self.plan_host.copy_(self.plan_dev, non_blocking=True)
+        self.expert_vt_host.copy_(self.expert_vt, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        return LayerResult(y, self, self.plan_host, self.expert_vt_host, ev, self.placement, self.cluster)
 
     def expert_compute(self, T: int, prec: np.ndarray) -> None:
         """Re-run only the expert GEMMs of the experts whose code in ``prec`` is

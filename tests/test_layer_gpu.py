@@ -21,7 +21,7 @@ def small(shape: MoEShape, E=None):
     return replace(shape, num_experts=E or shape.num_experts)
 
 
-def build_layer(shape, T, R=1, seed=2024, timing=False):
+def build_layer(shape, T, R=1, seed=2024):
     spec = WorkloadSpec(tokens=T, num_ranks=8 if shape.num_experts % 8 == 0 else 1, seed=seed)
     x, mod, router, planned = make_batch(shape, spec)
     gu, dn = make_experts(shape, seed=seed)
@@ -30,7 +30,7 @@ def build_layer(shape, T, R=1, seed=2024, timing=False):
         bias = torch.zeros(shape.num_experts, device="cuda")
     w = MoEWeights.from_hf(shape, router, gu, dn, bias=bias)
     cluster = ClusterConfig(R, 1, shape.num_experts // R, 1, shape.modality_isolated)
-    layer = MoELayer(w, max_tokens=T, cluster=cluster, timing=timing)
+    layer = MoELayer(w, max_tokens=T, cluster=cluster)
     return layer, x, mod, router, gu, dn, planned
 
 
@@ -181,3 +181,61 @@ def test_layer_w4a4_vs_oracle(name, E, T, strategy, R):
                               logits=layer.logits[:T].cpu().numpy())
     d16 = np.linalg.norm(y - ref16["y"]) / np.linalg.norm(ref16["y"])
     assert d16 > err
+
+
+def test_device_plan_matches_host_policy():
+    """realb_moe_align_plan (P1 on the device) == policy.plan_realb (the C host
+    policy pinned to the reference) on fuzzed per-expert counts, incl. boundaries."""
+    from paper_2604_19503_b200.policy import plan_for, rank_loads_from_counts
+
+    rng = np.random.default_rng(17)
+    for trial in range(300):
+        R = int(rng.choice([1, 2, 4, 8]))
+        epr = int(rng.choice([1, 2, 8, 16]))
+        E = R * epr
+        if E > 256:
+            continue
+        nch = int(rng.integers(1, 5))
+        kind = trial % 4
+        if kind == 0:
+            cc = rng.integers(0, 300, (nch, E, 2))
+        elif kind == 1:  # exact-mean boundary
+            cc = np.zeros((nch, E, 2), np.int64)
+            cc[0, :, 0] = 100
+            cc[0, 0, 0] = 200 if R > 1 else 100
+        elif kind == 2:
+            cc = rng.integers(0, 40, (nch, E, 2)) * (rng.random((nch, E, 1)) < 0.5)
+        else:
+            cc = (rng.pareto(1.0, (nch, E, 2)) * 50).astype(np.int64)
+        C = float(rng.choice([1.0, 0.5, 1.3]))
+        Md = float(rng.choice([0.0, 0.5, 0.7, 1.0, float(rng.random())]))
+        thr = int(rng.choice([0, 2048, int(cc.sum())]))
+        iso = bool(rng.random() < 0.3)
+        strategy = str(rng.choice(["baseline", "fp4all", "realb"]))
+        cluster = ClusterConfig(R, 1, epr, 1, iso)
+        params = RealbParams(C, Md, thr)
+        d_cc = torch.from_numpy(cc.astype(np.int32)).cuda()
+        prec = torch.zeros(E, dtype=torch.uint8, device="cuda")
+        plan_out = torch.full((3 + R,), -1, dtype=torch.int32, device="cuda")
+        lay = torch.zeros(int(_lib.load().realb_layout_words(E, nch)), dtype=torch.int32, device="cuda")
+        vt = torch.zeros(E, 2, dtype=torch.int32, device="cuda")
+        code = {"baseline": 0, "fp4all": 1, "realb": 2}[strategy]
+        _lib.call("realb_moe_align_plan", d_cc.data_ptr(), nch, E, R, code, C, Md, thr, int(iso),
+                  prec.data_ptr(), plan_out.data_ptr(), lay.data_ptr(), vt.data_ptr(), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        ref = plan_for(strategy, rank_loads_from_counts(cc.sum(0), cluster), cluster, params)
+        po = plan_out.cpu().numpy()
+        assert bool(po[0]) == ref.active
+        flags = po[3:]
+        assert [bool(f & 4) for f in flags] == [p.value == "w4a4" for p in ref.per_rank_precision]
+        if strategy == "realb":
+            assert {r for r in range(R) if flags[r] & 1} == set(ref.hot_ranks)
+            assert {r for r in range(R) if flags[r] & 2} == set(ref.vision_heavy_ranks)
+        assert (prec.cpu().numpy() == ref.expert_precision(ref_placement(cluster))).all()
+        assert (vt.cpu().numpy() == cc.sum(0)).all()
+
+
+def ref_placement(cluster):
+    from paper_2604_19503_b200.policy import place_experts_static
+
+    return place_experts_static(cluster)
