@@ -133,8 +133,10 @@ REALB_API int realb_router_topk_stats(const void* d_x, const void* d_wg, const f
  * ------------------------------------------------------------------------ */
 REALB_API int64_t realb_layout_words(int E, int nchunks);
 REALB_API int realb_moe_align(const int32_t* d_chunk_counts, int nchunks, int E,
-                    const uint8_t* d_expert_prec, int32_t* d_layout,
-                    int32_t* d_expert_vt, void* stream);
+                              const uint8_t* d_expert_prec, int row_align, int32_t* d_layout,
+                              int32_t* d_expert_vt, void* stream);
+/* row_align: 128 for the GEMM row space; 1 for an unpadded, expert-sorted
+ * (hence destination-rank-contiguous) EP send buffer. */
 
 /* realb_moe_align with the P1 policy evaluated ON THE DEVICE (no host sync):
  * expert totals -> per-rank (v,t) over the contiguous placement of R ranks
@@ -163,6 +165,27 @@ REALB_API int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx,
                            const int32_t* d_layout, int nchunks, int64_t rows_cap,
                            int32_t* d_pair_pos, void* d_a_bf16, uint8_t* d_a_codes,
                            uint8_t* d_a_sf, int32_t* d_nonfinite_flag, void* stream);
+
+/* The row-movement half of realb_dispatch_permute, exposed for the EP
+ * receive side: row p of x (token p / k) goes to position d_pos[p] of the
+ * grouped space as bf16 or, when d_prec[d_expert[p]] is W4A4, as NVFP4 (K4). */
+REALB_API int realb_gather_rows(const void* d_x, const int32_t* d_expert, const int32_t* d_pos,
+                                int64_t P, int H, int k, const uint8_t* d_prec, void* d_a_bf16,
+                                uint8_t* d_a_codes, uint8_t* d_a_sf, int32_t* d_nonfinite_flag,
+                                void* stream);
+
+/* EP receive side (C2): rows arrive source-major, per source ordered by local
+ * expert (senders pack by global expert id). From the [R][El] count matrix
+ * build the local grouped layout (as realb_moe_align, El experts) and, for
+ * every received row, its local expert and grouped position.
+ *   d_base : int32 workspace [2*R*El + 2] */
+REALB_API int realb_ep_regroup(const int32_t* d_cnt, int R, int El, const uint8_t* d_prec_local,
+                               int64_t n_recv, int32_t* d_layout, int32_t* d_base,
+                               int32_t* d_row_expert, int32_t* d_row_pos, void* stream);
+
+/* dst[i] = src[idx[i]] for bf16 rows of H (EP return path before C3). */
+REALB_API int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t n, int H,
+                               void* d_dst, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * K5 — grouped BF16 expert GEMM on tcgen05 (kind::f16, TMA, TMEM).

@@ -49,7 +49,10 @@ SIGNATURES: dict[str, tuple] = {
     "realb_layout_words": (_i64, [_i32, _i32]),
     "realb_moe_align_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _f64, _f64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_quantize_experts_nvfp4": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
-    "realb_moe_align": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "realb_moe_align": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
+    "realb_gather_rows": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "realb_ep_regroup": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "realb_index_rows": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "realb_dispatch_permute": (
         _i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "realb_grouped_gemm_bf16": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]),
@@ -67,6 +70,7 @@ LAUNCHES_KERNEL = {
     "realb_quantize_nvfp4": 1, "realb_router_topk_stats": 1, "realb_moe_align": 1,
     "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_nvfp4": 1, "realb_combine": 1,
+    "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ 
                                                     int E, uint8_t* __restrict__ prec,
                                                     int32_t* __restrict__ layout,
                                                     int32_t* __restrict__ expert_vt,
-                                                    PlanParams pp, int32_t* plan_out) {
+                                                    PlanParams pp, int32_t* plan_out, int ra) {
   __shared__ int32_t s_cnt[256], s_start[256];
   const int e = threadIdx.x;
   if (e < E) {
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ 
     int run = 0;
     for (int i = 0; i < E; ++i) {
       s_start[i] = run;
-      run += (s_cnt[i] + 127) / 128 * 128;
+      run += (s_cnt[i] + ra - 1) / ra * ra;
     }
     layout[0] = run;
     for (int p = 0; p < 2; ++p) {
@@ -219,6 +219,96 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
   }
 }
 
+// ----------------------------------------------------------------- EP receive side
+// Received rows arrive source-major: from rank s, the rows of local expert 0,
+// then 1, ... (each sender packs by global expert id). regroup builds the local
+// grouped layout (128-row padded, per precision) and, per received row, its
+// local expert and its position in the grouped row space.
+__global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t* __restrict__ cnt, int R,
+                                                        int El, const uint8_t* __restrict__ prec,
+                                                        int32_t* __restrict__ layout,
+                                                        int32_t* __restrict__ base /*[R*El+1]*/) {
+  __shared__ int32_t s_tot[256], s_start[256];
+  const int e = threadIdx.x;
+  if (e < El) {
+    int t = 0;
+    for (int r = 0; r < R; ++r) t += cnt[r * El + e];
+    s_tot[e] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < El; ++i) {
+      s_start[i] = run;
+      run += (s_tot[i] + 127) / 128 * 128;
+    }
+    layout[0] = run;
+    for (int p = 0; p < 2; ++p) {
+      int32_t* gl = layout + LayoutView::off_glist(El, p);
+      int32_t* pf = layout + LayoutView::off_prefix(El, p);
+      int g = 0, mt = 0;
+      for (int i = 0; i < El; ++i) {
+        if ((int)prec[i] != p) continue;
+        gl[g] = i;
+        pf[g] = mt;
+        mt += (s_tot[i] + 127) / 128;
+        ++g;
+      }
+      pf[g] = mt;
+      layout[1 + p] = g;
+    }
+    // source-major prefix of received rows (row index space of the recv buffer)
+    int pr = 0;
+    for (int f = 0; f < R * El; ++f) {
+      base[R * El + 1 + f] = pr;  // recv prefix
+      pr += cnt[f];
+    }
+    base[2 * R * El + 1] = pr;
+  }
+  __syncthreads();
+  if (e < El) {
+    layout[LayoutView::off_row_start(El) + e] = s_start[e];
+    layout[LayoutView::off_row_count(El) + e] = s_tot[e];
+    int run = s_start[e];
+    for (int r = 0; r < R; ++r) {
+      base[r * El + e] = run;  // grouped position of (source r, expert e)'s first row
+      run += cnt[r * El + e];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) ep_rows_kernel(const int32_t* __restrict__ base, int R,
+                                                      int El, int64_t n,
+                                                      int32_t* __restrict__ row_expert,
+                                                      int32_t* __restrict__ row_pos) {
+  const int F = R * El;
+  const int32_t* pre = base + F + 1;  // [F+1] source-major prefix
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = F - 1;  // largest f with pre[f] <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pre[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    row_expert[i] = lo % El;
+    row_pos[i] = base[lo] + (int32_t)(i - pre[lo]);
+  }
+}
+
+// dst[i] = src[idx[i]]  (bf16 rows; return path of the EP combine)
+__global__ void __launch_bounds__(256) index_rows_kernel(const __nv_bfloat16* __restrict__ src,
+                                                         const int32_t* __restrict__ idx,
+                                                         int64_t n, int H,
+                                                         __nv_bfloat16* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t)idx[r] * H);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + r * H);
+    for (int i = lane; i < H / 8; i += 32) d4[i] = __ldg(s4 + i);
+  }
+}
+
 // ----------------------------------------------------------------- combine
 __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ rows,
                                                       const int32_t* __restrict__ pos,
@@ -260,14 +350,19 @@ extern "C" int64_t realb_layout_words(int E, int nchunks) {
 }
 
 extern "C" int realb_moe_align(const int32_t* d_cc, int nchunks, int E, const uint8_t* d_prec,
-                               int32_t* d_layout, int32_t* d_expert_vt, void* stream) {
+                               int row_align, int32_t* d_layout, int32_t* d_expert_vt,
+                               void* stream) {
   if (!d_cc || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 || nchunks < 0) {
     set_error("realb_moe_align: bad arguments (E=%d nchunks=%d; E <= 256)", E, nchunks);
     return REALB_EINVAL;
   }
+  if (row_align != 1 && row_align != 128) {
+    set_error("realb_moe_align: row_align must be 1 or 128 (got %d)", row_align);
+    return REALB_EINVAL;
+  }
   PlanParams pp{};
   align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, const_cast<uint8_t*>(d_prec),
-                                                    d_layout, d_expert_vt, pp, nullptr);
+                                                    d_layout, d_expert_vt, pp, nullptr, row_align);
   return check_launch("realb_moe_align");
 }
 
@@ -289,7 +384,7 @@ extern "C" int realb_moe_align_plan(const int32_t* d_cc, int nchunks, int E, int
   PlanParams pp{1, strategy, R, modality_isolated, capacity_factor, modality_threshold,
                 (long long)global_batch_threshold};
   align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
-                                                    d_expert_vt, pp, d_plan_out);
+                                                    d_expert_vt, pp, d_plan_out, 128);
   return check_launch("realb_moe_align_plan");
 }
 
@@ -330,4 +425,54 @@ extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const flo
       reinterpret_cast<const __nv_bfloat16*>(d_rows), d_pos, d_w, T, H, k,
       reinterpret_cast<__nv_bfloat16*>(d_y));
   return check_launch("realb_combine");
+}
+
+extern "C" int realb_gather_rows(const void* d_x, const int32_t* d_expert, const int32_t* d_pos,
+                                 int64_t P, int H, int k, const uint8_t* d_prec, void* d_a_bf16,
+                                 uint8_t* d_a_codes, uint8_t* d_a_sf, int32_t* d_flag,
+                                 void* stream) {
+  if (!d_x || !d_expert || !d_pos || !d_prec || !d_a_bf16 || P < 0 || H <= 0 || H % 64 || k < 1) {
+    set_error("realb_gather_rows: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (P == 0) return REALB_OK;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  gather_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_expert, d_pos, P, H, k, d_prec,
+      reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag);
+  return check_launch("realb_gather_rows");
+}
+
+extern "C" int realb_ep_regroup(const int32_t* d_cnt, int R, int El, const uint8_t* d_prec_local,
+                                int64_t n_recv, int32_t* d_layout, int32_t* d_base,
+                                int32_t* d_row_expert, int32_t* d_row_pos, void* stream) {
+  if (!d_cnt || !d_prec_local || !d_layout || !d_base || R < 1 || El < 1 || El > 256 ||
+      R * El > 4096 || n_recv < 0 || (n_recv > 0 && (!d_row_expert || !d_row_pos))) {
+    set_error("realb_ep_regroup: bad arguments (R=%d El=%d)", R, El);
+    return REALB_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  ep_layout_kernel<<<1, 256, 0, st>>>(d_cnt, R, El, d_prec_local, d_layout, d_base);
+  int rc = check_launch("realb_ep_regroup (layout)");
+  if (rc || n_recv == 0) return rc;
+  int64_t grid = (n_recv + 255) / 256;
+  if (grid > (int64_t)num_sms() * 8) grid = (int64_t)num_sms() * 8;
+  ep_rows_kernel<<<(unsigned)grid, 256, 0, st>>>(d_base, R, El, n_recv, d_row_expert, d_row_pos);
+  return check_launch("realb_ep_regroup (rows)");
+}
+
+extern "C" int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t n, int H,
+                                void* d_dst, void* stream) {
+  if (!d_src || !d_idx || !d_dst || n < 0 || H <= 0 || H % 8) {
+    set_error("realb_index_rows: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (n == 0) return REALB_OK;
+  int64_t grid = (n + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  index_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_src), d_idx, n, H,
+      reinterpret_cast<__nv_bfloat16*>(d_dst));
+  return check_launch("realb_index_rows");
 }

@@ -1,0 +1,319 @@
+"""Expert-parallel ReaLB MoE layer: one process per GPU, NCCL over NVLink.
+
+Per layer on rank r of R (contiguous placement: rank r hosts experts
+[r*El, (r+1)*El), place_experts_static, core.py:92-97):
+
+  K1+K2  route the local tokens                         -> top-k, per-expert (v,t)
+  C1     all_gather of the [E,2] counts (1 KB)           -> identical global loads on
+         every rank (integer sums: identical plans); one host sync, which
+         NCCL's all_to_allv needs anyway for its split sizes
+  P1     plan_for(strategy) on the global loads (policy.py -> C realb_plan,
+         balancers.py:89-122); my precision = plan[r]
+  pack   rows sorted by global expert (unpadded): rank-contiguous send buffer
+  K3     [side stream] quantise my experts' weights if plan[r] is W4A4 — issued
+         before C2 so it runs under the dispatch
+  C2     all_to_all_v of bf16 token rows
+  regroup + K4 + K5/K6   grouped expert MLPs over the received rows
+  C3     all_to_all_v back, then the weighted top-k combine
+
+The device work goes through a backend object (``CudaEPOps`` here; the CPU
+tests inject an oracle backend) and the collectives through ``EPComm``, so the
+host orchestration is one piece of code on GPUs (NCCL), in CPU tests (gloo)
+and in the one-GPU, two-process test (gloo staged through the host).
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .moe import MoEShape, MoEWeights
+from .policy import ClusterConfig, Precision, PrecisionPlan, RealbParams, plan_for, \
+    rank_loads_from_counts
+
+
+# ----------------------------------------------------------------------------- comm
+class EPComm:
+    """Collectives of the EP layer. ``staged`` copies device tensors through the
+    host (gloo on a shared GPU / CPU tests); otherwise tensors go to NCCL as-is."""
+
+    def __init__(self, group=None, staged: bool = False):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.staged = staged
+
+    def all_gather_counts(self, vt_local: torch.Tensor) -> np.ndarray:
+        """[E,2] int32 per rank -> host numpy [R,E,2] (the layer's one sync)."""
+        src = vt_local.cpu() if self.staged else vt_local
+        out = [torch.empty_like(src) for _ in range(self.world)]
+        dist.all_gather(out, src.contiguous(), group=self.group)
+        return torch.stack(out).cpu().numpy().astype(np.int64)
+
+    def all_to_all_rows(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits):
+        out_splits = [int(a) for a in out_splits]
+        in_splits = [int(a) for a in in_splits]
+        if self.staged:
+            o = torch.empty((sum(out_splits),) + tuple(out.shape[1:]), dtype=out.dtype)
+            dist.all_to_all_single(o, inp[:sum(in_splits)].cpu(), out_splits, in_splits, group=self.group)
+            out[:sum(out_splits)].copy_(o)
+        else:
+            dist.all_to_all_single(out[:sum(out_splits)], inp[:sum(in_splits)], out_splits, in_splits,
+                                   group=self.group)
+        return out
+
+
+# ----------------------------------------------------------------------------- device backend
+class CudaEPOps:
+    """The sm_100a kernels behind the EP layer (C-ABI library)."""
+
+    def __init__(self, shape: MoEShape, router: torch.Tensor, bias, local: MoEWeights, world: int,
+                 max_tokens: int, device="cuda", quant_max_ctas: int = 0):
+        self.s, self.router, self.bias, self.local = shape, router, bias, local
+        E, k, H, I = shape.num_experts, shape.top_k, shape.hidden, shape.intermediate
+        self.E, self.k, self.H, self.I, self.R = E, k, H, I, world
+        self.El = E // world
+        T = max_tokens
+        self.T = T
+        dev, i32, bf, u8 = torch.device(device), torch.int32, torch.bfloat16, torch.uint8
+        self.dev = dev
+        self.nch = (T + 127) // 128
+        self.logits = torch.empty(T, E, dtype=torch.float32, device=dev)
+        self.topk_idx = torch.empty(T, k, dtype=i32, device=dev)
+        self.topk_w = torch.empty(T, k, dtype=torch.float32, device=dev)
+        self.cc = torch.empty(self.nch, E, 2, dtype=i32, device=dev)
+        self.send_layout = torch.zeros(int(_lib.load().realb_layout_words(E, self.nch)), dtype=i32, device=dev)
+        self.vt_local = torch.empty(E, 2, dtype=i32, device=dev)
+        self.zero_prec = torch.zeros(E, dtype=u8, device=dev)
+        self.send_pos = torch.empty(T, k, dtype=i32, device=dev)
+        self.send_buf = torch.empty(T * k, H, dtype=bf, device=dev)
+        self.ret_buf = torch.empty(T * k, H, dtype=bf, device=dev)
+        recv_cap = world * T * k  # every token of every rank could pick my experts
+        self.recv_cap = recv_cap
+        self.recv_buf = torch.empty(recv_cap, H, dtype=bf, device=dev)
+        self.back_buf = torch.empty(recv_cap, H, dtype=bf, device=dev)
+        self.row_expert = torch.empty(recv_cap, dtype=i32, device=dev)
+        self.row_pos = torch.empty(recv_cap, dtype=i32, device=dev)
+        El = self.El
+        self.rows_cap = (recv_cap + El * 127 + 127) // 128 * 128
+        self.local_layout = torch.zeros(int(_lib.load().realb_layout_words(El, 1)), dtype=i32, device=dev)
+        self.base = torch.empty(2 * world * El + 2, dtype=i32, device=dev)
+        self.cnt_dev = torch.empty(world, El, dtype=i32, device=dev)
+        self.cnt_host = torch.empty(world, El, dtype=i32, pin_memory=True)
+        self.prec_local = torch.zeros(El, dtype=u8, device=dev)
+        self.a_bf16 = torch.empty(self.rows_cap, H, dtype=bf, device=dev)
+        self.h_bf16 = torch.empty(self.rows_cap, I, dtype=bf, device=dev)
+        self.rows_out = torch.empty(self.rows_cap, H, dtype=bf, device=dev)
+        self.flag = torch.zeros(1, dtype=i32, device=dev)
+        self.quant_max_ctas = quant_max_ctas
+        self.side = torch.cuda.Stream(device=dev)
+        self._fp4 = None
+
+    def _fp4_ws(self):
+        if self._fp4 is None:
+            El, H, I, R = self.El, self.H, self.I, self.rows_cap
+            u8, dev = torch.uint8, self.dev
+            self._fp4 = dict(
+                a_codes=torch.empty(R, H // 2, dtype=u8, device=dev),
+                a_sf=torch.empty(R * H // 16, dtype=u8, device=dev),
+                h_codes=torch.empty(R, I // 2, dtype=u8, device=dev),
+                h_sf=torch.empty(R * I // 16, dtype=u8, device=dev),
+                wgu_codes=torch.empty(El * 2 * I, H // 2, dtype=u8, device=dev),
+                wgu_sf=torch.empty(El * 2 * I * H // 16, dtype=u8, device=dev),
+                wd_codes=torch.empty(El * H, I // 2, dtype=u8, device=dev),
+                wd_sf=torch.empty(El * H * I // 16, dtype=u8, device=dev),
+            )
+        return self._fp4
+
+    # K1+K2 and the local counts
+    def route(self, x, mod):
+        T = x.shape[0]
+        s, sp = self.s, _lib.stream_ptr()
+        _lib.call("realb_router_topk_stats", x.data_ptr(), self.router.data_ptr(), _lib.ptr(self.bias),
+                  mod.data_ptr(), T, self.H, self.E, self.k, s.scoring, float(s.routed_scaling),
+                  float(s.norm_min), self.logits.data_ptr(), self.topk_idx.data_ptr(),
+                  self.topk_w.data_ptr(), self.cc.data_ptr(), sp)
+        _lib.call("realb_moe_align", self.cc.data_ptr(), (T + 127) // 128, self.E, self.zero_prec.data_ptr(),
+                  1, self.send_layout.data_ptr(), self.vt_local.data_ptr(), sp)
+        return self.topk_idx[:T], self.topk_w[:T], self.vt_local
+
+    # rows sorted by global expert id (unpadded) -> rank-contiguous send buffer
+    def pack(self, x, topk_idx):
+        T = x.shape[0]
+        _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, self.H, self.E,
+                  self.k, self.zero_prec.data_ptr(), self.send_layout.data_ptr(), (T + 127) // 128,
+                  T * self.k, self.send_pos.data_ptr(), self.send_buf.data_ptr(), None, None,
+                  self.flag.data_ptr(), _lib.stream_ptr())
+        return self.send_buf, self.send_pos[:T]
+
+    def quantize_local_weights_async(self):
+        ws = self._fp4_ws()
+        main = torch.cuda.current_stream()
+        self.side.wait_stream(main)
+        with torch.cuda.stream(self.side):
+            sp = _lib.stream_ptr(self.side)
+            El, H, I = self.El, self.H, self.I
+            _lib.call("realb_quantize_nvfp4", self.local.w_gu.data_ptr(), _lib.DT_BF16, El * 2 * I, H,
+                      ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), _lib.SF_MMA128x4,
+                      self.flag.data_ptr(), self.quant_max_ctas, sp)
+            _lib.call("realb_quantize_nvfp4", self.local.w_d.data_ptr(), _lib.DT_BF16, El * H, I,
+                      ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), _lib.SF_MMA128x4,
+                      self.flag.data_ptr(), self.quant_max_ctas, sp)
+
+    def recv_buffer(self):
+        return self.recv_buf
+
+    # regroup received rows + local expert MLPs
+    def expert_compute(self, recv_buf, cnt: np.ndarray, w4a4: bool):
+        El, H, I = self.El, self.H, self.I
+        n = int(cnt.sum())
+        sp = _lib.stream_ptr()
+        self.cnt_host.numpy()[:] = cnt
+        self.cnt_dev.copy_(self.cnt_host, non_blocking=True)
+        self.prec_local.fill_(_lib.PREC_W4A4 if w4a4 else _lib.PREC_W16A16)
+        _lib.call("realb_ep_regroup", self.cnt_dev.data_ptr(), self.R, El, self.prec_local.data_ptr(), n,
+                  self.local_layout.data_ptr(), self.base.data_ptr(), self.row_expert.data_ptr(),
+                  self.row_pos.data_ptr(), sp)
+        ws = self._fp4_ws() if w4a4 else None
+        _lib.call("realb_gather_rows", recv_buf.data_ptr(), self.row_expert.data_ptr(), self.row_pos.data_ptr(),
+                  n, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(),
+                  _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
+                  self.flag.data_ptr(), sp)
+        lay = self.local_layout.data_ptr()
+        if not w4a4:
+            _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.local.w_gu.data_ptr(),
+                      self.rows_cap, 2 * I, H, El, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                      self.h_bf16.data_ptr(), 0, sp)
+            _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.local.w_d.data_ptr(),
+                      self.rows_cap, H, I, El, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
+                      self.rows_out.data_ptr(), 0, sp)
+        else:
+            torch.cuda.current_stream().wait_stream(self.side)
+            _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
+                      ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, El,
+                      lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
+            _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+                      ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
+                      _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+        _lib.call("realb_index_rows", self.rows_out.data_ptr(), self.row_pos.data_ptr(), n, H,
+                  self.back_buf.data_ptr(), sp)
+        return self.back_buf
+
+    def ret_buffer(self):
+        return self.ret_buf
+
+    def combine(self, ret_buf, send_pos, topk_w):
+        T = send_pos.shape[0]
+        y = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.dev)
+        _lib.call("realb_combine", ret_buf.data_ptr(), self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+                  T, self.H, self.k, y.data_ptr(), _lib.stream_ptr())
+        return y
+
+
+# ----------------------------------------------------------------------------- the EP layer
+class EPMoELayer:
+    """One EP rank of a ReaLB MoE layer (host orchestration, backend-agnostic)."""
+
+    def __init__(self, shape: MoEShape, comm: EPComm, ops):
+        if shape.num_experts % comm.world:
+            raise ValueError("experts must divide evenly over the EP ranks")
+        self.shape, self.comm, self.ops = shape, comm, ops
+        self.R, self.rank = comm.world, comm.rank
+        self.El = shape.num_experts // self.R
+        self.cluster = ClusterConfig(self.R, 1, self.El, 1, shape.modality_isolated)
+
+    def forward(self, x, mod, strategy: str = "realb", params: RealbParams | None = None):
+        R, r, El, E = self.R, self.rank, self.El, self.shape.num_experts
+        topk_idx, topk_w, vt_local = self.ops.route(x, mod)
+        vt_all = self.comm.all_gather_counts(vt_local)                      # C1 (host sync)
+        plan = plan_for(strategy, rank_loads_from_counts(vt_all.sum(0), self.cluster), self.cluster,
+                        params or RealbParams())                             # P1
+        w4a4 = plan.per_rank_precision[r] is Precision.W4A4
+        send_counts = vt_all[r].reshape(R, El, 2).sum(axis=(1, 2))
+        cnt = vt_all[:, r * El:(r + 1) * El, :].sum(axis=2)                 # [R, El]
+        recv_counts = cnt.sum(axis=1)
+        send_buf, send_pos = self.ops.pack(x, topk_idx)
+        if w4a4:
+            self.ops.quantize_local_weights_async()                          # K3 under C2
+        recv_buf = self.comm.all_to_all_rows(self.ops.recv_buffer(), send_buf, recv_counts, send_counts)
+        back = self.ops.expert_compute(recv_buf, cnt, w4a4)
+        ret = self.comm.all_to_all_rows(self.ops.ret_buffer(), back, send_counts, recv_counts)  # C3
+        y = self.ops.combine(ret, send_pos, topk_w)
+        return y, plan, vt_all
+
+
+def split_weights(shape: MoEShape, router, gate_up_hf, down_hf, rank: int, world: int, bias=None,
+                  device="cuda") -> MoEWeights:
+    """The local experts' weights of an EP rank (contiguous placement)."""
+    from dataclasses import replace
+
+    El = shape.num_experts // world
+    sl = slice(rank * El, (rank + 1) * El)
+    local_shape = replace(shape, num_experts=El)
+    return MoEWeights.from_hf(local_shape, router[:El], gate_up_hf[sl], down_hf[sl], device=device)
+
+
+# ----------------------------------------------------------------------------- bench (N > 1)
+def run_bench(args):
+    """bench.py under torchrun: one rank per GPU, NCCL, weak scaling (tokens/GPU fixed)."""
+    import json
+
+    from .moe import SHAPES
+    from .workload import WorkloadSpec, make_batch, make_experts
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    shape = SHAPES[args.config]
+    T = args.tokens
+    spec = WorkloadSpec(tokens=T, vision_frac=args.vision_frac, num_ranks=world, rank=rank)
+    x, mod, router, _ = make_batch(shape, spec)
+    gu, dn = make_experts(shape)  # same seed on every rank: identical global weights
+    bias = torch.zeros(shape.num_experts, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
+    local = split_weights(shape, router, gu, dn, rank, world)
+    del gu, dn
+    comm = EPComm()
+    ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
+    layer = EPMoELayer(shape, comm, ops)
+
+    def timed(strategy):
+        for _ in range(args.warmup):
+            layer.forward(x, mod, strategy)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            layer.forward(x, mod, strategy)
+        e.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([s.elapsed_time(e)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / args.steps
+
+    _lib.launch_count = 0
+    ms = timed("realb")
+    launches = _lib.launch_count * args.steps // (args.steps + args.warmup)
+    ms_bf16 = timed("baseline")
+    _, plan, vt_all = layer.forward(x, mod, "realb")
+    if rank == 0:
+        out = {"metric": "MoE-layer prefill tokens/s and speedup vs all-BF16 EP at 1/2/4/8 B200",
+               "value": world * T / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16 (nvfp4 on W4A4 ranks)", "data": "synthetic",
+               "config": {"workload": f"{shape.name} MoE layer prefill, {T} tokens/GPU, EP{world}",
+                          "strategy": "realb", "ep_ranks": world, "tokens_per_gpu": T,
+                          "parallelism": f"ep{world}"},
+               "speedup_vs_bf16": ms_bf16 / ms, "ms_per_step_bf16": ms_bf16,
+               "plan_w4a4_ranks": sorted(plan.accelerated_ranks),
+               "rank_pairs": vt_all.sum(0).reshape(world, -1, 2).sum(axis=(1, 2)).tolist(),
+               "gpu_launches": int(launches)}
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()

@@ -269,10 +269,10 @@ class MoELayer:
                   self.topk_idx.data_ptr(), self.topk_w.data_ptr(), self.chunk_counts.data_ptr(),
                   _lib.stream_ptr())
 
-    def align(self, T: int):
+    def align(self, T: int, row_align: int = 128):
         _lib.call("realb_moe_align", self.chunk_counts.data_ptr(), (T + 127) // 128, self.E,
-                  self.prec_dev.data_ptr(), self.layout.data_ptr(), self.expert_vt.data_ptr(),
-                  _lib.stream_ptr())
+                  self.prec_dev.data_ptr(), row_align, self.layout.data_ptr(),
+                  self.expert_vt.data_ptr(), _lib.stream_ptr())
 
     def align_plan(self, T: int, strategy: str, params: RealbParams):
         """Expert totals + the precision plan evaluated on the device (no sync)."""

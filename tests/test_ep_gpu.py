@@ -1,0 +1,85 @@
+"""EP layer with the real sm_100a kernels: two processes share cuda:0 and
+exchange through gloo staged via the host (NCCL needs distinct GPUs; the box
+has one). The EP result must equal the single-GPU MoELayer run on the union of
+both ranks' tokens with the plan over 2 (virtual) ranks — every kernel is
+row-independent, so the match is exact."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _setup(shape_name, E, T, world, rank, device="cuda"):
+    from dataclasses import replace
+
+    from paper_2604_19503_b200.moe import SHAPES
+    from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts
+
+    shape = replace(SHAPES[shape_name], num_experts=E)
+    x, mod, router, _ = make_batch(shape, WorkloadSpec(tokens=T, num_ranks=world, rank=rank), device=device)
+    gu, dn = make_experts(shape, device=device)
+    return shape, x, mod, router, gu, dn
+
+
+def _worker(rank, world, port, shape_name, E, T, strategy, outdir):
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "tests")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_19503_b200 import _lib
+    from paper_2604_19503_b200.ep import CudaEPOps, EPComm, EPMoELayer, split_weights
+    from paper_2604_19503_b200.policy import RealbParams
+
+    shape, x, mod, router, gu, dn = _setup(shape_name, E, T, world, rank)
+    bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
+    local = split_weights(shape, router, gu, dn, rank, world)
+    ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
+    layer = EPMoELayer(shape, EPComm(staged=True), ops)
+    y, plan, vt = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+    torch.cuda.synchronize()
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), y=y.float().cpu().numpy(),
+             acc=np.array(sorted(plan.accelerated_ranks), dtype=np.int64))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape_name,E,T,strategy", [("tiny", 8, 512, "realb"), ("kimi", 16, 384, "realb"),
+                                                     ("qwen", 16, 256, "fp4all"), ("kimi", 16, 384, "baseline")])
+def test_ep2_on_one_gpu_equals_single_gpu_layer(tmp_path, shape_name, E, T, strategy):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, str(tmp_path)), nprocs=world)
+    from paper_2604_19503_b200 import _lib
+    from paper_2604_19503_b200.moe import MoELayer, MoEWeights
+    from paper_2604_19503_b200.policy import ClusterConfig, RealbParams
+
+    parts = [_setup(shape_name, E, T, world, r) for r in range(world)]
+    shape, _, _, router, gu, dn = parts[0]
+    x = torch.cat([p[1] for p in parts])
+    mod = torch.cat([p[2] for p in parts])
+    bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
+    single = MoELayer(MoEWeights.from_hf(shape, router, gu, dn, bias=bias), max_tokens=world * T,
+                      cluster=ClusterConfig(world, 1, E // world, 1, shape.modality_isolated))
+    res = single.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+    ref = res.y.float().cpu().numpy()
+    r = [np.load(tmp_path / f"r{i}.npz") for i in range(world)]
+    y = np.concatenate([a["y"] for a in r])
+    assert list(r[0]["acc"]) == sorted(res.plan.accelerated_ranks)
+    np.testing.assert_array_equal(y, ref)
