@@ -26,19 +26,33 @@ struct SmemBf16 {
   static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int B_BYTES = BN * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;       // 4 warps x 2 x (32 rows x 64 B)
+  static constexpr int EPI_BYTES = 4 * 2 * 2048;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // + barriers/slots + alignment slack
 };
+
+constexpr int kTileRing = 4;  // depth of the dynamic tile-id ring (producer -> MMA/epilogue)
 
 __device__ __forceinline__ float silu_mul(float g, float u) {
   return g / (1.0f + __expf(-g)) * u;
 }
 
+// 32 rows x 32 bf16 (64 B) staging chunk, TMA SWIZZLE_64B layout: the 16-B piece
+// c of row r lives at piece c ^ ((r >> 1) & 3) -> conflict-free 16-B smem stores.
+__device__ __forceinline__ void stage_row64(uint32_t buf, int r, const uint32_t (&p)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    st_shared_v4(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4), p[4 * c], p[4 * c + 1], p[4 * c + 2],
+                 p[4 * c + 3]);
+}
+
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA,
-                             const __grid_constant__ CUtensorMap tmB, const int32_t* layout,
-                             int E, int prec, int N, int K, __nv_bfloat16* __restrict__ out) {
+                             const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmOut, const int32_t* layout,
+                             int E, int prec, int N, int K) {
   using S = SmemBf16<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -47,7 +61,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* slot_full = tempty + 2;
+  uint64_t* slot_empty = slot_full + kTileRing;
+  int32_t* slot_tile = reinterpret_cast<int32_t*>(slot_empty + kTileRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_tile + kTileRing);
 
   const int warp = warp_id(), lane = lane_id();
   const GroupedSched sched = GroupedSched::make(layout, E, prec, N, BN);
@@ -57,6 +74,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmOut);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -64,6 +82,10 @@ __global__ void __launch_bounds__(256, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
+    }
+    for (int i = 0; i < kTileRing; ++i) {
+      mbar_init(&slot_full[i], 1);
+      mbar_init(&slot_empty[i], 5);  // MMA thread + 4 epilogue warps
     }
     fence_barrier_init();
   }
@@ -74,10 +96,18 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer + dynamic tile fetch
+      int* ctr = GroupedSched::counters(layout, prec);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int i = 0;; ++i) {
+        const int slot = i % kTileRing;
+        mbar_wait(&slot_empty[slot], ((i / kTileRing) & 1) ^ 1);
+        int t = atomicAdd(ctr, 1);
+        if (t >= total) t = -1;
+        slot_tile[slot] = t;
+        mbar_arrive(&slot_full[slot]);
+        if (t < 0) break;
         const TileCoord c = sched.coord(t);
         const int brow = c.group * N + c.n0;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -95,10 +125,14 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc = idesc_bf16(kBM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+      for (int i = 0;; ++i) {
+        const int slot = i % kTileRing;
+        mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
+        const int t = slot_tile[slot];
+        mbar_arrive(&slot_empty[slot]);
+        if (t < 0) break;
+        const int acc = i & 1;
+        const uint32_t acc_phase = (i >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t dtmem = tmem_base + acc * BN;
@@ -120,72 +154,85 @@ __global__ void __launch_bounds__(256, 1)
         tc_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue
-    const int q = warp & 3;  // TMEM lane quadrant
-    const int row_in_tile = q * 32 + lane;
-    int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+  } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> smem -> TMA store
+    const int q = warp & 3;  // TMEM lane quadrant = 32-row slice of the tile
+    const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + q * 4096);
+    int nbuf = 0;
+    for (int i = 0;; ++i) {
+      const int slot = i % kTileRing;
+      mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
+      const int t = slot_tile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[slot]);
+      if (t < 0) break;
       const TileCoord c = sched.coord(t);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
+      const int acc = i & 1;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
-      const int64_t r = (int64_t)c.a_row + row_in_tile;
-      if constexpr (EPI == REALB_EPI_STORE) {
-        __nv_bfloat16* orow = out + r * N + c.n0;
+      const int row0 = c.a_row + q * 32;
+      constexpr int NCH = EPI == REALB_EPI_STORE ? BN / 32 : BN / 64;
 #pragma unroll 1
-        for (int cc = 0; cc < BN; cc += 32) {
+      for (int ch = 0; ch < NCH; ++ch) {
+        uint32_t p[16];
+        if constexpr (EPI == REALB_EPI_STORE) {
           uint32_t v[32];
-          tmem_ld32(tbase + cc, v);
+          tmem_ld32(tbase + ch * 32, v);
           tmem_wait_ld();
-          uint32_t p[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            p[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            st_global_v4(orow + cc + 8 * i, p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
-        }
-      } else {  // SwiGLU: columns [0, BN/2) gate, [BN/2, BN) up of the same outputs
-        const int NO = N / 2;
-        __nv_bfloat16* orow = out + r * NO + c.n0 / 2;
-#pragma unroll 1
-        for (int cc = 0; cc < BN / 2; cc += 16) {
-          uint32_t g[16], u[16];
-          tmem_ld16(tbase + cc, g);
-          tmem_ld16(tbase + BN / 2 + cc, u);
+          for (int j = 0; j < 16; ++j)
+            p[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        } else {  // SwiGLU: gate columns [0, BN/2), up columns [BN/2, BN) of the same outputs
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + ch * 32, g);
+          tmem_ld32(tbase + BN / 2 + ch * 32, u);
           tmem_wait_ld();
-          uint32_t p[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            p[i] = pack_bf16x2(silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i])),
-                               silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1])));
-          st_global_v4(orow + cc, p[0], p[1], p[2], p[3]);
-          st_global_v4(orow + cc + 8, p[4], p[5], p[6], p[7]);
+          for (int j = 0; j < 16; ++j)
+            p[j] = pack_bf16x2(silu_mul(__uint_as_float(g[2 * j]), __uint_as_float(u[2 * j])),
+                               silu_mul(__uint_as_float(g[2 * j + 1]), __uint_as_float(u[2 * j + 1])));
         }
+        // the buffer about to be reused must have been read out by its TMA store
+        if (lane == 0) bulk_wait_group_read<1>();
+        __syncwarp();
+        const uint32_t buf = ebuf + nbuf * 2048;
+        stage_row64(buf, lane, p);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int col = EPI == REALB_EPI_STORE ? c.n0 + ch * 32 : c.n0 / 2 + ch * 32;
+          tma_store_2d(&tmOut, smem + S::EPI_OFF + q * 4096 + nbuf * 2048, col, row0);
+          bulk_commit_group();
+        }
+        nbuf ^= 1;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait_group<0>();  // all stores of this CTA complete
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<2 * BN>(tmem_base);
+  if (threadIdx.x == 0) GroupedSched::finish(layout, prec);
 }
 
 template <int BN, int STAGES, int EPI>
 static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, int N, int K, int E,
                                const int32_t* layout, int prec, void* out, int max_ctas,
                                cudaStream_t st) {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, to;
   int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a, K, rows_cap, (uint64_t)K * 2, kBK,
                         kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, K, (uint64_t)E * N, (uint64_t)K * 2,
                     kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  const int NO = EPI == REALB_EPI_STORE ? N : N / 2;
+  rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, NO, rows_cap, (uint64_t)NO * 2, 32,
+                    32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
   auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI>;
   const int smem = SmemBf16<BN, STAGES>::TOTAL;
@@ -194,8 +241,7 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   if (rc) return rc;
   int grid = num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, 256, smem, st>>>(ta, tb, layout, E, prec, N, K,
-                                reinterpret_cast<__nv_bfloat16*>(out));
+  kern<<<grid, 256, smem, st>>>(ta, tb, to, layout, E, prec, N, K);
   return check_launch("realb_grouped_gemm_bf16");
 }
 

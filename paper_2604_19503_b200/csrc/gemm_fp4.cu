@@ -39,6 +39,7 @@ struct SmemFp4 {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 constexpr uint32_t kTmemAcc = 0, kTmemSf = 256, kTmemSfStride = 48;
+constexpr int kF4Ring = 4;
 
 struct Fp4Args {
   const uint8_t* a_sf;
@@ -49,6 +50,7 @@ struct Fp4Args {
   uint8_t* out_codes;   // SWIGLU: E2M1 [rows][N/4]
   uint8_t* out_sf;      // SWIGLU: MMA-layout scales of the [rows][N/2] result
   uint32_t sf_lbo, sf_sbo;
+  uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies
 };
 
 __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -72,7 +74,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   uint64_t* empty = full + kF4Stages;
   uint64_t* tfull = empty + kF4Stages;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* slot_full = tempty + 1;
+  uint64_t* slot_empty = slot_full + kF4Ring;
+  int32_t* slot_tile = reinterpret_cast<int32_t*>(slot_empty + kF4Ring);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_tile + kF4Ring);
 
   const int warp = warp_id(), lane = lane_id();
   const int N = args.N, K = args.K;
@@ -91,6 +96,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 8);
+    for (int i = 0; i < kF4Ring; ++i) {
+      mbar_init(&slot_full[i], 1);
+      mbar_init(&slot_empty[i], 9);  // MMA thread + 8 epilogue warps
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -100,10 +109,18 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer
+    if (lane == 0) {  // ---------------- producer + dynamic tile fetch
+      int* ctr = GroupedSched::counters(args.layout, REALB_PREC_W4A4);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int i = 0;; ++i) {
+        const int slot = i % kF4Ring;
+        mbar_wait(&slot_empty[slot], ((i / kF4Ring) & 1) ^ 1);
+        int t = atomicAdd(ctr, 1);
+        if (t >= total) t = -1;
+        slot_tile[slot] = t;
+        mbar_arrive(&slot_full[slot]);
+        if (t < 0) break;
         const TileCoord c = sched.coord(t);
         const int brow = c.group * N + c.n0;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -135,8 +152,12 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
       int stage = 0;
       uint32_t phase = 0, sfsel = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
+        const int slot = it % kF4Ring;
+        mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
+        const int t = slot_tile[slot];
+        mbar_arrive(&slot_empty[slot]);
+        if (t < 0) break;
         mbar_wait(tempty, (it & 1) ^ 1);
         tc_fence_after();
         for (int kb = 0; kb < nkb; ++kb) {
@@ -147,7 +168,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           const uint32_t sa = smem_u32(smem + stage * S::STAGE);
           const uint32_t sb = sa + S::A_BYTES, ssfa = sb + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
           const uint32_t tsf = tmem_base + kTmemSf + sfsel * kTmemSfStride;
-          for (int j = 0; j < nmma; ++j) {
+          for (int j = 0; j < nmma && !(args.dbg & 2u); ++j) {
             utccp_32x128b_warpx4(tsf + 4 * j, sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
             utccp_32x128b_warpx4(tsf + 16 + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
             utccp_32x128b_warpx4(tsf + 20 + 8 * j,
@@ -167,8 +188,13 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   } else if (warp >= 4) {  // ---------------- epilogue (8 warps)
     const int q = warp & 3, half = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
-    int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int slot = it % kF4Ring;
+      mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
+      const int t = slot_tile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[slot]);
+      if (t < 0) break;
       const TileCoord c = sched.coord(t);
       mbar_wait(tfull, it & 1);
       tc_fence_after();
@@ -187,6 +213,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);  // accumulator free: next mainloop may start
+      if (args.dbg & 1u) continue;
       const int64_t r = (int64_t)c.a_row + row_in_tile;
       if constexpr (EPI == REALB_EPI_SWIGLU) {
         // outputs [n0/2 + half*64, +64): h = bf16(silu(g) * u), then NVFP4
@@ -202,7 +229,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             const int col = b * 16 + i;  // 0..63
             const float g = __uint_as_float(v[col >> 5][col & 31]);
             const float u = __uint_as_float(v[2 + (col >> 5)][col & 31]);
-            h[i] = __bfloat162float(__float2bfloat16_rn(g / (1.0f + __expf(-g)) * u));
+            h[i] = __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u));
           }
           uint32_t sb;
           cw[b] = quant_block16_bf16vals(h, sb);
@@ -233,6 +260,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<512>(tmem_base);
+  if (threadIdx.x == 0) GroupedSched::finish(args.layout, REALB_PREC_W4A4);
 }
 
 static uint32_t env_u32(const char* name, uint32_t dflt) {
@@ -263,6 +291,7 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   args.out_sf = out_sf;
   args.sf_lbo = env_u32("REALB_DBG_SF_LBO", 128);
   args.sf_sbo = env_u32("REALB_DBG_SF_SBO", 128);
+  args.dbg = env_u32("REALB_DBG_FP4", 0);
   auto kern = grouped_gemm_fp4_kernel<EPI>;
   const int smem = SmemFp4::TOTAL;
   rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),

@@ -39,6 +39,22 @@ struct GroupedSched {
     return s;
   }
   __device__ __forceinline__ int total() const { return G > 0 ? prefix[G] * n_tiles : 0; }
+
+  // Dynamic tile fetch: layout words [4 + 2p] (next tile) and [5 + 2p] (CTAs
+  // done) of precision class p are zeroed by the align kernels; the last CTA
+  // to finish re-zeroes them so the next launch on the same layout starts at 0.
+  __device__ __forceinline__ static int* counters(const int32_t* layout, int prec) {
+    return const_cast<int*>(layout) + 4 + 2 * prec;
+  }
+  __device__ __forceinline__ static void finish(const int32_t* layout, int prec) {
+    int* c = counters(layout, prec);
+    __threadfence();
+    if (atomicAdd(c + 1, 1) == (int)gridDim.x - 1) {
+      c[0] = 0;
+      c[1] = 0;
+      __threadfence();
+    }
+  }
   __device__ __forceinline__ TileCoord coord(int t) const {
     const int mt = t / n_tiles, nt = t - mt * n_tiles;
     // largest g with prefix[g] <= mt (groups with zero tiles are skipped naturally)

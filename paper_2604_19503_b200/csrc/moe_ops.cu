@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ 
       run += (s_cnt[i] + ra - 1) / ra * ra;
     }
     layout[0] = run;
+    for (int w = 3; w < 8; ++w) layout[w] = 0;  // GEMM tile counters (grouped.cuh)
     for (int p = 0; p < 2; ++p) {
       int32_t* gl = layout + LayoutView::off_glist(E, p);
       int32_t* pf = layout + LayoutView::off_prefix(E, p);
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t* __restric
       run += (s_tot[i] + 127) / 128 * 128;
     }
     layout[0] = run;
+    for (int w = 3; w < 8; ++w) layout[w] = 0;  // GEMM tile counters (grouped.cuh)
     for (int p = 0; p < 2; ++p) {
       int32_t* gl = layout + LayoutView::off_glist(El, p);
       int32_t* pf = layout + LayoutView::off_prefix(El, p);
