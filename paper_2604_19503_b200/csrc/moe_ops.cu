@@ -57,22 +57,37 @@ __device__ void plan_on_device(const int32_t* ev, int E, const PlanParams& pp, u
   if (plan_out) { plan_out[0] = active; plan_out[1] = nacc; plan_out[2] = R; }
 }
 
-__global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ cc, int nchunks,
-                                                    int E, uint8_t* __restrict__ prec,
-                                                    int32_t* __restrict__ layout,
-                                                    int32_t* __restrict__ expert_vt,
-                                                    PlanParams pp, int32_t* plan_out, int ra) {
+// 1024 threads = E experts x G chunk groups (G = 1024 / E): chunk sums and
+// per-chunk offsets are computed with all threads, the serial part (scan over
+// experts, P1, group lists) by one thread over E <= 256 entries.
+__global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__ cc, int nchunks,
+                                                     int E, uint8_t* __restrict__ prec,
+                                                     int32_t* __restrict__ layout,
+                                                     int32_t* __restrict__ expert_vt,
+                                                     PlanParams pp, int32_t* plan_out, int ra) {
+  __shared__ int32_t s_v[1024], s_t[1024];
   __shared__ int32_t s_cnt[256], s_start[256];
-  const int e = threadIdx.x;
-  if (e < E) {
-    int v = 0, t = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      v += cc[((int64_t)c * E + e) * 2];
-      t += cc[((int64_t)c * E + e) * 2 + 1];
-    }
-    expert_vt[2 * e] = v;
-    expert_vt[2 * e + 1] = t;
-    s_cnt[e] = v + t;
+  const int G = blockDim.x / E;  // chunk groups per expert
+  const int e = threadIdx.x % E, g = threadIdx.x / E;
+  const bool act = g < G;
+  // chunk range of group g (contiguous, for the offset scan)
+  const int per = (nchunks + G - 1) / G;
+  const int c0 = act ? min(nchunks, g * per) : 0, c1 = act ? min(nchunks, c0 + per) : 0;
+  int v = 0, t = 0;
+#pragma unroll 4
+  for (int c = c0; c < c1; ++c) {
+    v += cc[((int64_t)c * E + e) * 2];
+    t += cc[((int64_t)c * E + e) * 2 + 1];
+  }
+  s_v[threadIdx.x] = v;
+  s_t[threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x < E) {
+    int tv = 0, tt = 0;
+    for (int j = 0; j < G; ++j) { tv += s_v[j * E + threadIdx.x]; tt += s_t[j * E + threadIdx.x]; }
+    expert_vt[2 * threadIdx.x] = tv;
+    expert_vt[2 * threadIdx.x + 1] = tt;
+    s_cnt[threadIdx.x] = tv + tt;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -87,25 +102,29 @@ __global__ void __launch_bounds__(256) align_kernel(const int32_t* __restrict__ 
     for (int p = 0; p < 2; ++p) {
       int32_t* gl = layout + LayoutView::off_glist(E, p);
       int32_t* pf = layout + LayoutView::off_prefix(E, p);
-      int g = 0, mt = 0;
+      int gg = 0, mt = 0;
       for (int i = 0; i < E; ++i) {
         if ((int)prec[i] != p) continue;
-        gl[g] = i;
-        pf[g] = mt;
+        gl[gg] = i;
+        pf[gg] = mt;
         mt += (s_cnt[i] + 127) / 128;
-        ++g;
+        ++gg;
       }
-      pf[g] = mt;
-      layout[1 + p] = g;
+      pf[gg] = mt;
+      layout[1 + p] = gg;
     }
   }
   __syncthreads();
-  if (e < E) {
-    layout[LayoutView::off_row_start(E) + e] = s_start[e];
-    layout[LayoutView::off_row_count(E) + e] = s_cnt[e];
-    int32_t* co = layout + LayoutView::off_chunk(E);
+  if (threadIdx.x < E) {
+    layout[LayoutView::off_row_start(E) + threadIdx.x] = s_start[threadIdx.x];
+    layout[LayoutView::off_row_count(E) + threadIdx.x] = s_cnt[threadIdx.x];
+  }
+  if (act) {
+    // exclusive offset of my chunk range within expert e, then per chunk
     int run = s_start[e];
-    for (int c = 0; c < nchunks; ++c) {
+    for (int j = 0; j < g; ++j) run += s_v[j * E + e] + s_t[j * E + e];
+    int32_t* co = layout + LayoutView::off_chunk(E);
+    for (int c = c0; c < c1; ++c) {
       co[(int64_t)c * E + e] = run;
       run += cc[((int64_t)c * E + e) * 2] + cc[((int64_t)c * E + e) * 2 + 1];
     }
@@ -312,24 +331,29 @@ __global__ void __launch_bounds__(256) index_rows_kernel(const __nv_bfloat16* __
 }
 
 // ----------------------------------------------------------------- combine
+template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ rows,
                                                       const int32_t* __restrict__ pos,
                                                       const float* __restrict__ w, int T, int H,
-                                                      int k, __nv_bfloat16* __restrict__ y) {
+                                                      __nv_bfloat16* __restrict__ y) {
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  int64_t p[8];
-  float wt[8];
-  for (int j = 0; j < k; ++j) {
-    p[j] = pos[(int64_t)t * k + j];
-    wt[j] = w[(int64_t)t * k + j];
+  const uint4* src[K];
+  float wt[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    src[j] = reinterpret_cast<const uint4*>(rows + (int64_t)pos[(int64_t)t * K + j] * H);
+    wt[j] = w[(int64_t)t * K + j];
   }
   for (int c = lane; c < H / 8; c += 32) {
+    uint4 u[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) u[j] = __ldg(src[j] + c);  // all K loads in flight
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < k; ++j) {
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(rows + p[j] * H) + c);
-      const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t v[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         acc[2 * i] = fmaf(wt[j], bf16lo(v[i]), acc[2 * i]);
@@ -363,7 +387,7 @@ extern "C" int realb_moe_align(const int32_t* d_cc, int nchunks, int E, const ui
     return REALB_EINVAL;
   }
   PlanParams pp{};
-  align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, const_cast<uint8_t*>(d_prec),
+  align_kernel<<<1, (1024 / E) * E, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, const_cast<uint8_t*>(d_prec),
                                                     d_layout, d_expert_vt, pp, nullptr, row_align);
   return check_launch("realb_moe_align");
 }
@@ -385,7 +409,7 @@ extern "C" int realb_moe_align_plan(const int32_t* d_cc, int nchunks, int E, int
   }
   PlanParams pp{1, strategy, R, modality_isolated, capacity_factor, modality_threshold,
                 (long long)global_batch_threshold};
-  align_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
+  align_kernel<<<1, (1024 / E) * E, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
                                                     d_expert_vt, pp, d_plan_out, 128);
   return check_launch("realb_moe_align_plan");
 }
@@ -423,9 +447,20 @@ extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const flo
     return REALB_EINVAL;
   }
   if (T == 0) return REALB_OK;
-  combine_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(d_rows), d_pos, d_w, T, H, k,
-      reinterpret_cast<__nv_bfloat16*>(d_y));
+  const dim3 grid((T + 7) / 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto r = reinterpret_cast<const __nv_bfloat16*>(d_rows);
+  auto y = reinterpret_cast<__nv_bfloat16*>(d_y);
+  switch (k) {
+    case 1: combine_kernel<1><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
+    case 2: combine_kernel<2><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
+    case 4: combine_kernel<4><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
+    case 6: combine_kernel<6><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
+    case 8: combine_kernel<8><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
+    default:
+      set_error("realb_combine: top-k must be one of 1,2,4,6,8 (k=%d)", k);
+      return REALB_EUNSUPPORTED;
+  }
   return check_launch("realb_combine");
 }
 

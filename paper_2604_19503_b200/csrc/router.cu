@@ -19,7 +19,7 @@
 namespace realb {
 
 constexpr int kRBK = 64;
-constexpr int kRStages = 4;
+
 constexpr int kKMax = 8;
 
 template <int EPAD>
@@ -27,7 +27,10 @@ struct RouterSmem {
   static constexpr int A_BYTES = 128 * kRBK * 2;
   static constexpr int B_BYTES = EPAD * kRBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int HIST_OFF = kRStages * STAGE;
+  // as many stages as fit in ~200 KB: the router is latency-bound per SM (one CTA
+  // per 128 tokens), so bytes in flight set its HBM throughput
+  static constexpr int STAGES = (200 * 1024) / STAGE > 12 ? 12 : (200 * 1024) / STAGE;
+  static constexpr int HIST_OFF = STAGES * STAGE;
   static constexpr int BAR_OFF = HIST_OFF + 256 * 2 * 4;
   static constexpr int TOTAL = BAR_OFF + 128 + 1024;
   static constexpr uint32_t TMEM_COLS = EPAD <= 32 ? 32 : EPAD <= 64 ? 64 : EPAD <= 128 ? 128 : 256;
@@ -46,8 +49,8 @@ __global__ void __launch_bounds__(256, 1)
                                              ~uintptr_t(1023));
   int32_t* hist = reinterpret_cast<int32_t*>(smem + S::HIST_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-  uint64_t* empty = full + kRStages;
-  uint64_t* done = empty + kRStages;
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* done = empty + S::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = warp_id(), lane = lane_id();
@@ -58,7 +61,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmX);
     tma_prefetch_desc(&tmW);
-    for (int s = 0; s < kRStages; ++s) {
+    for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive_expect_tx(&full[stage], S::STAGE);
         tma_load_2d(sa, &tmX, &full[stage], kb * kRBK, chunk * 128);
         tma_load_2d(sa + S::A_BYTES, &tmW, &full[stage], kb * kRBK, 0);
-        if (++stage == kRStages) { stage = 0; phase ^= 1; }
+        if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(256, 1)
           umma_bf16(tmem_base, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
                     (kb | kk) != 0);
         tc_commit(&empty[stage]);
-        if (++stage == kRStages) { stage = 0; phase ^= 1; }
+        if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
       }
       tc_commit(done);
     }
