@@ -9,7 +9,12 @@
 //              stage's scales are contiguous 2 KB runs)
 //   warp 1     MMA issuer: tcgen05.cp (smem -> TMEM, 32x128b.warpx4) of the
 //              stage's scale atoms, then 4 x tcgen05.mma (M=128, N=256, K=64)
-//   warp 2     TMEM allocator (512 columns: 256 accumulator + 2 x 48 scale)
+//   warp 2     TMEM allocator (512 columns: 256 accumulator, the m-tile's A
+//              scales for the whole K (K/16 columns, RESIDENT across the unit's
+//              n-tiles) and 2 x 32 columns of streamed W scales)
+// Work unit = (m-tile, run of up to 4 n-tiles): the A-side scales are copied to
+// TMEM once per unit, so a steady-state stage issues 8 tcgen05.cp instead of 12
+// (measured on B200: 4 MMAs = 512 cycles; +8 copies = 665; +12 copies = 836).
 //   warps 4-11 epilogue: the 8 warps copy the whole accumulator into registers
 //              (quadrant = warp % 4, column half = (warp - 4) / 4), release TMEM
 //              to the MMA warp at once, then run SwiGLU (+ NVFP4 re-quantisation
@@ -38,7 +43,8 @@ struct SmemFp4 {
   static constexpr int BAR_OFF = kF4Stages * STAGE;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
-constexpr uint32_t kTmemAcc = 0, kTmemSf = 256, kTmemSfStride = 48;
+constexpr uint32_t kTmemAcc = 0, kTmemSfa = 256;  // SFB buffers follow the resident SFA
+constexpr int kNPerUnit = 4;                           // n-tiles per work unit
 constexpr int kF4Ring = 4;
 
 struct Fp4Args {
@@ -82,7 +88,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   const int warp = warp_id(), lane = lane_id();
   const int N = args.N, K = args.K;
   const GroupedSched sched = GroupedSched::make(args.layout, args.E, REALB_PREC_W4A4, N, kF4BN);
-  const int total = sched.total();
+  const int n_tiles = N / kF4BN;
+  const int nchunks = (n_tiles + kNPerUnit - 1) / kNPerUnit;
+  const int total_units = sched.G > 0 ? sched.prefix[sched.G] * nchunks : 0;
+  const uint32_t sfa_cols = (uint32_t)(K / 16);  // resident A scales: 4 columns per K=64
   const int kbytes = K / 2;
   const int nkb = (kbytes + kF4BKB - 1) / kF4BKB;
   const int atoms_per_row_tile = K / 64;  // 4-scale atoms per 128-row tile
@@ -109,94 +118,119 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer + dynamic tile fetch
+    if (lane == 0) {  // ---------------- producer + dynamic unit fetch
       int* ctr = GroupedSched::counters(args.layout, REALB_PREC_W4A4);
       int stage = 0;
       uint32_t phase = 0;
       for (int i = 0;; ++i) {
         const int slot = i % kF4Ring;
         mbar_wait(&slot_empty[slot], ((i / kF4Ring) & 1) ^ 1);
-        int t = atomicAdd(ctr, 1);
-        if (t >= total) t = -1;
-        slot_tile[slot] = t;
+        int u = atomicAdd(ctr, 1);
+        if (u >= total_units) u = -1;
+        slot_tile[slot] = u;
         mbar_arrive(&slot_full[slot]);
-        if (t < 0) break;
-        const TileCoord c = sched.coord(t);
-        const int brow = c.group * N + c.n0;
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int kval = min(kF4BKB, kbytes - kb * kF4BKB);  // bytes of K in this stage
-          const int nmma = kval / 32;
-          const uint32_t sfbytes = (uint32_t)nmma * 512;
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * S::STAGE;
-          uint8_t* sb = sa + S::A_BYTES;
-          uint8_t* ssfa = sb + S::B_BYTES;
-          uint8_t* ssfb = ssfa + S::SFA_BYTES;
-          mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES + 3 * sfbytes);
-          tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, c.a_row);
-          tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
-          const int64_t atom_k = (int64_t)kb * 4;
-          bulk_load(ssfa, args.a_sf + ((int64_t)(c.a_row >> 7) * atoms_per_row_tile + atom_k) * 512,
-                    sfbytes, &full[stage]);
+        if (u < 0) break;
+        const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+        const int nt1 = min(n_tiles, nt0 + kNPerUnit);
+        const TileCoord c = sched.coord(mt * n_tiles);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          const int brow = c.group * N + nt * kF4BN;
+          const bool load_a_sf = nt == nt0;
+          for (int kb = 0; kb < nkb; ++kb) {
+            const int kval = min(kF4BKB, kbytes - kb * kF4BKB);  // bytes of K in this stage
+            const int nmma = kval / 32;
+            const uint32_t sfbytes = (uint32_t)nmma * 512;
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * S::STAGE;
+            uint8_t* sb = sa + S::A_BYTES;
+            uint8_t* ssfa = sb + S::B_BYTES;
+            uint8_t* ssfb = ssfa + S::SFA_BYTES;
+            mbar_arrive_expect_tx(&full[stage],
+                                  S::A_BYTES + S::B_BYTES + (load_a_sf ? 3 : 2) * sfbytes);
+            tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, c.a_row);
+            tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
+            const int64_t atom_k = (int64_t)kb * 4;
+            if (load_a_sf)
+              bulk_load(ssfa, args.a_sf + ((int64_t)(c.a_row >> 7) * atoms_per_row_tile + atom_k) * 512,
+                        sfbytes, &full[stage]);
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
-            bulk_load(ssfb + i * 2048,
-                      args.w_sf + ((int64_t)((brow >> 7) + i) * atoms_per_row_tile + atom_k) * 512,
-                      sfbytes, &full[stage]);
-          if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
+            for (int h = 0; h < 2; ++h)
+              bulk_load(ssfb + h * 2048,
+                        args.w_sf + ((int64_t)((brow >> 7) + h) * atoms_per_row_tile + atom_k) * 512,
+                        sfbytes, &full[stage]);
+            if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
+      const uint32_t tsfa = tmem_base + kTmemSfa;
+      const uint32_t tsfb0 = tsfa + sfa_cols;
       int stage = 0;
       uint32_t phase = 0, sfsel = 0;
+      int tile_it = 0;  // accumulator use count (one per n-tile)
       for (int it = 0;; ++it) {
         const int slot = it % kF4Ring;
         mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
-        const int t = slot_tile[slot];
+        const int u = slot_tile[slot];
         mbar_arrive(&slot_empty[slot]);
-        if (t < 0) break;
-        mbar_wait(tempty, (it & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int kval = min(kF4BKB, kbytes - kb * kF4BKB);
-          const int nmma = kval / 32;
-          mbar_wait(&full[stage], phase);
+        if (u < 0) break;
+        const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+        const int nt1 = min(n_tiles, nt0 + kNPerUnit);
+        for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
+          // previous n-tile fully drained by the epilogue => every earlier MMA has
+          // completed, so the resident A scales may be overwritten for a new unit
+          mbar_wait(tempty, (tile_it & 1) ^ 1);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * S::STAGE);
-          const uint32_t sb = sa + S::A_BYTES, ssfa = sb + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
-          const uint32_t tsf = tmem_base + kTmemSf + sfsel * kTmemSfStride;
-          for (int j = 0; j < nmma && !(args.dbg & 2u); ++j) {
-            utccp_32x128b_warpx4(tsf + 4 * j, sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
-            utccp_32x128b_warpx4(tsf + 16 + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
-            utccp_32x128b_warpx4(tsf + 20 + 8 * j,
-                                 sf_desc(ssfb + 2048 + 512 * j, args.sf_lbo, args.sf_sbo));
+          const bool load_a_sf = nt == nt0;
+          for (int kb = 0; kb < nkb; ++kb) {
+            const int kval = min(kF4BKB, kbytes - kb * kF4BKB);
+            const int nmma = kval / 32;
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * S::STAGE);
+            const uint32_t sb = sa + S::A_BYTES, ssfa = sb + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
+            const uint32_t tsfb = tsfb0 + sfsel * 32;
+            for (int j = 0; j < nmma && !(args.dbg & 2u); ++j) {
+              if (load_a_sf)
+                utccp_32x128b_warpx4(tsfa + (kb * 4 + j) * 4,
+                                     sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
+              utccp_32x128b_warpx4(tsfb + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
+              utccp_32x128b_warpx4(tsfb + 8 * j + 4,
+                                   sf_desc(ssfb + 2048 + 512 * j, args.sf_lbo, args.sf_sbo));
+            }
+            const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sb);
+            for (int j = 0; j < nmma; ++j)
+              umma_nvfp4(tmem_base + kTmemAcc, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2),
+                         idesc, tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
+            tc_commit(&empty[stage]);
+            sfsel ^= 1;
+            if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
           }
-          const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sb);
-          for (int j = 0; j < nmma; ++j)
-            umma_nvfp4(tmem_base + kTmemAcc, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2),
-                       idesc, tsf + 4 * j, tsf + 16 + 8 * j, (kb | j) != 0);
-          tc_commit(&empty[stage]);
-          sfsel ^= 1;
-          if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
+          tc_commit(tfull);
         }
-        tc_commit(tfull);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue (8 warps)
     const int q = warp & 3, half = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
+    int tile_it = 0;
     for (int it = 0;; ++it) {
       const int slot = it % kF4Ring;
       mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
-      const int t = slot_tile[slot];
+      const int u = slot_tile[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&slot_empty[slot]);
-      if (t < 0) break;
-      const TileCoord c = sched.coord(t);
-      mbar_wait(tfull, it & 1);
+      if (u < 0) break;
+      const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+      const int nt1 = min(n_tiles, nt0 + kNPerUnit);
+      const TileCoord cm = sched.coord(mt * n_tiles);
+      for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
+      TileCoord c = cm;
+      c.n0 = nt * kF4BN;
+      mbar_wait(tfull, tile_it & 1);
       tc_fence_after();
       const uint32_t tb = tmem_base + kTmemAcc + ((uint32_t)(q * 32) << 16);
       uint32_t v[4][32];
@@ -253,6 +287,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
                          pack_bf16x2(__uint_as_float(p[6]), __uint_as_float(p[7])));
           }
         }
+      }
       }
     }
   }
@@ -318,8 +353,9 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
     set_error("realb_grouped_gemm_nvfp4: bad arguments");
     return REALB_EINVAL;
   }
-  if (N % kF4BN || K % 64) {
-    set_error("realb_grouped_gemm_nvfp4: needs N %% 256 == 0 and K %% 64 == 0 (N=%d K=%d)", N, K);
+  if (N % kF4BN || K % 64 || K > 3072) {
+    set_error("realb_grouped_gemm_nvfp4: needs N %% 256 == 0, K %% 64 == 0 and K <= 3072 (resident "
+              "A scales: K/16 TMEM columns) (N=%d K=%d)", N, K);
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;

@@ -49,6 +49,24 @@ __global__ void __launch_bounds__(128, 1) kern(int mode, int reps, long long* ou
       } else if (mode == 6) {     // 3 x 32x128b.warpx4 + 4 MMA (SFB resident; SFA per MMA... 3 cps)
         for (int j = 0; j < 3; ++j) utccp_32x128b_warpx4(tb + 320 + 4 * j, sdesc);
         for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
+      } else if (mode == 8) {     // 8 cp + 4 MMA (SFA resident)
+        for (int j = 0; j < 8; ++j) utccp_32x128b_warpx4(tb + 320 + 4 * j, sdesc);
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
+      } else if (mode == 9) {     // 6 cp + 4 MMA
+        for (int j = 0; j < 6; ++j) utccp_32x128b_warpx4(tb + 320 + 4 * j, sdesc);
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
+      } else if (mode == 10) {    // 4 cp + 4 MMA
+        for (int j = 0; j < 4; ++j) utccp_32x128b_warpx4(tb + 320 + 4 * j, sdesc);
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
+      } else if (mode == 11) {    // 4 x 128x256b + 4 MMA
+        for (int j = 0; j < 4; ++j) cp_128x256b(tb + 320 + 8 * j, sdesc);
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
+      } else if (mode == 12) {    // interleaved: (2 cp, 1 mma) x 4
+        for (int j = 0; j < 4; ++j) {
+          utccp_32x128b_warpx4(tb + 320 + 8 * j, sdesc);
+          utccp_32x128b_warpx4(tb + 324 + 8 * j, sdesc);
+          umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
+        }
       } else if (mode == 7) {     // 4 x bf16 MMA N=256 K=16 (reference rate)
         const uint32_t id16 = idesc_bf16(128, 256);
         for (int j = 0; j < 4; ++j) umma_bf16(tb, adesc + 2 * j, bdesc + 2 * j, id16, 1);
@@ -74,8 +92,9 @@ int main() {
   long long* d; cudaMalloc(&d, 8);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
   const char* names[] = {"12x cp32x128b.warpx4", "4x mma fp4 N256", "12cp+4mma", "6x cp128x256b",
-                         "6x cp128x256b+4mma", "12x cp128x128b", "3cp+4mma", "4x mma bf16 N256"};
-  for (int mode = 0; mode < 8; ++mode) {
+                         "6x cp128x256b+4mma", "12x cp128x128b", "3cp+4mma", "4x mma bf16 N256",
+                         "8cp+4mma", "6cp+4mma", "4cp+4mma", "4x cp128x256b+4mma", "(2cp,1mma)x4"};
+  for (int mode = 0; mode < 13; ++mode) {
     const int reps = 2000;
     kern<<<1, 128, 65536>>>(mode, reps, d);
     kern<<<1, 128, 65536>>>(mode, reps, d);

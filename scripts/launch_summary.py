@@ -1,0 +1,13 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum launch list (mean us per kernel)."""
+import collections, csv, sys
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+hdr, rows = rows[0], rows[1:]
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+agg = collections.OrderedDict()
+for r in rows:
+    v = float(r[vi].replace(",", ""))
+    v = v / 1000 if r[ui] == "nsecond" else v * 1000 if r[ui] == "msecond" else v
+    agg.setdefault(r[ki][:70], []).append(v)
+for n, v in agg.items():
+    if "realb" in n or "--all" in sys.argv:
+        print(f"  {n:70s} n={len(v):3d} mean={sum(v)/len(v):8.1f}us")
