@@ -165,12 +165,28 @@ __global__ void __launch_bounds__(kF4Threads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
+      // Scale copies run ONE STAGE AHEAD of the MMAs that consume them, so the
+      // tcgen05.cp latency overlaps the previous stage's MMAs (the copies of a
+      // stage and its MMAs would otherwise serialise on the TMEM dependency).
       constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
       const uint32_t tsfa = tmem_base + kTmemSfa;
       const uint32_t tsfb0 = tsfa + sfa_cols;
       int stage = 0;
-      uint32_t phase = 0, sfsel = 0;
-      int tile_it = 0;  // accumulator use count (one per n-tile)
+      uint32_t phase = 0;
+      int tile_it = 0;   // accumulator use count (one per n-tile)
+      int kiter = 0;     // global k-step counter: SFB buffer = kiter & 1
+      bool pre = false;  // are the current stage's copies already issued?
+      auto issue_copies = [&](int st, int kb, int nmma, bool a_sf, int buf) {
+        const uint32_t sa = smem_u32(smem + st * S::STAGE);
+        const uint32_t ssfa = sa + S::A_BYTES + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
+        const uint32_t tsfb = tsfb0 + buf * 32;
+        for (int j = 0; j < nmma && !(args.dbg & 2u); ++j) {
+          if (a_sf)
+            utccp_32x128b_warpx4(tsfa + (kb * 4 + j) * 4, sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
+          utccp_32x128b_warpx4(tsfb + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
+          utccp_32x128b_warpx4(tsfb + 8 * j + 4, sf_desc(ssfb + 2048 + 512 * j, args.sf_lbo, args.sf_sbo));
+        }
+      };
       for (int it = 0;; ++it) {
         const int slot = it % kF4Ring;
         mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
@@ -180,34 +196,40 @@ __global__ void __launch_bounds__(kF4Threads, 1)
         const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
         const int nt1 = min(n_tiles, nt0 + kNPerUnit);
         for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
-          // previous n-tile fully drained by the epilogue => every earlier MMA has
-          // completed, so the resident A scales may be overwritten for a new unit
+          // previous n-tile drained by the epilogue => every earlier MMA completed,
+          // so the resident A scales may be rewritten at the start of a new unit
           mbar_wait(tempty, (tile_it & 1) ^ 1);
           tc_fence_after();
-          const bool load_a_sf = nt == nt0;
-          for (int kb = 0; kb < nkb; ++kb) {
-            const int kval = min(kF4BKB, kbytes - kb * kF4BKB);
-            const int nmma = kval / 32;
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t sa = smem_u32(smem + stage * S::STAGE);
-            const uint32_t sb = sa + S::A_BYTES, ssfa = sb + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
-            const uint32_t tsfb = tsfb0 + sfsel * 32;
-            for (int j = 0; j < nmma && !(args.dbg & 2u); ++j) {
-              if (load_a_sf)
-                utccp_32x128b_warpx4(tsfa + (kb * 4 + j) * 4,
-                                     sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
-              utccp_32x128b_warpx4(tsfb + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
-              utccp_32x128b_warpx4(tsfb + 8 * j + 4,
-                                   sf_desc(ssfb + 2048 + 512 * j, args.sf_lbo, args.sf_sbo));
+          const bool first_tile = nt == nt0;
+          for (int kb = 0; kb < nkb; ++kb, ++kiter) {
+            const int nmma = min(kF4BKB, kbytes - kb * kF4BKB) / 32;
+            if (!pre) {  // not prefetched (start of a unit): copy now
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              issue_copies(stage, kb, nmma, first_tile, kiter & 1);
             }
-            const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sb);
+            // prefetch the NEXT stage's scales (same unit only; a new unit's first
+            // stage rewrites the resident A scales and must wait for the drain)
+            const int nst = stage + 1 == kF4Stages ? 0 : stage + 1;
+            const uint32_t nph = stage + 1 == kF4Stages ? phase ^ 1 : phase;
+            const bool next_in_unit = kb + 1 < nkb || nt + 1 < nt1;
+            if (next_in_unit) {
+              const int nkb_next = kb + 1 < nkb ? kb + 1 : 0;
+              const int nmma_next = min(kF4BKB, kbytes - nkb_next * kF4BKB) / 32;
+              mbar_wait(&full[nst], nph);
+              tc_fence_after();
+              issue_copies(nst, nkb_next, nmma_next, first_tile && kb + 1 < nkb, (kiter + 1) & 1);
+            }
+            pre = next_in_unit;
+            const uint32_t sa = smem_u32(smem + stage * S::STAGE);
+            const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sa + S::A_BYTES);
+            const uint32_t tsfb = tsfb0 + (kiter & 1) * 32;
             for (int j = 0; j < nmma; ++j)
               umma_nvfp4(tmem_base + kTmemAcc, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2),
                          idesc, tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
             tc_commit(&empty[stage]);
-            sfsel ^= 1;
-            if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
+            stage = nst;
+            phase = nph;
           }
           tc_commit(tfull);
         }
