@@ -95,64 +95,75 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer + dynamic tile fetch
-      int* ctr = GroupedSched::counters(layout, prec);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int i = 0;; ++i) {
-        const int slot = i % kTileRing;
-        mbar_wait(&slot_empty[slot], ((i / kTileRing) & 1) ^ 1);
-        int t = atomicAdd(ctr, 1);
+  // Producer and MMA roles run on their whole warp with warp-uniform values and
+  // one elected lane issuing (see gemm_fp4.cu: lane-0-only code makes ptxas wrap
+  // every tcgen05 instruction in an ELECT/R2UR waterfall loop).
+  if (warp == 0) {  // ---------------- TMA producer + dynamic tile fetch
+    const bool leader = elect_one();
+    int* ctr = GroupedSched::counters(layout, prec);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0;; ++i) {
+      const int slot = i % kTileRing;
+      mbar_wait(&slot_empty[slot], ((i / kTileRing) & 1) ^ 1);
+      int t = 0;
+      if (leader) {
+        t = atomicAdd(ctr, 1);
         if (t >= total) t = -1;
         slot_tile[slot] = t;
         mbar_arrive(&slot_full[slot]);
-        if (t < 0) break;
-        const TileCoord c = sched.coord(t);
-        const int brow = c.group * N + c.n0;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t < 0) break;
+      const TileCoord c = sched.coord(t);
+      const int a_row = __shfl_sync(0xffffffffu, c.a_row, 0);
+      const int brow = __shfl_sync(0xffffffffu, c.group * N + c.n0, 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) {
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * kBK, c.a_row);
+          tma_load_2d(sa, &tmA, &full[stage], kb * kBK, a_row);
           tma_load_2d(sa + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16(kBM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int i = 0;; ++i) {
-        const int slot = i % kTileRing;
-        mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
-        const int t = slot_tile[slot];
-        mbar_arrive(&slot_empty[slot]);
-        if (t < 0) break;
-        const int acc = i & 1;
-        const uint32_t acc_phase = (i >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+  } else if (warp == 1) {  // ---------------- MMA issuer
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t s0 = smem_u32(smem);
+    const uint64_t adesc0 = umma_desc_sw128(s0), bdesc0 = umma_desc_sw128(s0 + S::A_BYTES);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0;; ++i) {
+      const int slot = i % kTileRing;
+      mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
+      const int t = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
+      __syncwarp();
+      if (leader) mbar_arrive(&slot_empty[slot]);
+      if (t < 0) break;
+      const int acc = i & 1;
+      mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dtmem = tbase + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t dtmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * S::STAGE_BYTES);
-          const uint64_t adesc = umma_desc_sw128(sa);
-          const uint64_t bdesc = umma_desc_sw128(sa + S::A_BYTES);
+        const uint64_t soff = (uint64_t)((uint32_t)(stage * S::STAGE_BYTES) >> 4);
+        if (leader) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // advance the start address by 32 B (16 bf16) inside the 128-B swizzle atom
-            umma_bf16(dtmem, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
-                      (kb | k) != 0);
-          }
+          for (int k = 0; k < kBK / 16; ++k)  // +32 B (16 bf16) inside the 128-B swizzle atom
+            umma_bf16(dtmem, adesc0 + soff + 2 * k, bdesc0 + soff + 2 * k, idesc, (kb | k) != 0);
           tc_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (leader) tc_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> smem -> TMA store
     const int q = warp & 3;  // TMEM lane quadrant = 32-row slice of the tile

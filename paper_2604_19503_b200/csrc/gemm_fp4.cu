@@ -117,122 +117,122 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer + dynamic unit fetch
-      int* ctr = GroupedSched::counters(args.layout, REALB_PREC_W4A4);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int i = 0;; ++i) {
-        const int slot = i % kF4Ring;
-        mbar_wait(&slot_empty[slot], ((i / kF4Ring) & 1) ^ 1);
-        int u = atomicAdd(ctr, 1);
+  // Producer and MMA roles run on their WHOLE warp: every lane computes the same
+  // (hence provably warp-uniform) values and one elected lane issues the TMA /
+  // tcgen05 instructions. Issuing from `lane == 0` code makes the compiler wrap
+  // each tcgen05 instruction in an ELECT/R2UR waterfall loop, which made the
+  // single issuing thread, not the tensor pipe, the bottleneck.
+  if (warp == 0) {  // ---------------- producer + dynamic unit fetch
+    const bool leader = elect_one();
+    int* ctr = GroupedSched::counters(args.layout, REALB_PREC_W4A4);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0;; ++i) {
+      const int slot = i % kF4Ring;
+      mbar_wait(&slot_empty[slot], ((i / kF4Ring) & 1) ^ 1);
+      int u = 0;
+      if (leader) {
+        u = atomicAdd(ctr, 1);
         if (u >= total_units) u = -1;
         slot_tile[slot] = u;
         mbar_arrive(&slot_full[slot]);
-        if (u < 0) break;
-        const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
-        const int nt1 = min(n_tiles, nt0 + kNPerUnit);
-        const TileCoord c = sched.coord(mt * n_tiles);
-        for (int nt = nt0; nt < nt1; ++nt) {
-          const int brow = c.group * N + nt * kF4BN;
-          const bool load_a_sf = nt == nt0;
-          for (int kb = 0; kb < nkb; ++kb) {
-            const int kval = min(kF4BKB, kbytes - kb * kF4BKB);  // bytes of K in this stage
-            const int nmma = kval / 32;
-            const uint32_t sfbytes = (uint32_t)nmma * 512;
-            mbar_wait(&empty[stage], phase ^ 1);
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u < 0) break;
+      const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+      const int nt1 = min(n_tiles, nt0 + kNPerUnit);
+      const TileCoord c = sched.coord(mt * n_tiles);
+      const int a_row = __shfl_sync(0xffffffffu, c.a_row, 0);
+      const int group = __shfl_sync(0xffffffffu, c.group, 0);
+      for (int nt = nt0; nt < nt1; ++nt) {
+        const int brow = group * N + nt * kF4BN;
+        const bool load_a_sf = nt == nt0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int kval = min(kF4BKB, kbytes - kb * kF4BKB);  // bytes of K in this stage
+          const uint32_t sfbytes = (uint32_t)(kval / 32) * 512;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) {
             uint8_t* sa = smem + stage * S::STAGE;
             uint8_t* sb = sa + S::A_BYTES;
             uint8_t* ssfa = sb + S::B_BYTES;
             uint8_t* ssfb = ssfa + S::SFA_BYTES;
             mbar_arrive_expect_tx(&full[stage],
                                   S::A_BYTES + S::B_BYTES + (load_a_sf ? 3 : 2) * sfbytes);
-            tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, c.a_row);
+            tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, a_row);
             tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
             const int64_t atom_k = (int64_t)kb * 4;
             if (load_a_sf)
-              bulk_load(ssfa, args.a_sf + ((int64_t)(c.a_row >> 7) * atoms_per_row_tile + atom_k) * 512,
+              bulk_load(ssfa, args.a_sf + ((int64_t)(a_row >> 7) * atoms_per_row_tile + atom_k) * 512,
                         sfbytes, &full[stage]);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               bulk_load(ssfb + h * 2048,
                         args.w_sf + ((int64_t)((brow >> 7) + h) * atoms_per_row_tile + atom_k) * 512,
                         sfbytes, &full[stage]);
-            if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
           }
+          __syncwarp();
+          if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      // Scale copies run ONE STAGE AHEAD of the MMAs that consume them, so the
-      // tcgen05.cp latency overlaps the previous stage's MMAs (the copies of a
-      // stage and its MMAs would otherwise serialise on the TMEM dependency).
-      constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
-      const uint32_t tsfa = tmem_base + kTmemSfa;
-      const uint32_t tsfb0 = tsfa + sfa_cols;
-      int stage = 0;
-      uint32_t phase = 0;
-      int tile_it = 0;   // accumulator use count (one per n-tile)
-      int kiter = 0;     // global k-step counter: SFB buffer = kiter & 1
-      bool pre = false;  // are the current stage's copies already issued?
-      auto issue_copies = [&](int st, int kb, int nmma, bool a_sf, int buf) {
-        const uint32_t sa = smem_u32(smem + st * S::STAGE);
-        const uint32_t ssfa = sa + S::A_BYTES + S::B_BYTES, ssfb = ssfa + S::SFA_BYTES;
-        const uint32_t tsfb = tsfb0 + buf * 32;
-        for (int j = 0; j < nmma && !(args.dbg & 2u); ++j) {
-          if (a_sf)
-            utccp_32x128b_warpx4(tsfa + (kb * 4 + j) * 4, sf_desc(ssfa + 512 * j, args.sf_lbo, args.sf_sbo));
-          utccp_32x128b_warpx4(tsfb + 8 * j, sf_desc(ssfb + 512 * j, args.sf_lbo, args.sf_sbo));
-          utccp_32x128b_warpx4(tsfb + 8 * j + 4, sf_desc(ssfb + 2048 + 512 * j, args.sf_lbo, args.sf_sbo));
-        }
-      };
-      for (int it = 0;; ++it) {
-        const int slot = it % kF4Ring;
-        mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
-        const int u = slot_tile[slot];
-        mbar_arrive(&slot_empty[slot]);
-        if (u < 0) break;
-        const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
-        const int nt1 = min(n_tiles, nt0 + kNPerUnit);
-        for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
-          // previous n-tile drained by the epilogue => every earlier MMA completed,
-          // so the resident A scales may be rewritten at the start of a new unit
-          mbar_wait(tempty, (tile_it & 1) ^ 1);
+  } else if (warp == 1) {  // ---------------- MMA issuer
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t tsfa = tbase + kTmemSfa;
+    const uint32_t tsfb0 = tsfa + sfa_cols;
+    const uint32_t s0 = smem_u32(smem);
+    const uint64_t adesc0 = umma_desc_sw128(s0);
+    const uint64_t bdesc0 = umma_desc_sw128(s0 + S::A_BYTES);
+    const uint64_t sfadesc0 = sf_desc(s0 + S::A_BYTES + S::B_BYTES, args.sf_lbo, args.sf_sbo);
+    const uint64_t sfbdesc0 = sf_desc(s0 + S::A_BYTES + S::B_BYTES + S::SFA_BYTES, args.sf_lbo, args.sf_sbo);
+    const bool copy_sf = !(args.dbg & 2u);
+    int stage = 0;
+    uint32_t phase = 0, sfsel = 0;
+    int tile_it = 0;  // accumulator use count (one per n-tile)
+    for (int it = 0;; ++it) {
+      const int slot = it % kF4Ring;
+      mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
+      const int u = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
+      __syncwarp();
+      if (leader) mbar_arrive(&slot_empty[slot]);
+      if (u < 0) break;
+      const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+      const int nt1 = min(n_tiles, nt0 + kNPerUnit);
+      for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
+        // previous n-tile drained by the epilogue => every earlier MMA completed,
+        // so the resident A scales may be rewritten at the start of a new unit
+        mbar_wait(tempty, (tile_it & 1) ^ 1);
+        tc_fence_after();
+        const bool load_a_sf = nt == nt0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int nmma = min(kF4BKB, kbytes - kb * kF4BKB) / 32;
+          mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const bool first_tile = nt == nt0;
-          for (int kb = 0; kb < nkb; ++kb, ++kiter) {
-            const int nmma = min(kF4BKB, kbytes - kb * kF4BKB) / 32;
-            if (!pre) {  // not prefetched (start of a unit): copy now
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
-              issue_copies(stage, kb, nmma, first_tile, kiter & 1);
+          const uint64_t soff = (uint64_t)((uint32_t)(stage * S::STAGE) >> 4);
+          const uint32_t tsfb = tsfb0 + sfsel * 32;
+          if (leader) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (j < nmma && copy_sf) {
+                if (load_a_sf) utccp_32x128b_warpx4(tsfa + (kb * 4 + j) * 4, sfadesc0 + soff + 32 * j);
+                utccp_32x128b_warpx4(tsfb + 8 * j, sfbdesc0 + soff + 32 * j);
+                utccp_32x128b_warpx4(tsfb + 8 * j + 4, sfbdesc0 + soff + 128 + 32 * j);
+              }
             }
-            // prefetch the NEXT stage's scales (same unit only; a new unit's first
-            // stage rewrites the resident A scales and must wait for the drain)
-            const int nst = stage + 1 == kF4Stages ? 0 : stage + 1;
-            const uint32_t nph = stage + 1 == kF4Stages ? phase ^ 1 : phase;
-            const bool next_in_unit = kb + 1 < nkb || nt + 1 < nt1;
-            if (next_in_unit) {
-              const int nkb_next = kb + 1 < nkb ? kb + 1 : 0;
-              const int nmma_next = min(kF4BKB, kbytes - nkb_next * kF4BKB) / 32;
-              mbar_wait(&full[nst], nph);
-              tc_fence_after();
-              issue_copies(nst, nkb_next, nmma_next, first_tile && kb + 1 < nkb, (kiter + 1) & 1);
-            }
-            pre = next_in_unit;
-            const uint32_t sa = smem_u32(smem + stage * S::STAGE);
-            const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sa + S::A_BYTES);
-            const uint32_t tsfb = tsfb0 + (kiter & 1) * 32;
-            for (int j = 0; j < nmma; ++j)
-              umma_nvfp4(tmem_base + kTmemAcc, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2),
-                         idesc, tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < nmma)
+                umma_nvfp4(tbase + kTmemAcc, adesc0 + soff + 2 * j, bdesc0 + soff + 2 * j, idesc,
+                           tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
             tc_commit(&empty[stage]);
-            stage = nst;
-            phase = nph;
           }
-          tc_commit(tfull);
+          __syncwarp();
+          sfsel ^= 1;
+          if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
         }
+        if (leader) tc_commit(tfull);
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue (8 warps)

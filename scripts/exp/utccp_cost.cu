@@ -67,6 +67,33 @@ __global__ void __launch_bounds__(128, 1) kern(int mode, int reps, long long* ou
           utccp_32x128b_warpx4(tb + 324 + 8 * j, sdesc);
           umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256, tb + 272, 1);
         }
+      } else if (mode == 13) {    // 12 cp + 4 MMA consuming THIS stage's copies (RAW)
+        const uint32_t buf = tb + 320 + (r & 1) * 48;
+        for (int j = 0; j < 4; ++j) {
+          utccp_32x128b_warpx4(buf + 4 * j, sdesc);
+          utccp_32x128b_warpx4(buf + 16 + 8 * j, sdesc);
+          utccp_32x128b_warpx4(buf + 20 + 8 * j, sdesc);
+        }
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, buf + 4 * j, buf + 16 + 8 * j, 1);
+      } else if (mode == 14) {    // 12 cp for stage r+1, then 4 MMA consuming stage r (lookahead)
+        const uint32_t buf = tb + 320 + (r & 1) * 48, nbuf = tb + 320 + ((r + 1) & 1) * 48;
+        for (int j = 0; j < 4; ++j) {
+          utccp_32x128b_warpx4(nbuf + 4 * j, sdesc);
+          utccp_32x128b_warpx4(nbuf + 16 + 8 * j, sdesc);
+          utccp_32x128b_warpx4(nbuf + 20 + 8 * j, sdesc);
+        }
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, buf + 4 * j, buf + 16 + 8 * j, 1);
+      } else if (mode == 15) {    // 8 cp (SFB only) RAW + 4 MMA, SFA resident
+        const uint32_t buf = tb + 384 + (r & 1) * 32;
+        for (int j = 0; j < 4; ++j) {
+          utccp_32x128b_warpx4(buf + 8 * j, sdesc);
+          utccp_32x128b_warpx4(buf + 4 + 8 * j, sdesc);
+        }
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, tb + 256 + 4 * j, buf + 8 * j, 1);
+      } else if (mode == 16) {    // 12 cp, each reading a different 512 B of a 6 KB stage, + 4 MMA RAW
+        const uint32_t buf = tb + 320 + (r & 1) * 48;
+        for (int j = 0; j < 12; ++j) utccp_32x128b_warpx4(buf + 4 * j, sdesc + (uint64_t)(j * 32));
+        for (int j = 0; j < 4; ++j) umma_nvfp4(tb, adesc + 2 * j, bdesc + 2 * j, idesc, buf + 4 * j, buf + 16 + 8 * j, 1);
       } else if (mode == 7) {     // 4 x bf16 MMA N=256 K=16 (reference rate)
         const uint32_t id16 = idesc_bf16(128, 256);
         for (int j = 0; j < 4; ++j) umma_bf16(tb, adesc + 2 * j, bdesc + 2 * j, id16, 1);
@@ -93,8 +120,10 @@ int main() {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
   const char* names[] = {"12x cp32x128b.warpx4", "4x mma fp4 N256", "12cp+4mma", "6x cp128x256b",
                          "6x cp128x256b+4mma", "12x cp128x128b", "3cp+4mma", "4x mma bf16 N256",
-                         "8cp+4mma", "6cp+4mma", "4cp+4mma", "4x cp128x256b+4mma", "(2cp,1mma)x4"};
-  for (int mode = 0; mode < 13; ++mode) {
+                         "8cp+4mma", "6cp+4mma", "4cp+4mma", "4x cp128x256b+4mma", "(2cp,1mma)x4",
+                         "12cp+4mma RAW", "12cp(next)+4mma lookahead", "8cp RAW + 4mma (SFA res)",
+                         "12cp spread smem RAW"};
+  for (int mode = 0; mode < 17; ++mode) {
     const int reps = 2000;
     kern<<<1, 128, 65536>>>(mode, reps, d);
     kern<<<1, 128, 65536>>>(mode, reps, d);
