@@ -31,16 +31,24 @@ namespace realb {
 
 constexpr int kF4BM = 128, kF4BN = 256;
 constexpr int kF4BKB = 128;               // bytes of K per stage = 256 E2M1 values
-constexpr int kF4Stages = 4;
+// STORE (bf16 out) needs 32 KB of TMA-store staging, so it runs 3 stages
+template <int EPI>
+struct F4Cfg {
+  static constexpr int STAGES = EPI == REALB_EPI_STORE ? 3 : 4;
+};
 constexpr int kF4Threads = 384;
 
+template <int EPI>
 struct SmemFp4 {
+  static constexpr int STAGES = F4Cfg<EPI>::STAGES;
   static constexpr int A_BYTES = kF4BM * kF4BKB;    // 16 KB
   static constexpr int B_BYTES = kF4BN * kF4BKB;    // 32 KB
   static constexpr int SFA_BYTES = 4 * 512;         // 128 rows x 16 scales
   static constexpr int SFB_BYTES = 2 * 4 * 512;     // 256 rows x 16 scales
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-  static constexpr int BAR_OFF = kF4Stages * STAGE;
+  static constexpr int EPI_OFF = STAGES * STAGE;    // 8 warps x 2 x 2 KB (STORE only)
+  static constexpr int EPI_BYTES = EPI == REALB_EPI_STORE ? 8 * 4096 : 0;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 constexpr uint32_t kTmemAcc = 0, kTmemSfa = 256;  // SFB buffers follow the resident SFA
@@ -71,8 +79,10 @@ __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32
 template <int EPI>
 __global__ void __launch_bounds__(kF4Threads, 1)
     grouped_gemm_fp4_kernel(const __grid_constant__ CUtensorMap tmA,
-                            const __grid_constant__ CUtensorMap tmB, const Fp4Args args) {
-  using S = SmemFp4;
+                            const __grid_constant__ CUtensorMap tmB,
+                            const __grid_constant__ CUtensorMap tmOut, const Fp4Args args) {
+  using S = SmemFp4<EPI>;
+  constexpr int kF4Stages = S::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -295,23 +305,36 @@ __global__ void __launch_bounds__(kF4Threads, 1)
         cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
         cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
         *reinterpret_cast<uint32_t*>(args.out_sf + sf_mma_offset(r, ocol / 16, I / 16)) = sfw;
-      } else {
-        __nv_bfloat16* orow = args.out + r * N + c.n0 + half * 128;
+      } else {  // bf16 out via smem staging (SWIZZLE_64B) + TMA store, 32 columns at a time
+        const int wi = warp - 4;
+        const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + wi * 4096);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+          uint32_t p[16];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t* p = &v[i][8 * j];
-            st_global_v4(orow + 32 * i + 8 * j,
-                         pack_bf16x2(__uint_as_float(p[0]), __uint_as_float(p[1])),
-                         pack_bf16x2(__uint_as_float(p[2]), __uint_as_float(p[3])),
-                         pack_bf16x2(__uint_as_float(p[4]), __uint_as_float(p[5])),
-                         pack_bf16x2(__uint_as_float(p[6]), __uint_as_float(p[7])));
+          for (int j = 0; j < 16; ++j)
+            p[j] = pack_bf16x2(__uint_as_float(v[i][2 * j]), __uint_as_float(v[i][2 * j + 1]));
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+          const uint32_t buf = ebuf + (i & 1) * 2048;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            st_shared_v4(buf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), p[4 * cc], p[4 * cc + 1],
+                         p[4 * cc + 2], p[4 * cc + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmOut, smem + S::EPI_OFF + wi * 4096 + (i & 1) * 2048,
+                         c.n0 + half * 128 + 32 * i, c.a_row + q * 32);
+            bulk_commit_group();
           }
         }
       }
       }
     }
+  }
+  if constexpr (EPI == REALB_EPI_STORE) {
+    if (warp >= 4 && lane == 0) bulk_wait_group<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -329,13 +352,20 @@ template <int EPI>
 static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, const uint8_t* w_sf,
                       int64_t rows_cap, int N, int K, int E, const int32_t* layout, void* out,
                       uint8_t* out_codes, uint8_t* out_sf, int max_ctas, cudaStream_t st) {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, to;
   int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, a, (uint64_t)K / 2, rows_cap,
                         (uint64_t)K / 2, kF4BKB, kF4BM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, (uint64_t)K / 2, (uint64_t)E * N,
                     (uint64_t)K / 2, kF4BKB, kF4BN, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
+  if (EPI == REALB_EPI_STORE) {
+    rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, rows_cap, (uint64_t)N * 2, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  } else {
+    to = ta;  // unused
+  }
   Fp4Args args;
   args.a_sf = a_sf;
   args.w_sf = w_sf;
@@ -350,13 +380,13 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   args.sf_sbo = env_u32("REALB_DBG_SF_SBO", 128);
   args.dbg = env_u32("REALB_DBG_FP4", 0);
   auto kern = grouped_gemm_fp4_kernel<EPI>;
-  const int smem = SmemFp4::TOTAL;
+  const int smem = SmemFp4<EPI>::TOTAL;
   rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                    "grouped_gemm_nvfp4: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, kF4Threads, smem, st>>>(ta, tb, args);
+  kern<<<grid, kF4Threads, smem, st>>>(ta, tb, to, args);
   return check_launch("realb_grouped_gemm_nvfp4");
 }
 
