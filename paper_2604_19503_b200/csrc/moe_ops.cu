@@ -27,7 +27,7 @@ struct PlanParams {
 // plan_realb (balancers.py:89-122) on the device: one thread, the reference's
 // fp64 operation order (identical to realb_plan in runtime.cu).
 __device__ void plan_on_device(const int32_t* ev, int E, const PlanParams& pp, uint8_t* prec,
-                               int32_t* plan_out) {
+                               int32_t* plan_out) {  // ev, prec: shared memory
   const int R = pp.R, epr = E / R;
   long long rv[256], rt[256];
   long long total = 0;
@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
                                                      int32_t* __restrict__ expert_vt,
                                                      PlanParams pp, int32_t* plan_out, int ra) {
   __shared__ int32_t s_v[1024], s_t[1024];
-  __shared__ int32_t s_cnt[256], s_start[256];
+  __shared__ int32_t s_cnt[256], s_start[256], s_vt[512];
+  __shared__ uint8_t s_prec[256];
   const int G = blockDim.x / E;  // chunk groups per expert
   const int e = threadIdx.x % E, g = threadIdx.x / E;
   const bool act = g < G;
@@ -87,11 +88,15 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
     for (int j = 0; j < G; ++j) { tv += s_v[j * E + threadIdx.x]; tt += s_t[j * E + threadIdx.x]; }
     expert_vt[2 * threadIdx.x] = tv;
     expert_vt[2 * threadIdx.x + 1] = tt;
+    s_vt[2 * threadIdx.x] = tv;
+    s_vt[2 * threadIdx.x + 1] = tt;
     s_cnt[threadIdx.x] = tv + tt;
+    s_prec[threadIdx.x] = prec[threadIdx.x];
   }
   __syncthreads();
+  // serial part on shared memory only (global writes are fire-and-forget)
   if (threadIdx.x == 0) {
-    if (pp.enabled) plan_on_device(expert_vt, E, pp, prec, plan_out);
+    if (pp.enabled) plan_on_device(s_vt, E, pp, s_prec, plan_out);
     int run = 0;
     for (int i = 0; i < E; ++i) {
       s_start[i] = run;
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
       int32_t* pf = layout + LayoutView::off_prefix(E, p);
       int gg = 0, mt = 0;
       for (int i = 0; i < E; ++i) {
-        if ((int)prec[i] != p) continue;
+        if ((int)s_prec[i] != p) continue;
         gl[gg] = i;
         pf[gg] = mt;
         mt += (s_cnt[i] + 127) / 128;
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
   if (threadIdx.x < E) {
     layout[LayoutView::off_row_start(E) + threadIdx.x] = s_start[threadIdx.x];
     layout[LayoutView::off_row_count(E) + threadIdx.x] = s_cnt[threadIdx.x];
+    if (pp.enabled) prec[threadIdx.x] = s_prec[threadIdx.x];
   }
   if (act) {
     // exclusive offset of my chunk range within expert e, then per chunk

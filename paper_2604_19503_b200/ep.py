@@ -268,8 +268,15 @@ def run_bench(args):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # REALB_EP_COMM=gloo: validation mode for a one-GPU box (all ranks share cuda:0,
+    # collectives staged through the host); the default is NCCL, one GPU per rank.
+    staged = os.environ.get("REALB_EP_COMM", "nccl") == "gloo"
+    if staged:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     shape = SHAPES[args.config]
     T = args.tokens
     spec = WorkloadSpec(tokens=T, vision_frac=args.vision_frac, num_ranks=world, rank=rank)
@@ -278,7 +285,7 @@ def run_bench(args):
     bias = torch.zeros(shape.num_experts, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
     local = split_weights(shape, router, gu, dn, rank, world)
     del gu, dn
-    comm = EPComm()
+    comm = EPComm(staged=staged)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
     layer = EPMoELayer(shape, comm, ops)
 
@@ -294,8 +301,8 @@ def run_bench(args):
         e.record()
         torch.cuda.synchronize()
         dist.barrier()
-        t = torch.tensor([s.elapsed_time(e)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([s.elapsed_time(e)], device="cpu" if staged else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks of the device-timed region
         return float(t.item()) / args.steps
 
     _lib.launch_count = 0
@@ -314,6 +321,7 @@ def run_bench(args):
                "speedup_vs_bf16": ms_bf16 / ms, "ms_per_step_bf16": ms_bf16,
                "plan_w4a4_ranks": sorted(plan.accelerated_ranks),
                "rank_pairs": vt_all.sum(0).reshape(world, -1, 2).sum(axis=(1, 2)).tolist(),
-               "gpu_launches": int(launches)}
+               "gpu_launches": int(launches),
+               "comm": "gloo-staged on one shared GPU (validation only)" if staged else "nccl"}
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()
