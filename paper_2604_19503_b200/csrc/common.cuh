@@ -21,6 +21,9 @@ void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 inline int check_launch(const char* where) { return cuda_status(cudaGetLastError(), where); }
 int num_sms();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (kept out of the per-launch path so launches can be captured in CUDA graphs)
+int set_smem_once(const void* kernel, int bytes, const char* where);
 // cuTensorMapEncodeTiled resolved through the runtime (no -lcuda link).
 int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
                  uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,

@@ -247,8 +247,7 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   if (rc) return rc;
   auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI>;
   const int smem = SmemBf16<BN, STAGES>::TOTAL;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                   "grouped_gemm_bf16: smem attribute");
+  rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_bf16: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;

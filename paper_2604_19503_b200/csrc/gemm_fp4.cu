@@ -381,8 +381,7 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   args.dbg = env_u32("REALB_DBG_FP4", 0);
   auto kern = grouped_gemm_fp4_kernel<EPI>;
   const int smem = SmemFp4<EPI>::TOTAL;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                   "grouped_gemm_nvfp4: smem attribute");
+  rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_nvfp4: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;

@@ -203,8 +203,7 @@ static int launch_router(const void* x, const void* wg, const float* bias, const
   if (rc) return rc;
   auto kern = router_kernel<EPAD, KK>;
   const int smem = RouterSmem<EPAD>::TOTAL;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                   "router smem attribute");
+  rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "router smem attribute");
   if (rc) return rc;
   const int grid = (T + 127) / 128;
   kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc);

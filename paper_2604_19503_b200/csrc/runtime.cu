@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "common.cuh"
 
@@ -36,6 +38,20 @@ int num_sms() {
     cached[dev] = n;
   }
   return cached[dev];
+}
+
+int set_smem_once(const void* kernel, int bytes, const char* where) {
+  static std::mutex mu;
+  static std::vector<std::tuple<const void*, int, int>> done;  // (kernel, device, bytes)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (std::get<0>(d) == kernel && std::get<1>(d) == dev && std::get<2>(d) >= bytes) return REALB_OK;
+  int rc = cuda_status(
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), where);
+  if (rc == REALB_OK) done.emplace_back(kernel, dev, bytes);
+  return rc;
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,

@@ -171,6 +171,17 @@ class LayerResult:
         return self._plan
 
 
+class CapturedLayer:
+    """A MoE layer forward recorded as a CUDA graph (MoELayer.capture)."""
+
+    def __init__(self, graph, y, layer):
+        self.graph, self.y, self.layer = graph, y, layer
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.y
+
+
 class MoELayer:
     """Executes one MoE layer for ``T`` local tokens with preallocated workspaces.
 
@@ -217,6 +228,7 @@ class MoELayer:
         self.h_bf16 = torch.empty(R, I, dtype=bf, device=dev)
         self.rows_out = torch.empty(R, H, dtype=bf, device=dev)
         self.flag = torch.zeros(1, dtype=i32, device=dev)
+        self.y_buf = torch.empty(T, H, dtype=bf, device=dev)
         self._fp4 = None  # lazily allocated W4A4 workspaces
         self.side = torch.cuda.Stream(device=dev, priority=0)
 
@@ -339,15 +351,32 @@ class MoELayer:
             _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
-        y = torch.empty(T, H, dtype=torch.bfloat16, device=x.device)
+        y = self.y_buf[:T]
         _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
                   self.topk_w.data_ptr(), T, H, k, y.data_ptr(), sp)
+        if torch.cuda.is_current_stream_capturing():
+            return LayerResult(y, self, self.plan_host, self.expert_vt_host, None, self.placement,
+                               self.cluster)
         # lazy, asynchronous read-back of the plan and the counts (pinned, event-guarded)
         self.plan_host.copy_(self.plan_dev, non_blocking=True)
         self.expert_vt_host.copy_(self.expert_vt, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(main)
         return LayerResult(y, self, self.plan_host, self.expert_vt_host, ev, self.placement, self.cluster)
+
+    def capture(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
+                params: RealbParams | None = None) -> "CapturedLayer":
+        """Record one forward() into a CUDA graph over the given (static) input
+        tensors. The forward is host-sync-free, so the whole layer — router,
+        device-side plan, side-stream K3, dispatch, both GEMM precisions, combine
+        — replays as one graph launch. Refill ``x``/``modality`` in place and call
+        ``replay()``; the output is ``captured.y``."""
+        self.forward(x, modality, strategy, params)  # warm-up: allocations, kernel attributes
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            res = self.forward(x, modality, strategy, params)
+        return CapturedLayer(g, res.y, self)
 
     def expert_compute(self, T: int, prec: np.ndarray) -> None:
         """Re-run only the expert GEMMs of the experts whose code in ``prec`` is

@@ -239,3 +239,24 @@ def ref_placement(cluster):
     from paper_2604_19503_b200.policy import place_experts_static
 
     return place_experts_static(cluster)
+
+
+@pytest.mark.parametrize("strategy,R", [("baseline", 1), ("realb", 8)])
+def test_cuda_graph_capture_matches_eager(strategy, R):
+    """The forward is host-sync-free, so it is CUDA-graph capturable; replay must
+    reproduce the eager result exactly, also after refilling the static inputs."""
+    shape = small(SHAPES["kimi"], 64)
+    T = 1024
+    layer, x, mod, router, gu, dn, _ = build_layer(shape, T, R=R)
+    params = RealbParams(global_batch_threshold=0)
+    eager = layer.forward(x, mod, strategy, params).y.clone()
+    cap = layer.capture(x, mod, strategy, params)
+    y = cap.replay().clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y, eager)
+    x2 = torch.roll(x, 17, dims=0)
+    m2 = torch.roll(mod, 17, dims=0)
+    eager2 = layer.forward(x2, m2, strategy, params).y.clone()
+    x.copy_(x2)
+    mod.copy_(m2)
+    assert torch.equal(cap.replay(), eager2)
