@@ -171,19 +171,12 @@ def run_ours(args):
     ms_bf16 = float(np.mean(t_bf16))
     value = T / (ms / 1e3)
 
-    # --- e2e through the public API with host buffers (H2D of x and modality, D2H of y)
-    xh = x.cpu().pin_memory()
-    mh = mod.cpu().pin_memory()
-    yh = torch.empty(T, shape.hidden, dtype=torch.bfloat16).pin_memory()
-
-    def e2e_step():  # H2D into the graph's static inputs, replay, D2H of the output
-        x.copy_(xh, non_blocking=True)
-        mod.copy_(mh, non_blocking=True)
-        yh.copy_(g_realb.replay(), non_blocking=True)
-
-    t_e2e = time_steps(torch, e2e_step, args.steps, args.warmup, flush)
-    ms_e2e = float(np.mean(t_e2e))
-
+    # --- e2e through the public API with host buffers: every step copies its
+    # inputs H2D from pinned memory and its output D2H. Serving-style pipeline:
+    # two graph instances over double-buffered inputs/outputs, H2D and D2H on
+    # their own streams, so step i+1's upload and step i-1's download overlap
+    # step i's compute (PCIe is full duplex).
+    ms_e2e, e2e_bytes = run_e2e(torch, layer, x, mod, params, args)
     # --- roofline of the dominant kernel (K5 gate_up grouped GEMM), events on its stream
     roof = roofline_gate_up(torch, layer, x, mod, shape, args)
 
@@ -197,8 +190,8 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MB write, untimed); weights 1.1 GB > L2"},
         "speedup_vs_bf16": ms_bf16 / ms, "ms_per_step_bf16": ms_bf16,
         "e2e": {"value": T / (ms_e2e / 1e3), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(xh.numel() * 2 + mh.numel()),
-                "d2h_bytes_per_step": int(yh.numel() * 2)},
+                "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1],
+                "pipeline": "double-buffered: H2D(i+1) || compute(i) || D2H(i-1)"},
         "roofline": roof,
         "gpu_launches": int(launches_per_step * args.steps),
         "cuda_graph": True,
@@ -214,6 +207,53 @@ def run_ours(args):
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, sample=args.cpu_sample_tokens)
     print(json.dumps(out), flush=True)
+
+
+def run_e2e(torch, layer, x, mod, params, args):
+    T, H = x.shape
+    K, W = args.steps, args.warmup
+    nbuf = 2
+    xs = [torch.empty_like(x) for _ in range(nbuf)]
+    ms = [torch.empty_like(mod) for _ in range(nbuf)]
+    ys = [torch.empty(T, H, dtype=torch.bfloat16, device="cuda") for _ in range(nbuf)]
+    for i in range(nbuf):
+        xs[i].copy_(x)
+        ms[i].copy_(mod)
+    graphs = [layer.capture(xs[i], ms[i], "realb", params, out=ys[i]) for i in range(nbuf)]
+    n = K + W
+    xh = [x.cpu().pin_memory() for _ in range(min(n, 4))]   # distinct host input buffers
+    mh = [mod.cpu().pin_memory() for _ in range(min(n, 4))]
+    yh = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(min(n, 4))]
+    comp = torch.cuda.current_stream()
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    h2d_done = [ev() for _ in range(n)]
+    comp_done = [ev() for _ in range(n)]
+    d2h_done = [ev() for _ in range(n)]
+    torch.cuda.synchronize()
+    t0, t1 = ev(), ev()
+    for i in range(n):
+        if i == W:
+            t0.record(up)
+        b = i % nbuf
+        with torch.cuda.stream(up):
+            if i >= nbuf:
+                up.wait_event(comp_done[i - nbuf])  # graph i-2 finished reading xs[b]
+            xs[b].copy_(xh[i % len(xh)], non_blocking=True)
+            ms[b].copy_(mh[i % len(mh)], non_blocking=True)
+            h2d_done[i].record(up)
+        comp.wait_event(h2d_done[i])
+        if i >= nbuf:
+            comp.wait_event(d2h_done[i - nbuf])     # ys[b] downloaded before it is rewritten
+        graphs[b].replay()
+        comp_done[i].record(comp)
+        with torch.cuda.stream(down):
+            down.wait_event(comp_done[i])
+            yh[i % len(yh)].copy_(ys[b], non_blocking=True)
+            d2h_done[i].record(down)
+    t1.record(down)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / K, (int(x.numel() * 2 + mod.numel()), int(T * H * 2))
 
 
 def roofline_gate_up(torch, layer, x, mod, shape, args):

@@ -296,7 +296,7 @@ class MoELayer:
                   self.layout.data_ptr(), self.expert_vt.data_ptr(), _lib.stream_ptr())
 
     def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
-                params: RealbParams | None = None) -> LayerResult:
+                params: RealbParams | None = None, out: torch.Tensor | None = None) -> LayerResult:
         """One MoE layer over the local tokens; stream-ordered, no host sync.
 
         strategy "baseline" (and the EPLB tags) runs the all-BF16 comparator with
@@ -351,7 +351,7 @@ class MoELayer:
             _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
-        y = self.y_buf[:T]
+        y = self.y_buf[:T] if out is None else out
         _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
                   self.topk_w.data_ptr(), T, H, k, y.data_ptr(), sp)
         if torch.cuda.is_current_stream_capturing():
@@ -365,17 +365,17 @@ class MoELayer:
         return LayerResult(y, self, self.plan_host, self.expert_vt_host, ev, self.placement, self.cluster)
 
     def capture(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
-                params: RealbParams | None = None) -> "CapturedLayer":
+                params: RealbParams | None = None, out: torch.Tensor | None = None) -> "CapturedLayer":
         """Record one forward() into a CUDA graph over the given (static) input
         tensors. The forward is host-sync-free, so the whole layer — router,
         device-side plan, side-stream K3, dispatch, both GEMM precisions, combine
         — replays as one graph launch. Refill ``x``/``modality`` in place and call
         ``replay()``; the output is ``captured.y``."""
-        self.forward(x, modality, strategy, params)  # warm-up: allocations, kernel attributes
+        self.forward(x, modality, strategy, params, out)  # warm-up: allocations, kernel attributes
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            res = self.forward(x, modality, strategy, params)
+            res = self.forward(x, modality, strategy, params, out)
         return CapturedLayer(g, res.y, self)
 
     def expert_compute(self, T: int, prec: np.ndarray) -> None:
