@@ -34,7 +34,7 @@ int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uin
 struct LayoutView {
   int E, nchunks;
   __host__ __device__ static int64_t words(int E, int nchunks) {
-    return 8 + 3LL * E + 2LL * (2 * E + 1) + (int64_t)nchunks * E;
+    return 8 + 3LL * E + 2LL * (2 * E + 1) + 2LL * (E + 1) + (int64_t)nchunks * E;
   }
   __host__ __device__ static int off_row_start(int) { return 8; }
   __host__ __device__ static int off_row_count(int E) { return 8 + E; }
@@ -42,7 +42,10 @@ struct LayoutView {
   // per precision p: glist[E] then mtile_prefix[E+1]
   __host__ __device__ static int off_glist(int E, int p) { return 8 + 3 * E + p * (2 * E + 1); }
   __host__ __device__ static int off_prefix(int E, int p) { return off_glist(E, p) + E; }
-  __host__ __device__ static int off_chunk(int E) { return 8 + 3 * E + 2 * (2 * E + 1); }
+  // per precision p: exclusive prefix of ceil(m-tiles / 2) ("m-tile pairs" of the
+  // 2-CTA cluster GEMMs), aligned with glist
+  __host__ __device__ static int off_pprefix(int E, int p) { return 8 + 3 * E + 2 * (2 * E + 1) + p * (E + 1); }
+  __host__ __device__ static int off_chunk(int E) { return 8 + 3 * E + 2 * (2 * E + 1) + 2 * (E + 1); }
 };
 
 #if defined(__CUDACC__)
@@ -143,6 +146,48 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// ---- thread-block clusters (2-CTA pairs sharing operand tiles)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of `p` (a local smem pointer) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA load whose box lands at the same smem offset in every CTA of `mask` and
+// completes `bytes` on the mbarrier at the same offset in each of them
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* m, uint64_t* bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load_mc(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                             uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
 // ---- tcgen05: TMEM allocation (one warp), fences, commit, loads
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_slot) {
@@ -168,6 +213,14 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+// commit arriving on the mbarrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() {

@@ -13,6 +13,8 @@
 //   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> (SwiGLU) -> bf16
 //               -> global; each warp owns TMEM lane quadrant (warp % 4)
 // Roofline: tensor-bound, 2*M*N*K flop per tile.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "grouped.cuh"
 
@@ -47,12 +49,19 @@ __device__ __forceinline__ void stage_row64(uint32_t buf, int r, const uint32_t 
                  p[4 * c + 3]);
 }
 
-template <int BN, int STAGES, int EPI>
+// CL = 1: one CTA per SM, each CTA loads its own A and W tiles.
+// CL = 2: 2-CTA clusters working on the SAME (expert, n-tile) with the two
+//   m-tiles of a pair; each CTA TMA-loads HALF of the W tile and multicasts it to
+//   both, so per-SM L2->SM operand traffic drops from A+W to A+W/2 (the 1-GPU
+//   gate_up was bound by that traffic: TMA-only time 0.38 of 0.49 ms). The MMAs
+//   stay cta_group::1; a stage may be refilled only when BOTH CTAs' MMAs are done
+//   with it (multicast tcgen05.commit into both CTAs' empty barriers).
+template <int BN, int STAGES, int EPI, int CL>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut, const int32_t* layout,
-                             int E, int prec, int N, int K) {
+                             int E, int prec, int N, int K, uint32_t dbg) {
   using S = SmemBf16<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -67,9 +76,13 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_tile + kTileRing);
 
   const int warp = warp_id(), lane = lane_id();
+  const uint32_t crank = CL == 2 ? cluster_ctarank() : 0u;
   const GroupedSched sched = GroupedSched::make(layout, E, prec, N, BN);
-  const int total = sched.total();
+  const int total = CL == 2 ? sched.total_pairs() : sched.total();
   const int nkb = K / kBK;
+  constexpr uint16_t kBoth = 0x3;
+  // consumers of a tile slot: MMA + 4 epilogue warps per CTA (+ the peer producer)
+  constexpr uint32_t kSlotConsumers = CL == 2 ? 11 : 5;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -77,7 +90,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmOut);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // one tcgen05.commit per CTA of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -85,15 +98,28 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < kTileRing; ++i) {
       mbar_init(&slot_full[i], 1);
-      mbar_init(&slot_empty[i], 5);  // MMA thread + 4 epilogue warps
+      mbar_init(&slot_empty[i], kSlotConsumers);
     }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // peer barriers initialised before any remote op
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_of = [&](int u, bool& dummy) -> TileCoord {
+    if constexpr (CL == 2) return sched.coord_pair(u, (int)crank, dummy);
+    dummy = false;
+    return sched.coord(u);
+  };
+  // consumer-side release of a ring slot: local in a 1-CTA launch; in a pair all
+  // consumers release the LEADER's slot (the leader owns the tile fetch)
+  auto release_slot = [&](int slot) {
+    if constexpr (CL == 2) mbar_arrive_cluster(mapa_shared(&slot_empty[slot], 0));
+    else mbar_arrive(&slot_empty[slot]);
+  };
 
   // Producer and MMA roles run on their whole warp with warp-uniform values and
   // one elected lane issuing (see gemm_fp4.cu: lane-0-only code makes ptxas wrap
@@ -105,26 +131,42 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     for (int i = 0;; ++i) {
       const int slot = i % kTileRing;
-      mbar_wait(&slot_empty[slot], ((i / kTileRing) & 1) ^ 1);
       int t = 0;
-      if (leader) {
-        t = atomicAdd(ctr, 1);
-        if (t >= total) t = -1;
-        slot_tile[slot] = t;
-        mbar_arrive(&slot_full[slot]);
+      if (crank == 0) {  // the (cluster) leader fetches and publishes the unit
+        mbar_wait(&slot_empty[slot], ((i / kTileRing) & 1) ^ 1);
+        if (leader) {
+          t = atomicAdd(ctr, 1);
+          if (t >= total) t = -1;
+          slot_tile[slot] = t;
+          if constexpr (CL == 2) {
+            st_cluster_u32(mapa_shared(&slot_tile[slot], 1), (uint32_t)t);
+            mbar_arrive_cluster(mapa_shared(&slot_full[slot], 1));
+          }
+          mbar_arrive(&slot_full[slot]);
+        }
+        t = __shfl_sync(0xffffffffu, t, 0);
+      } else {
+        mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
+        t = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
+        __syncwarp();
+        if (leader) release_slot(slot);
       }
-      t = __shfl_sync(0xffffffffu, t, 0);
       if (t < 0) break;
-      const TileCoord c = sched.coord(t);
+      bool dummy;
+      const TileCoord c = tile_of(t, dummy);
       const int a_row = __shfl_sync(0xffffffffu, c.a_row, 0);
       const int brow = __shfl_sync(0xffffffffu, c.group * N + c.n0, 0);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * kBK, a_row);
-          tma_load_2d(sa + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
+          mbar_arrive_expect_tx(&full[stage], (dummy ? 0 : S::A_BYTES) + S::B_BYTES);
+          if (!dummy) tma_load_2d(sa, &tmA, &full[stage], kb * kBK, a_row);
+          if constexpr (CL == 2)
+            tma_load_2d_mc(sa + S::A_BYTES + crank * (S::B_BYTES / 2), &tmB, &full[stage], kb * kBK,
+                           brow + (int)crank * (BN / 2), kBoth);
+          else
+            tma_load_2d(sa + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -143,8 +185,14 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
       const int t = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
       __syncwarp();
-      if (leader) mbar_arrive(&slot_empty[slot]);
+      if (leader) release_slot(slot);
       if (t < 0) break;
+      bool dummy = false;
+      if constexpr (CL == 2) {
+        const TileCoord c = tile_of(t, dummy);
+        (void)c;
+        dummy = __shfl_sync(0xffffffffu, (int)dummy, 0) != 0;
+      }
       const int acc = i & 1;
       mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -154,10 +202,13 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         const uint64_t soff = (uint64_t)((uint32_t)(stage * S::STAGE_BYTES) >> 4);
         if (leader) {
+          if (!(dbg & 4u) && !dummy) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)  // +32 B (16 bf16) inside the 128-B swizzle atom
-            umma_bf16(dtmem, adesc0 + soff + 2 * k, bdesc0 + soff + 2 * k, idesc, (kb | k) != 0);
-          tc_commit(&empty[stage]);
+            for (int k = 0; k < kBK / 16; ++k)  // +32 B (16 bf16) inside the 128-B swizzle atom
+              umma_bf16(dtmem, adesc0 + soff + 2 * k, bdesc0 + soff + 2 * k, idesc, (kb | k) != 0);
+          }
+          if constexpr (CL == 2) tc_commit_mc(&empty[stage], kBoth);
+          else tc_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -174,14 +225,21 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
       const int t = slot_tile[slot];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&slot_empty[slot]);
+      if (lane == 0) release_slot(slot);
       if (t < 0) break;
-      const TileCoord c = sched.coord(t);
+      bool dummy;
+      const TileCoord c = tile_of(t, dummy);
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       const int row0 = c.a_row + q * 32;
+      if ((dbg & 1u) || dummy) {  // nothing to store: release the accumulator at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        continue;
+      }
       constexpr int NCH = EPI == REALB_EPI_STORE ? BN / 32 : BN / 64;
 #pragma unroll 1
       for (int ch = 0; ch < NCH; ++ch) {
@@ -225,12 +283,13 @@ __global__ void __launch_bounds__(256, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // no peer may still multicast / arrive into us
   tc_fence_after();
   if (warp == 2) tmem_dealloc<2 * BN>(tmem_base);
   if (threadIdx.x == 0) GroupedSched::finish(layout, prec);
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, int CL>
 static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, int N, int K, int E,
                                const int32_t* layout, int prec, void* out, int max_ctas,
                                cudaStream_t st) {
@@ -239,19 +298,37 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
                         kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, K, (uint64_t)E * N, (uint64_t)K * 2,
-                    kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+                    kBK, BN / CL, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   const int NO = EPI == REALB_EPI_STORE ? N : N / 2;
   rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, NO, rows_cap, (uint64_t)NO * 2, 32,
                     32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
-  auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI>;
+  auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL>;
   const int smem = SmemBf16<BN, STAGES>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_bf16: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, 256, smem, st>>>(ta, tb, to, layout, E, prec, N, K);
+  grid = grid / CL * CL;
+  if (grid < CL) grid = CL;
+  const char* dbg_env = getenv("REALB_DBG_BF16");
+  const uint32_t dbg = dbg_env ? (uint32_t)strtoul(dbg_env, nullptr, 0) : 0u;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = cuda_status(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, layout, E, prec, N, K, dbg),
+                   "realb_grouped_gemm_bf16 launch");
+  if (rc) return rc;
   return check_launch("realb_grouped_gemm_bf16");
 }
 
@@ -272,12 +349,19 @@ extern "C" int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  // 2-CTA clusters (W tile multicast) unless REALB_GEMM_CLUSTER=1
+  const char* cl_env = getenv("REALB_GEMM_CLUSTER");
+  const bool pair = !(cl_env && cl_env[0] == '1');
   if (epilogue == REALB_EPI_STORE)
-    return launch_grouped_bf16<256, 4, REALB_EPI_STORE>(d_a, d_w, rows_cap, N, K, E, d_layout,
-                                                        prec, d_out, max_ctas, st);
+    return pair ? launch_grouped_bf16<256, 4, REALB_EPI_STORE, 2>(d_a, d_w, rows_cap, N, K, E,
+                                                                   d_layout, prec, d_out, max_ctas, st)
+                : launch_grouped_bf16<256, 4, REALB_EPI_STORE, 1>(d_a, d_w, rows_cap, N, K, E,
+                                                                   d_layout, prec, d_out, max_ctas, st);
   if (epilogue == REALB_EPI_SWIGLU)
-    return launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU>(d_a, d_w, rows_cap, N, K, E, d_layout,
-                                                         prec, d_out, max_ctas, st);
+    return pair ? launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 2>(d_a, d_w, rows_cap, N, K, E,
+                                                                    d_layout, prec, d_out, max_ctas, st)
+                : launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 1>(d_a, d_w, rows_cap, N, K, E,
+                                                                    d_layout, prec, d_out, max_ctas, st);
   set_error("realb_grouped_gemm_bf16: unknown epilogue %d", epilogue);
   return REALB_EINVAL;
 }

@@ -20,6 +20,7 @@ struct TileCoord {
 struct GroupedSched {
   const int32_t* glist;   // [G] expert ids of this precision class
   const int32_t* prefix;  // [G+1] exclusive prefix of m-tiles
+  const int32_t* pprefix; // [G+1] exclusive prefix of m-tile pairs (2-CTA clusters)
   const int32_t* row_start;
   const int32_t* row_count;
   int G;
@@ -31,6 +32,7 @@ struct GroupedSched {
     GroupedSched s;
     s.glist = layout + LayoutView::off_glist(E, prec);
     s.prefix = layout + LayoutView::off_prefix(E, prec);
+    s.pprefix = layout + LayoutView::off_pprefix(E, prec);
     s.row_start = layout + LayoutView::off_row_start(E);
     s.row_count = layout + LayoutView::off_row_count(E);
     s.G = layout[1 + prec];
@@ -39,6 +41,31 @@ struct GroupedSched {
     return s;
   }
   __device__ __forceinline__ int total() const { return G > 0 ? prefix[G] * n_tiles : 0; }
+
+  // 2-CTA pair units: u = pair * n_tiles + nt. Both CTAs of a cluster take the
+  // same (expert, n-tile) and the two m-tiles of the pair (cluster rank 0 / 1);
+  // an expert with an odd m-tile count gives rank 1 a dummy (no compute) slot.
+  __device__ __forceinline__ int total_pairs() const { return G > 0 ? pprefix[G] * n_tiles : 0; }
+  __device__ __forceinline__ TileCoord coord_pair(int u, int rank, bool& dummy) const {
+    const int pp = u / n_tiles, nt = u - pp * n_tiles;
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pprefix[mid] <= pp) lo = mid; else hi = mid - 1;
+    }
+    TileCoord c;
+    c.group = glist[lo];
+    const int mt_lo = prefix[lo], mt_hi = prefix[lo + 1];
+    int mt = mt_lo + 2 * (pp - pprefix[lo]) + rank;
+    dummy = mt >= mt_hi;
+    if (dummy) mt -= 1;
+    const int local = mt - mt_lo;
+    c.a_row = row_start[c.group] + local * 128;
+    c.n0 = nt * BN;
+    const int rem = row_count[c.group] - local * 128;
+    c.valid = rem < 128 ? rem : 128;
+    return c;
+  }
 
   // Dynamic tile fetch: layout words [4 + 2p] (next tile) and [5 + 2p] (CTAs
   // done) of precision class p are zeroed by the align kernels; the last CTA

@@ -107,15 +107,20 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
     for (int p = 0; p < 2; ++p) {
       int32_t* gl = layout + LayoutView::off_glist(E, p);
       int32_t* pf = layout + LayoutView::off_prefix(E, p);
-      int gg = 0, mt = 0;
+      int32_t* pp2 = layout + LayoutView::off_pprefix(E, p);
+      int gg = 0, mt = 0, np = 0;
       for (int i = 0; i < E; ++i) {
         if ((int)s_prec[i] != p) continue;
         gl[gg] = i;
         pf[gg] = mt;
-        mt += (s_cnt[i] + 127) / 128;
+        pp2[gg] = np;
+        const int m = (s_cnt[i] + 127) / 128;
+        mt += m;
+        np += (m + 1) / 2;
         ++gg;
       }
       pf[gg] = mt;
+      pp2[gg] = np;
       layout[1 + p] = gg;
     }
   }
@@ -273,15 +278,20 @@ __global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t* __restric
     for (int p = 0; p < 2; ++p) {
       int32_t* gl = layout + LayoutView::off_glist(El, p);
       int32_t* pf = layout + LayoutView::off_prefix(El, p);
-      int g = 0, mt = 0;
+      int32_t* pp2 = layout + LayoutView::off_pprefix(El, p);
+      int g = 0, mt = 0, np = 0;
       for (int i = 0; i < El; ++i) {
         if ((int)prec[i] != p) continue;
         gl[g] = i;
         pf[g] = mt;
-        mt += (s_tot[i] + 127) / 128;
+        pp2[g] = np;
+        const int m = (s_tot[i] + 127) / 128;
+        mt += m;
+        np += (m + 1) / 2;
         ++g;
       }
       pf[g] = mt;
+      pp2[g] = np;
       layout[1 + p] = g;
     }
     // source-major prefix of received rows (row index space of the recv buffer)

@@ -30,6 +30,13 @@ for label, E, N, K, per in [("kimi_gate_up_ep8hot", 8, 2816, 2048, 13000), ("kim
     f = lambda: _lib.call("realb_grouped_gemm_bf16", A.data_ptr(), W.data_ptr(), rows, N, K, E, lt.data_ptr(), 0, 0, o.data_ptr(), 0, _lib.stream_ptr())
     t = timeit(f)
     flops = 2.0 * rows * N * K
+    dbgt = {}
+    for dbg in (1, 4, 5):
+        os.environ["REALB_DBG_BF16"] = str(dbg)
+        dbgt[dbg] = timeit(f)
+    os.environ["REALB_DBG_BF16"] = "0"
+    fs = lambda: _lib.call("realb_grouped_gemm_bf16", A.data_ptr(), W.data_ptr(), rows, N, K, E, lt.data_ptr(), 0, 1, o.data_ptr(), 0, _lib.stream_ptr())
+    t_swiglu = timeit(fs)
     # torch grouped mm on the same padded rows
     offs = torch.tensor(np.cumsum((counts + 127)//128*128), dtype=torch.int32, device="cuda")
     Wt = W.view(E, N, K).transpose(1, 2)
@@ -38,7 +45,8 @@ for label, E, N, K, per in [("kimi_gate_up_ep8hot", 8, 2816, 2048, 13000), ("kim
         tg = timeit(g)
     except Exception as e:
         tg = repr(e)[:100]
-    out[label] = dict(rows=rows, ms=t, tflops=flops / t / 1e9, torch_ms=tg,
+    out[label] = dict(rows=rows, ms=t, tflops=flops / t / 1e9, ms_swiglu=t_swiglu, ms_no_epi=dbgt[1],
+                      ms_no_mma=dbgt[4], ms_tma_only=dbgt[5], torch_ms=tg,
                       torch_tflops=(flops / tg / 1e9) if isinstance(tg, float) else None)
     print(label, out[label], flush=True)
 os.makedirs("gpurun_out", exist_ok=True)

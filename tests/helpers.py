@@ -27,6 +27,8 @@ def host_layout(counts, prec, nchunks=1):
         lay[base:base + len(g)] = g
         mt = padded[g] // 128
         lay[base + E:base + E + len(g) + 1] = np.concatenate([[0], np.cumsum(mt)])
+        pbase = 8 + 3 * E + 2 * (2 * E + 1) + p * (E + 1)
+        lay[pbase:pbase + len(g) + 1] = np.concatenate([[0], np.cumsum((mt + 1) // 2)])
         lay[1 + p] = len(g)
     lay[0] = int(padded.sum())
     return lay, int(padded.sum())
