@@ -23,10 +23,10 @@ namespace realb {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B rows = one SWIZZLE_128B atom width
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CL>
 struct SmemBf16 {
   static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int B_BYTES = (BN / CL) * kBK * 2;  // a pair stages half of W per CTA
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;       // 4 warps x 2 x (32 rows x 64 B)
   static constexpr int EPI_BYTES = 4 * 2 * 2048;
@@ -49,20 +49,22 @@ __device__ __forceinline__ void stage_row64(uint32_t buf, int r, const uint32_t 
                  p[4 * c + 3]);
 }
 
-// CL = 1: one CTA per SM, each CTA loads its own A and W tiles.
-// CL = 2: 2-CTA clusters working on the SAME (expert, n-tile) with the two
-//   m-tiles of a pair; each CTA TMA-loads HALF of the W tile and multicasts it to
-//   both, so per-SM L2->SM operand traffic drops from A+W to A+W/2 (the 1-GPU
-//   gate_up was bound by that traffic: TMA-only time 0.38 of 0.49 ms). The MMAs
-//   stay cta_group::1; a stage may be refilled only when BOTH CTAs' MMAs are done
-//   with it (multicast tcgen05.commit into both CTAs' empty barriers).
+// CL = 1: one CTA per SM, tcgen05.mma.cta_group::1, M = 128.
+// CL = 2: a 2-CTA cluster is one tcgen05 "CTA pair" (cta_group::2, M = 256):
+//   CTA r stages ITS 128 A rows and HALF of the W tile (W rows 128r..128r+127);
+//   the leader (rank 0) issues the pair MMA, which reads A/W from both CTAs'
+//   smem and accumulates rows 128r.. in CTA r's TMEM. Halving the W bytes staged
+//   per CTA lets 6 stages fit instead of 4: the 1-CTA kernel was bound by
+//   operand bytes in flight (TMA-only time 0.38 of 0.49 ms on the 1-GPU gate_up).
+//   Both CTAs' loads complete on the leader's full barrier; the leader's
+//   multicast commits release both CTAs' stages and publish both accumulators.
 template <int BN, int STAGES, int EPI, int CL>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut, const int32_t* layout,
                              int E, int prec, int N, int K, uint32_t dbg) {
-  using S = SmemBf16<BN, STAGES>;
+  using S = SmemBf16<BN, STAGES, CL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -81,8 +83,9 @@ __global__ void __launch_bounds__(256, 1)
   const int total = CL == 2 ? sched.total_pairs() : sched.total();
   const int nkb = K / kBK;
   constexpr uint16_t kBoth = 0x3;
-  // consumers of a tile slot: MMA + 4 epilogue warps per CTA (+ the peer producer)
-  constexpr uint32_t kSlotConsumers = CL == 2 ? 11 : 5;
+  // consumers of a tile-id slot: 1-CTA: MMA + 4 epilogue warps; pair: leader MMA +
+  // 4 leader epilogue warps + peer producer + 4 peer epilogue warps
+  constexpr uint32_t kSlotConsumers = CL == 2 ? 10 : 5;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -90,11 +93,11 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmOut);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // one tcgen05.commit per CTA of the cluster
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CL);
     }
     for (int i = 0; i < kTileRing; ++i) {
       mbar_init(&slot_full[i], 1);
@@ -102,23 +105,25 @@ __global__ void __launch_bounds__(256, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CL == 2) tmem_alloc_2sm<2 * BN>(tmem_slot);
+    else tmem_alloc<2 * BN>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL == 2) cluster_sync();  // peer barriers initialised before any remote op
+  if constexpr (CL == 2) cluster_sync();  // peer barriers / TMEM ready before any remote op
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto tile_of = [&](int u, bool& dummy) -> TileCoord {
-    if constexpr (CL == 2) return sched.coord_pair(u, (int)crank, dummy);
+  auto tile_of = [&](int u, int rank, bool& dummy) -> TileCoord {
+    if constexpr (CL == 2) return sched.coord_pair(u, rank, dummy);
     dummy = false;
     return sched.coord(u);
   };
-  // consumer-side release of a ring slot: local in a 1-CTA launch; in a pair all
-  // consumers release the LEADER's slot (the leader owns the tile fetch)
-  auto release_slot = [&](int slot) {
-    if constexpr (CL == 2) mbar_arrive_cluster(mapa_shared(&slot_empty[slot], 0));
-    else mbar_arrive(&slot_empty[slot]);
+  // arrive on a barrier of the pair leader (local barrier in a 1-CTA launch)
+  auto arrive_leader = [&](uint64_t* bar) {
+    if constexpr (CL == 2) mbar_arrive_cluster(mapa_shared(bar, 0));
+    else mbar_arrive(bar);
   };
 
   // Producer and MMA roles run on their whole warp with warp-uniform values and
@@ -127,12 +132,13 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {  // ---------------- TMA producer + dynamic tile fetch
     const bool leader = elect_one();
     int* ctr = GroupedSched::counters(layout, prec);
+    const uint32_t full0 = CL == 2 ? mapa_shared(&full[0], 0) : smem_u32(&full[0]);
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0;; ++i) {
       const int slot = i % kTileRing;
       int t = 0;
-      if (crank == 0) {  // the (cluster) leader fetches and publishes the unit
+      if (crank == 0) {  // the (pair) leader fetches and publishes the unit
         mbar_wait(&slot_empty[slot], ((i / kTileRing) & 1) ^ 1);
         if (leader) {
           t = atomicAdd(ctr, 1);
@@ -149,32 +155,41 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
         t = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
         __syncwarp();
-        if (leader) release_slot(slot);
+        if (leader) arrive_leader(&slot_empty[slot]);
       }
       if (t < 0) break;
-      bool dummy;
-      const TileCoord c = tile_of(t, dummy);
+      bool dummy, dummy1 = false;
+      const TileCoord c = tile_of(t, (int)crank, dummy);
+      if constexpr (CL == 2) {
+        if (crank == 0) { bool d1; (void)tile_of(t, 1, d1); dummy1 = d1; }
+      }
       const int a_row = __shfl_sync(0xffffffffu, c.a_row, 0);
       const int brow = __shfl_sync(0xffffffffu, c.group * N + c.n0, 0);
+      dummy = __shfl_sync(0xffffffffu, (int)dummy, 0) != 0;
+      dummy1 = __shfl_sync(0xffffffffu, (int)dummy1, 0) != 0;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], (dummy ? 0 : S::A_BYTES) + S::B_BYTES);
-          if (!dummy) tma_load_2d(sa, &tmA, &full[stage], kb * kBK, a_row);
-          if constexpr (CL == 2)
-            tma_load_2d_mc(sa + S::A_BYTES + crank * (S::B_BYTES / 2), &tmB, &full[stage], kb * kBK,
-                           brow + (int)crank * (BN / 2), kBoth);
-          else
+          if constexpr (CL == 2) {
+            const uint32_t fb = full0 + (uint32_t)stage * 8u;
+            if (crank == 0)
+              mbar_arrive_expect_tx(&full[stage], 2 * S::B_BYTES + S::A_BYTES + (dummy1 ? 0 : S::A_BYTES));
+            if (!dummy) tma_load_2d_2sm(sa, &tmA, fb, kb * kBK, a_row);
+            tma_load_2d_2sm(sa + S::A_BYTES, &tmB, fb, kb * kBK, brow + (int)crank * (BN / 2));
+          } else {
+            mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], kb * kBK, a_row);
             tma_load_2d(sa + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer
+  } else if (warp == 1 && crank == 0) {  // ---------------- MMA issuer (pair leader)
     const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+    constexpr uint32_t idesc = idesc_bf16(kBM * CL, BN);
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t s0 = smem_u32(smem);
     const uint64_t adesc0 = umma_desc_sw128(s0), bdesc0 = umma_desc_sw128(s0 + S::A_BYTES);
@@ -185,14 +200,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
       const int t = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
       __syncwarp();
-      if (leader) release_slot(slot);
+      if (leader) mbar_arrive(&slot_empty[slot]);
       if (t < 0) break;
-      bool dummy = false;
-      if constexpr (CL == 2) {
-        const TileCoord c = tile_of(t, dummy);
-        (void)c;
-        dummy = __shfl_sync(0xffffffffu, (int)dummy, 0) != 0;
-      }
       const int acc = i & 1;
       mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -202,22 +211,29 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         const uint64_t soff = (uint64_t)((uint32_t)(stage * S::STAGE_BYTES) >> 4);
         if (leader) {
-          if (!(dbg & 4u) && !dummy) {
+          if (!(dbg & 4u)) {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // +32 B (16 bf16) inside the 128-B swizzle atom
-              umma_bf16(dtmem, adesc0 + soff + 2 * k, bdesc0 + soff + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {  // +32 B (16 bf16) inside the 128-B swizzle atom
+              if constexpr (CL == 2)
+                umma_bf16_2sm(dtmem, adesc0 + soff + 2 * k, bdesc0 + soff + 2 * k, idesc, (kb | k) != 0);
+              else
+                umma_bf16(dtmem, adesc0 + soff + 2 * k, bdesc0 + soff + 2 * k, idesc, (kb | k) != 0);
+            }
           }
-          if constexpr (CL == 2) tc_commit_mc(&empty[stage], kBoth);
+          if constexpr (CL == 2) tc_commit_2sm_mc(&empty[stage], kBoth);
           else tc_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (leader) tc_commit(&tfull[acc]);
+      if (leader) {
+        if constexpr (CL == 2) tc_commit_2sm_mc(&tfull[acc], kBoth);
+        else tc_commit(&tfull[acc]);
+      }
       __syncwarp();
     }
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> smem -> TMA store
-    const int q = warp & 3;  // TMEM lane quadrant = 32-row slice of the tile
+    const int q = warp & 3;  // TMEM lane quadrant = 32-row slice of this CTA's 128 rows
     const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + q * 4096);
     int nbuf = 0;
     for (int i = 0;; ++i) {
@@ -225,10 +241,10 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
       const int t = slot_tile[slot];
       __syncwarp();
-      if (lane == 0) release_slot(slot);
+      if (lane == 0) arrive_leader(&slot_empty[slot]);
       if (t < 0) break;
       bool dummy;
-      const TileCoord c = tile_of(t, dummy);
+      const TileCoord c = tile_of(t, (int)crank, dummy);
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
@@ -237,7 +253,7 @@ __global__ void __launch_bounds__(256, 1)
       if ((dbg & 1u) || dummy) {  // nothing to store: release the accumulator at once
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) arrive_leader(&tempty[acc]);
         continue;
       }
       constexpr int NCH = EPI == REALB_EPI_STORE ? BN / 32 : BN / 64;
@@ -277,15 +293,18 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) arrive_leader(&tempty[acc]);
     }
     if (lane == 0) bulk_wait_group<0>();  // all stores of this CTA complete
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL == 2) cluster_sync();  // no peer may still multicast / arrive into us
+  if constexpr (CL == 2) cluster_sync();  // no peer may still load / arrive / read our smem
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<2 * BN>(tmem_base);
+  if (warp == 2) {
+    if constexpr (CL == 2) tmem_dealloc_2sm<2 * BN>(tmem_base);
+    else tmem_dealloc<2 * BN>(tmem_base);
+  }
   if (threadIdx.x == 0) GroupedSched::finish(layout, prec);
 }
 
@@ -305,7 +324,7 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
                     32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
   auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL>;
-  const int smem = SmemBf16<BN, STAGES>::TOTAL;
+  const int smem = SmemBf16<BN, STAGES, CL>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_bf16: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
@@ -349,16 +368,16 @@ extern "C" int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // 2-CTA clusters (W tile multicast) unless REALB_GEMM_CLUSTER=1
+  // 2-CTA pairs (cta_group::2, 6 stages) unless REALB_GEMM_CLUSTER=1
   const char* cl_env = getenv("REALB_GEMM_CLUSTER");
   const bool pair = !(cl_env && cl_env[0] == '1');
   if (epilogue == REALB_EPI_STORE)
-    return pair ? launch_grouped_bf16<256, 4, REALB_EPI_STORE, 2>(d_a, d_w, rows_cap, N, K, E,
+    return pair ? launch_grouped_bf16<256, 6, REALB_EPI_STORE, 2>(d_a, d_w, rows_cap, N, K, E,
                                                                    d_layout, prec, d_out, max_ctas, st)
                 : launch_grouped_bf16<256, 4, REALB_EPI_STORE, 1>(d_a, d_w, rows_cap, N, K, E,
                                                                    d_layout, prec, d_out, max_ctas, st);
   if (epilogue == REALB_EPI_SWIGLU)
-    return pair ? launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 2>(d_a, d_w, rows_cap, N, K, E,
+    return pair ? launch_grouped_bf16<256, 6, REALB_EPI_SWIGLU, 2>(d_a, d_w, rows_cap, N, K, E,
                                                                     d_layout, prec, d_out, max_ctas, st)
                 : launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 1>(d_a, d_w, rows_cap, N, K, E,
                                                                     d_layout, prec, d_out, max_ctas, st);
