@@ -368,9 +368,12 @@ extern "C" int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // 2-CTA pairs (cta_group::2, 6 stages) unless REALB_GEMM_CLUSTER=1
+  // 2-CTA pairs (cta_group::2, 6 stages) when experts are large: a pair needs an
+  // even number of 128-row m-tiles per expert and wastes half a pair otherwise,
+  // so small-expert launches (avg < 8 m-tiles per expert) stay 1-CTA.
+  // REALB_GEMM_CLUSTER=1|2 forces the choice.
   const char* cl_env = getenv("REALB_GEMM_CLUSTER");
-  const bool pair = !(cl_env && cl_env[0] == '1');
+  const bool pair = cl_env ? cl_env[0] == '2' : (rows_cap / E) >= 1024;
   if (epilogue == REALB_EPI_STORE)
     return pair ? launch_grouped_bf16<256, 6, REALB_EPI_STORE, 2>(d_a, d_w, rows_cap, N, K, E,
                                                                    d_layout, prec, d_out, max_ctas, st)
