@@ -59,6 +59,10 @@ extern "C" {
 #define REALB_SCORE_SOFTMAX_CLAMPNORM 2 /* ERNIE-4.5-VL: softmax, top-k,
                                            / max(sum, norm_min)                */
 
+/* token chunk of the router / stats / dispatch kernels: chunk_counts hold one
+ * [E][2] histogram per REALB_CHUNK_TOKENS consecutive tokens */
+#define REALB_CHUNK_TOKENS 64
+
 /* precision codes: values of moesim.core.Precision (core.py:9-11) */
 #define REALB_PREC_W16A16 0
 #define REALB_PREC_W4A4 1
@@ -109,7 +113,7 @@ REALB_API int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows_
  *   d_topk_idx : int32 [T][k], experts in selection order (score desc, ties
  *                to the lowest expert id)
  *   d_topk_w   : fp32 [T][k] routing weights
- *   d_chunk_counts : int32 [ceil(T/128)][E][2] per-128-token-chunk
+ *   d_chunk_counts : int32 [ceil(T/64)][E][2] per-64-token-chunk
  *                (vision, text) pair counts (deterministic, atomic-free)
  * E <= 256, 1 <= k <= 16.
  * ------------------------------------------------------------------------ */

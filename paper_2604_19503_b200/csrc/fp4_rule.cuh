@@ -137,8 +137,9 @@ __device__ __forceinline__ uint32_t canon_neg_zero(uint32_t x) {
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-// amax of 16 bf16 values held as 8 bf16x2 words (exact: integer max of |bits|)
-__device__ __forceinline__ float amax_bf16x16(const uint32_t (&w)[8]) {
+// amax of 16 bf16 values held as 8 bf16x2 words (exact: integer max of |bits|).
+// Returns the 16-bit magnitude pattern; >= 0x7F80 means an Inf/NaN is present.
+__device__ __forceinline__ uint32_t amax_bits_bf16x16(const uint32_t (&w)[8]) {
   uint32_t m = w[0] & 0x7FFF7FFFu;
 #pragma unroll
   for (int i = 1; i < 8; ++i) {
@@ -146,7 +147,10 @@ __device__ __forceinline__ float amax_bf16x16(const uint32_t (&w)[8]) {
     asm("max.u16x2 %0, %0, %1;" : "+r"(m) : "r"(a));
   }
   const uint32_t lo = m & 0xFFFFu, hi = m >> 16;
-  return __uint_as_float((lo > hi ? lo : hi) << 16);
+  return lo > hi ? lo : hi;
+}
+__device__ __forceinline__ float amax_bf16x16(const uint32_t (&w)[8]) {
+  return __uint_as_float(amax_bits_bf16x16(w) << 16);
 }
 
 __device__ __forceinline__ float q1_div(float v, float sc, float r) {
@@ -155,9 +159,13 @@ __device__ __forceinline__ float q1_div(float v, float sc, float r) {
   return fmaf(rho, r, q0);
 }
 
-// one block of 16 bf16 (8 words) -> packed codes (element 2i low nibble), scale bits
-__device__ __forceinline__ uint2 quant_block16_bf16(const uint32_t (&w)[8], uint32_t& sbits) {
-  const float amax = amax_bf16x16(w);
+// one block of 16 bf16 (8 words) -> packed codes (element 2i low nibble), scale bits;
+// `nonfinite` is set when the block holds an Inf/NaN (QuantizationDomainError)
+__device__ __forceinline__ uint2 quant_block16_bf16(const uint32_t (&w)[8], uint32_t& sbits,
+                                                    bool& nonfinite) {
+  const uint32_t ab = amax_bits_bf16x16(w);
+  nonfinite = ab >= 0x7F80u;
+  const float amax = __uint_as_float(ab << 16);
   sbits = block_scale_bits_f32(amax);
   if (sbits == 0u) return make_uint2(0u, 0u);
   const float sc = e4m3_decode(sbits);

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
 }
 
 // ----------------------------------------------------------------- dispatch
-// One CTA per 128-token chunk (the router's chunking). Pair ranks inside the
+// One CTA per 64-token chunk (REALB_CHUNK_TOKENS, the router's chunking). Pair ranks inside the
 // chunk are computed per warp with __match_any_sync, then offset by a per-warp
 // exclusive prefix: pairs of one expert keep (token, slot) order.
 constexpr int kPermWarps = 8;
@@ -154,10 +154,10 @@ __global__ void __launch_bounds__(256) permute_kernel(
   extern __shared__ int32_t sm[];
   int32_t* s_base = sm;                       // [E]
   int32_t* s_cnt = s_base + E;                // [kPermWarps][E]
-  int32_t* s_pos = s_cnt + kPermWarps * E;    // [128*k]
+  int32_t* s_pos = s_cnt + kPermWarps * E;    // [REALB_CHUNK_TOKENS * k]
   const int chunk = blockIdx.x;
-  const int t0 = chunk * 128;
-  const int ntok = min(128, T - t0);
+  const int t0 = chunk * REALB_CHUNK_TOKENS;
+  const int ntok = min(REALB_CHUNK_TOKENS, T - t0);
   const int P = ntok * k;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t* co = layout + LayoutView::off_chunk(E) + (int64_t)chunk * E;
@@ -230,15 +230,10 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
         for (int b = 0; b < 4; ++b) {
           const uint4 u0 = __ldg(src + (g * 4 + b) * 2), u1 = __ldg(src + (g * 4 + b) * 2 + 1);
           const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-          uint32_t nf = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t ex = w[i] & 0x7F807F80u;
-            nf |= ((ex & 0xFFFFu) == 0x7F80u) | ((ex >> 16) == 0x7F80u);
-          }
-          if (nf && flag) atomicOr(flag, 1);
           uint32_t sb;
-          cw[b] = quant_block16_bf16(w, sb);
+          bool nf;
+          cw[b] = quant_block16_bf16(w, sb, nf);
+          if (nf && flag) atomicOr(flag, 1);
           sfw |= sb << (8 * b);
         }
         uint4* cdst = reinterpret_cast<uint4*>(a_codes + pos * (H / 2) + g * 32);
@@ -436,13 +431,13 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
                                       int32_t* d_pair_pos, void* d_a_bf16, uint8_t* d_a_codes,
                                       uint8_t* d_a_sf, int32_t* d_flag, void* stream) {
   if (!d_x || !d_topk_idx || !d_prec || !d_layout || !d_pair_pos || !d_a_bf16 || T < 0 ||
-      H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || nchunks != (T + 127) / 128) {
+      H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
     set_error("realb_dispatch_permute: bad arguments (T=%d H=%d E=%d k=%d nchunks=%d)", T, H, E,
               k, nchunks);
     return REALB_EINVAL;
   }
   if (T == 0) return REALB_OK;
-  const int smem = (E + kPermWarps * E + 128 * k) * 4;
+  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
   permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout,
                                                                 d_pair_pos);
   int rc = check_launch("realb_dispatch_permute (positions)");

@@ -44,66 +44,69 @@ __device__ __forceinline__ void flag_nonfinite(int32_t* flag) {
   if (flag) atomicOr(flag, 1);
 }
 
-// bf16 product path: both halves' loads are issued before any compute (2 x 32 B
-// in flight per thread), then the cvt-based fast block rule.
+// One 128-row x 64-column tile (one 512-B scale atom) of a bf16 matrix: each
+// thread quantises 2 blocks, both loads issued before any compute. Non-finite
+// input is detected from the block amax bits (|bits| >= 0x7F80).
+template <int LAYOUT>
+__device__ __forceinline__ void quant_tile_bf16(const __nv_bfloat16* __restrict__ x, int64_t rows,
+                                                int64_t cols, int64_t nkb, int64_t tm, int64_t tk,
+                                                uint8_t* __restrict__ codes,
+                                                uint8_t* __restrict__ sf, int32_t* flag) {
+  uint32_t w[2][8];
+  bool ok[2];
+  int64_t rr[2], kk[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int b = threadIdx.x + h * 256;
+    rr[h] = tm * 128 + (b >> 2);
+    kk[h] = tk * 4 + (b & 3);
+    ok[h] = rr[h] < rows && kk[h] < nkb;
+    if (ok[h]) {
+      const uint4* q = reinterpret_cast<const uint4*>(x + rr[h] * cols + kk[h] * 16);
+      const uint4 a = __ldg(q), c = __ldg(q + 1);
+      w[h][0] = a.x; w[h][1] = a.y; w[h][2] = a.z; w[h][3] = a.w;
+      w[h][4] = c.x; w[h][5] = c.y; w[h][6] = c.z; w[h][7] = c.w;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!ok[h]) continue;
+    uint32_t sbits;
+    bool nf;
+    const uint2 c = quant_block16_bf16(w[h], sbits, nf);
+    if (nf) flag_nonfinite(flag);
+    *reinterpret_cast<uint2*>(codes + rr[h] * (cols >> 1) + kk[h] * 8) = c;
+    const int64_t so =
+        LAYOUT == REALB_SF_FLAT ? rr[h] * nkb + kk[h] : sf_mma_offset(rr[h], kk[h], nkb);
+    sf[so] = (uint8_t)sbits;
+  }
+}
+
 template <int LAYOUT>
 __global__ void __launch_bounds__(256) quant_kernel_bf16(const __nv_bfloat16* __restrict__ x,
                                                           int64_t rows, int64_t cols,
                                                           uint8_t* __restrict__ codes,
                                                           uint8_t* __restrict__ sf, int32_t* flag) {
   const int64_t nkb = cols >> 4;
-  const int64_t tiles_k = (nkb + 3) >> 2;
-  const int64_t tiles = ((rows + 127) >> 7) * tiles_k;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t tm = tile / tiles_k, tk = tile - tm * tiles_k;
-    uint32_t w[2][8];
-    bool ok[2];
-    int64_t rr[2], kk[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int b = threadIdx.x + h * 256;
-      rr[h] = tm * 128 + (b >> 2);
-      kk[h] = tk * 4 + (b & 3);
-      ok[h] = rr[h] < rows && kk[h] < nkb;
-      if (ok[h]) {
-        const uint4* q = reinterpret_cast<const uint4*>(x + rr[h] * cols + kk[h] * 16);
-        const uint4 a = __ldg(q), c = __ldg(q + 1);
-        w[h][0] = a.x; w[h][1] = a.y; w[h][2] = a.z; w[h][3] = a.w;
-        w[h][4] = c.x; w[h][5] = c.y; w[h][6] = c.z; w[h][7] = c.w;
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (!ok[h]) continue;
-      // non-finite bf16: exponent field all ones
-      uint32_t nf = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t e = w[h][i] & 0x7F807F80u;
-        nf |= ((e & 0xFFFFu) == 0x7F80u) | ((e >> 16) == 0x7F80u);
-      }
-      if (nf) flag_nonfinite(flag);
-      uint32_t sbits;
-      const uint2 c = quant_block16_bf16(w[h], sbits);
-      *reinterpret_cast<uint2*>(codes + rr[h] * (cols >> 1) + kk[h] * 8) = c;
-      const int64_t so =
-          LAYOUT == REALB_SF_FLAT ? rr[h] * nkb + kk[h] : sf_mma_offset(rr[h], kk[h], nkb);
-      sf[so] = (uint8_t)sbits;
-    }
+  const int tiles_k = (int)((nkb + 3) >> 2);
+  const int tiles = (int)((rows + 127) >> 7) * tiles_k;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int tm = tile / tiles_k, tk = tile - tm * tiles_k;
+    quant_tile_bf16<LAYOUT>(x, rows, cols, nkb, tm, tk, codes, sf, flag);
   }
 }
 
 // K3 on the device-side plan: quantise only the rows of experts whose
 // precision code is W4A4 (rows_per_expert % 128 == 0, so a tile never straddles
-// two experts); MMA scale layout. The tiles of one expert are contiguous, so
-// whole experts are skipped by a single compare per tile.
+// two experts); MMA scale layout.
 __global__ void __launch_bounds__(256) quant_experts_kernel(
     const __nv_bfloat16* __restrict__ x, int64_t rows_per_expert, int64_t cols, int E,
     const uint8_t* __restrict__ prec, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
     int32_t* flag) {
   const int64_t nkb = cols >> 4;
-  const int64_t tiles_k = nkb >> 2;
-  const int64_t tiles_per_expert = (rows_per_expert >> 7) * tiles_k;
+  const int tiles_k = (int)(nkb >> 2);
+  const int mt_per_expert = (int)(rows_per_expert >> 7);
+  const int tiles_per_expert = mt_per_expert * tiles_k;
   // enumerate only the W4A4 experts' tiles: tile -> (j-th W4A4 expert, local tile)
   __shared__ int s_list[256];
   __shared__ int s_n;
@@ -114,37 +117,28 @@ __global__ void __launch_bounds__(256) quant_experts_kernel(
     s_n = n;
   }
   __syncthreads();
-  const int64_t tiles = (int64_t)s_n * tiles_per_expert;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t j = tile / tiles_per_expert, lt = tile - j * tiles_per_expert;
-    const int64_t tm = s_list[j] * (rows_per_expert >> 7) + lt / tiles_k, tk = lt % tiles_k;
-    uint32_t w[2][8];
-    int64_t rr[2], kk[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int b = threadIdx.x + h * 256;
-      rr[h] = tm * 128 + (b >> 2);
-      kk[h] = tk * 4 + (b & 3);
-      const uint4* q = reinterpret_cast<const uint4*>(x + rr[h] * cols + kk[h] * 16);
-      const uint4 a = __ldg(q), c = __ldg(q + 1);
-      w[h][0] = a.x; w[h][1] = a.y; w[h][2] = a.z; w[h][3] = a.w;
-      w[h][4] = c.x; w[h][5] = c.y; w[h][6] = c.z; w[h][7] = c.w;
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint32_t nf = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t ex = w[h][i] & 0x7F807F80u;
-        nf |= ((ex & 0xFFFFu) == 0x7F80u) | ((ex >> 16) == 0x7F80u);
-      }
-      if (nf) flag_nonfinite(flag);
-      uint32_t sbits;
-      const uint2 c = quant_block16_bf16(w[h], sbits);
-      *reinterpret_cast<uint2*>(codes + rr[h] * (cols >> 1) + kk[h] * 8) = c;
-      sf[sf_mma_offset(rr[h], kk[h], nkb)] = (uint8_t)sbits;
-    }
+  const int tiles = s_n * tiles_per_expert;
+  const int64_t rows = (int64_t)E * rows_per_expert;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int j = tile / tiles_per_expert, lt = tile - j * tiles_per_expert;
+    const int lm = lt / tiles_k;
+    quant_tile_bf16<REALB_SF_MMA128x4>(x, rows, cols, nkb, (int64_t)s_list[j] * mt_per_expert + lm,
+                                        lt - lm * tiles_k, codes, sf, flag);
   }
+}
+
+// resident CTAs per SM x SMs (no partial last wave); capped by the work
+static int quant_grid(const void* kern, int64_t tiles, int max_ctas) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 4;
+  }
+  int64_t grid = (int64_t)num_sms() * per_sm;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid > tiles) grid = tiles;
+  return (int)(grid < 1 ? 1 : grid);
 }
 
 template <typename T, int LAYOUT>
@@ -229,10 +223,8 @@ static int launch_quant(void (*kernel)(const T*, int64_t, int64_t, uint8_t*, uin
                         const void* x, int64_t rows, int64_t cols, uint8_t* codes,
                         uint8_t* sf, int32_t* flag, int max_ctas, cudaStream_t st) {
   const int64_t tiles = ((rows + 127) / 128) * (((cols / 16) + 3) / 4);
-  int64_t grid = (int64_t)num_sms() * 8;
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (grid > tiles) grid = tiles;
-  if (grid < 1) return REALB_OK;
+  if (tiles < 1) return REALB_OK;
+  const int grid = quant_grid(reinterpret_cast<const void*>(kernel), tiles, max_ctas);
   kernel<<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, codes, sf, flag);
   return check_launch("realb_quantize_nvfp4");
 }
@@ -293,8 +285,8 @@ extern "C" int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows
               (long long)rows_per_expert, (long long)cols);
     return REALB_EINVAL;
   }
-  int grid = num_sms() * 8;
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  const int grid = quant_grid(reinterpret_cast<const void*>(quant_experts_kernel),
+                             (int64_t)E * (rows_per_expert / 128) * (cols / 64), max_ctas);
   quant_experts_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(d_w), rows_per_expert, cols, E, d_expert_prec,
       d_codes, d_sf, d_flag);

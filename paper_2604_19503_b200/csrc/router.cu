@@ -1,8 +1,10 @@
 // router.cu — K1 + K2: gating GEMM, top-k selection, routing weights and
 // per-chunk (vision, text) pair statistics in ONE kernel.
 //
-// One CTA per 128-token chunk. logits[128, E] = X[128, H] . Wg[E, H]^T runs on
-// tcgen05 (kind::f16, M=128, N=E padded to 16) with TMA-fed smem stages; the
+// One CTA per 64-token chunk (REALB_CHUNK_TOKENS; 128 CTAs at T = 8192 — the
+// kernel is HBM-bound and needs the SMs). logits[64, E] = X[64, H] . Wg[E, H]^T
+// runs on tcgen05 (kind::f16, M=128 with the upper 64 smem rows unused,
+// N=E padded to 16) with TMA-fed smem stages; the
 // epilogue thread that owns token row r streams its E fp32 logits out of TMEM
 // (tcgen05.ld 32x32b) and performs, in registers:
 //   - write logits[r, :]                (the D1 contract selects on these)
@@ -24,9 +26,11 @@ constexpr int kKMax = 8;
 
 template <int EPAD>
 struct RouterSmem {
-  static constexpr int A_BYTES = 128 * kRBK * 2;
+  static constexpr int A_BYTES = 128 * kRBK * 2;          // MMA reads 128 rows
+  static constexpr int A_LOAD = REALB_CHUNK_TOKENS * kRBK * 2;  // TMA fills 64
   static constexpr int B_BYTES = EPAD * kRBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGE_TX = A_LOAD + B_BYTES;
   // as many stages as fit in ~200 KB: the router is latency-bound per SM (one CTA
   // per 128 tokens), so bytes in flight set its HBM throughput
   static constexpr int STAGES = (200 * 1024) / STAGE > 12 ? 12 : (200 * 1024) / STAGE;
@@ -81,8 +85,8 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * S::STAGE;
-        mbar_arrive_expect_tx(&full[stage], S::STAGE);
-        tma_load_2d(sa, &tmX, &full[stage], kb * kRBK, chunk * 128);
+        mbar_arrive_expect_tx(&full[stage], S::STAGE_TX);
+        tma_load_2d(sa, &tmX, &full[stage], kb * kRBK, chunk * REALB_CHUNK_TOKENS);
         tma_load_2d(sa + S::A_BYTES, &tmW, &full[stage], kb * kRBK, 0);
         if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
       }
@@ -106,10 +110,10 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_commit(done);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + REALB_CHUNK_TOKENS / 32) {  // rows 0..63 = TMEM lanes 0..63
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int t = chunk * 128 + row;
+    const int t = chunk * REALB_CHUNK_TOKENS + row;
     const bool valid = t < T;
     mbar_wait(done, 0);
     tc_fence_after();
@@ -180,9 +184,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     tc_fence_before();
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    named_bar_sync(1, REALB_CHUNK_TOKENS);
     int32_t* out = chunk_counts + (int64_t)chunk * E * 2;
-    for (int i = row; i < 2 * E; i += 128) out[i] = hist[i];
+    for (int i = row; i < 2 * E; i += REALB_CHUNK_TOKENS) out[i] = hist[i];
   }
   tc_fence_before();
   __syncthreads();
@@ -195,8 +199,8 @@ static int launch_router(const void* x, const void* wg, const float* bias, const
                          int T, int H, int E, int k, int scoring, float rs, float nm, float* logits,
                          int32_t* idx, float* w, int32_t* cc, cudaStream_t st) {
   CUtensorMap tx, tw;
-  int rc = make_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, H, T, (uint64_t)H * 2, kRBK, 128,
-                        CU_TENSOR_MAP_SWIZZLE_128B);
+  int rc = make_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, H, T, (uint64_t)H * 2, kRBK,
+                        REALB_CHUNK_TOKENS, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, wg, H, E, (uint64_t)H * 2, kRBK, EPAD,
                     CU_TENSOR_MAP_SWIZZLE_128B);
@@ -205,7 +209,7 @@ static int launch_router(const void* x, const void* wg, const float* bias, const
   const int smem = RouterSmem<EPAD>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "router smem attribute");
   if (rc) return rc;
-  const int grid = (T + 127) / 128;
+  const int grid = (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS;
   kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc);
   return check_launch("realb_router_topk_stats");
 }

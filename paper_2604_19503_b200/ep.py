@@ -81,7 +81,7 @@ class CudaEPOps:
         self.T = T
         dev, i32, bf, u8 = torch.device(device), torch.int32, torch.bfloat16, torch.uint8
         self.dev = dev
-        self.nch = (T + 127) // 128
+        self.nch = (T + 63) // 64
         self.logits = torch.empty(T, E, dtype=torch.float32, device=dev)
         self.topk_idx = torch.empty(T, k, dtype=i32, device=dev)
         self.topk_w = torch.empty(T, k, dtype=torch.float32, device=dev)
@@ -137,7 +137,7 @@ class CudaEPOps:
                   mod.data_ptr(), T, self.H, self.E, self.k, s.scoring, float(s.routed_scaling),
                   float(s.norm_min), self.logits.data_ptr(), self.topk_idx.data_ptr(),
                   self.topk_w.data_ptr(), self.cc.data_ptr(), sp)
-        _lib.call("realb_moe_align", self.cc.data_ptr(), (T + 127) // 128, self.E, self.zero_prec.data_ptr(),
+        _lib.call("realb_moe_align", self.cc.data_ptr(), (T + 63) // 64, self.E, self.zero_prec.data_ptr(),
                   1, self.send_layout.data_ptr(), self.vt_local.data_ptr(), sp)
         return self.topk_idx[:T], self.topk_w[:T], self.vt_local
 
@@ -145,7 +145,7 @@ class CudaEPOps:
     def pack(self, x, topk_idx):
         T = x.shape[0]
         _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, self.H, self.E,
-                  self.k, self.zero_prec.data_ptr(), self.send_layout.data_ptr(), (T + 127) // 128,
+                  self.k, self.zero_prec.data_ptr(), self.send_layout.data_ptr(), (T + 63) // 64,
                   T * self.k, self.send_pos.data_ptr(), self.send_buf.data_ptr(), None, None,
                   self.flag.data_ptr(), _lib.stream_ptr())
         return self.send_buf, self.send_pos[:T]

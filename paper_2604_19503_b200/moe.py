@@ -208,7 +208,7 @@ class MoELayer:
         self.quant_max_ctas = quant_max_ctas
         E, k, H, I = self.E, self.k, self.H, self.I
         T = max_tokens
-        self.nchunks_max = (T + 127) // 128
+        self.nchunks_max = (T + 63) // 64
         self.rows_cap = ((T * k + E * 127) + 127) // 128 * 128
         dev, bf, u8, i32, f32 = self.device, torch.bfloat16, torch.uint8, torch.int32, torch.float32
         self.logits = torch.empty(T, E, dtype=f32, device=dev)
@@ -282,14 +282,14 @@ class MoELayer:
                   _lib.stream_ptr())
 
     def align(self, T: int, row_align: int = 128):
-        _lib.call("realb_moe_align", self.chunk_counts.data_ptr(), (T + 127) // 128, self.E,
+        _lib.call("realb_moe_align", self.chunk_counts.data_ptr(), (T + 63) // 64, self.E,
                   self.prec_dev.data_ptr(), row_align, self.layout.data_ptr(),
                   self.expert_vt.data_ptr(), _lib.stream_ptr())
 
     def align_plan(self, T: int, strategy: str, params: RealbParams):
         """Expert totals + the precision plan evaluated on the device (no sync)."""
         c = self.cluster
-        _lib.call("realb_moe_align_plan", self.chunk_counts.data_ptr(), (T + 127) // 128, self.E,
+        _lib.call("realb_moe_align_plan", self.chunk_counts.data_ptr(), (T + 63) // 64, self.E,
                   c.num_ranks, _STRATEGY_CODE[strategy], float(params.capacity_factor),
                   float(params.modality_threshold), int(params.global_batch_threshold),
                   int(bool(c.modality_isolated)), self.prec_dev.data_ptr(), self.plan_dev.data_ptr(),
@@ -311,7 +311,7 @@ class MoELayer:
         if T > self.max_tokens:
             raise ValueError("more tokens than the layer was sized for")
         E, k, H, I = self.E, self.k, self.H, self.I
-        nch = (T + 127) // 128
+        nch = (T + 63) // 64
         main = torch.cuda.current_stream()
         sp = _lib.stream_ptr(main)
         self.route(x, modality)

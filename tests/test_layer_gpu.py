@@ -94,7 +94,7 @@ def test_dispatch_layout_and_positions(name, E, T):
     layer.route(x, mod)
     layer.prec_dev.zero_()
     layer.align(T)
-    nch = (T + 127) // 128
+    nch = (T + 63) // 64
     _lib.call("realb_dispatch_permute", x.data_ptr(), layer.topk_idx.data_ptr(), T, shape.hidden,
               shape.num_experts, shape.top_k, layer.prec_dev.data_ptr(), layer.layout.data_ptr(), nch,
               layer.rows_cap, layer.pair_pos.data_ptr(), layer.a_bf16.data_ptr(), None, None,
