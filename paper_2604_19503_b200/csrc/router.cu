@@ -16,6 +16,8 @@
 // and the chunk histogram is written once, without global atomics, to
 // chunk_counts[c][E][2] (deterministic; summed by realb_moe_align).
 // Roofline: HBM-bound (2H bytes/token read, E <= 256 < ridge), DESIGN.md §K1.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace realb {
@@ -46,7 +48,7 @@ __global__ void __launch_bounds__(256, 1)
                   const float* __restrict__ bias, const uint8_t* __restrict__ modality, int T,
                   int H, int E, int scoring, float routed_scaling, float norm_min,
                   float* __restrict__ logits, int32_t* __restrict__ topk_idx,
-                  float* __restrict__ topk_w, int32_t* __restrict__ chunk_counts) {
+                  float* __restrict__ topk_w, int32_t* __restrict__ chunk_counts, uint32_t dbg) {
   using S = RouterSmem<EPAD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -85,9 +87,13 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * S::STAGE;
-        mbar_arrive_expect_tx(&full[stage], S::STAGE_TX);
-        tma_load_2d(sa, &tmX, &full[stage], kb * kRBK, chunk * REALB_CHUNK_TOKENS);
-        tma_load_2d(sa + S::A_BYTES, &tmW, &full[stage], kb * kRBK, 0);
+        if (dbg & 4u) {  // debug: no loads
+          mbar_arrive(&full[stage]);
+        } else {
+          mbar_arrive_expect_tx(&full[stage], S::STAGE_TX);
+          tma_load_2d(sa, &tmX, &full[stage], kb * kRBK, chunk * REALB_CHUNK_TOKENS);
+          tma_load_2d(sa + S::A_BYTES, &tmW, &full[stage], kb * kRBK, 0);
+        }
         if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -118,6 +124,11 @@ __global__ void __launch_bounds__(256, 1)
     mbar_wait(done, 0);
     tc_fence_after();
     const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16);
+    if (dbg & 1u) {  // debug: no epilogue work
+      named_bar_sync(1, REALB_CHUNK_TOKENS);
+      tc_fence_before();
+      goto router_done;
+    }
 
     constexpr int k = KK;
     float sval[KK], lsel[KK];
@@ -188,6 +199,7 @@ __global__ void __launch_bounds__(256, 1)
     int32_t* out = chunk_counts + (int64_t)chunk * E * 2;
     for (int i = row; i < 2 * E; i += REALB_CHUNK_TOKENS) out[i] = hist[i];
   }
+router_done:
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -210,7 +222,9 @@ static int launch_router(const void* x, const void* wg, const float* bias, const
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "router smem attribute");
   if (rc) return rc;
   const int grid = (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS;
-  kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc);
+  const char* dbg_env = getenv("REALB_DBG_ROUTER");
+  const uint32_t dbg = dbg_env ? (uint32_t)strtoul(dbg_env, nullptr, 0) : 0u;
+  kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc, dbg);
   return check_launch("realb_router_topk_stats");
 }
 

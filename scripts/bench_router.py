@@ -1,0 +1,25 @@
+"""Router microbenchmark with debug variants (REALB_DBG_ROUTER: 1 no epilogue, 4 no loads)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2604_19503_b200 import _lib
+from paper_2604_19503_b200.moe import SHAPES, MoELayer, MoEWeights
+from paper_2604_19503_b200.workload import WorkloadSpec, make_batch
+shape = SHAPES["kimi"]
+for T in (8192, 65536):
+    x, mod, router, _ = make_batch(shape, WorkloadSpec(tokens=T))
+    E, k, H = 64, 6, 2048
+    logits = torch.empty(T, E, device="cuda"); idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(T, k, device="cuda"); cc = torch.empty((T + 63) // 64, E, 2, dtype=torch.int32, device="cuda")
+    bias = torch.zeros(E, device="cuda")
+    f = lambda: _lib.call("realb_router_topk_stats", x.data_ptr(), router.data_ptr(), bias.data_ptr(), mod.data_ptr(), T, H, E, k, 1, 2.446, 1e-12, logits.data_ptr(), idx.data_ptr(), w.data_ptr(), cc.data_ptr(), _lib.stream_ptr())
+    for dbg in (0, 1, 4, 5):
+        os.environ["REALB_DBG_ROUTER"] = str(dbg)
+        for _ in range(3): f()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10):
+            a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+            a.record(); f(); b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
+        t = sorted(ts)[5]
+        print(f"T={T} dbg={dbg} {t*1e3:8.1f} us  {T*H*2/t/1e9:8.1f} GB/s", flush=True)
