@@ -35,7 +35,7 @@ struct RouterSmem {
   static constexpr int STAGE_TX = A_LOAD + B_BYTES;
   // as many stages as fit in ~200 KB: the router is latency-bound per SM (one CTA
   // per 128 tokens), so bytes in flight set its HBM throughput
-  static constexpr int STAGES = (200 * 1024) / STAGE > 12 ? 12 : (200 * 1024) / STAGE;
+  static constexpr int STAGES = 4;
   static constexpr int HIST_OFF = STAGES * STAGE;
   static constexpr int BAR_OFF = HIST_OFF + 256 * 2 * 4;
   static constexpr int TOTAL = BAR_OFF + 128 + 1024;
