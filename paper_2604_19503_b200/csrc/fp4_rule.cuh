@@ -73,6 +73,19 @@ __device__ __forceinline__ uint32_t block_scale_bits_f32(float amax) {
   uint32_t s = e4m3_encode_f32(__fdiv_rn(amax, 6.0f));  // IEEE division, DESIGN.md §Q
   return s == 0u ? 1u : s;
 }
+// Same for a bf16-representable amax without the IEEE-division slow path:
+// q = amax * rn(1/6) refined by one FMA residual step is the correctly rounded
+// amax / 6 for normal results; results below 2^-10 (where subnormal rounding
+// could differ) all encode to scale bits 0 -> 1 regardless. Verified over every
+// positive finite bf16 amax (tests/test_quant_gpu.py::test_all_bf16_amax_bf16_path).
+__device__ __forceinline__ uint32_t block_scale_bits_bf16amax(float amax) {
+  if (amax == 0.0f) return 0u;
+  const float r6 = 0.16666667163372039794921875f;  // rn(1/6)
+  const float q0 = amax * r6;
+  const float q = fmaf(fmaf(-q0, 6.0f, amax), r6, q0);
+  uint32_t s = e4m3_encode_f32(q);
+  return s == 0u ? 1u : s;
+}
 __device__ __forceinline__ uint32_t block_scale_bits_f64(double amax) {
   if (amax == 0.0) return 0u;
   uint32_t s = e4m3_encode_f64(__ddiv_rn(amax, 6.0));
@@ -166,7 +179,7 @@ __device__ __forceinline__ uint2 quant_block16_bf16(const uint32_t (&w)[8], uint
   const uint32_t ab = amax_bits_bf16x16(w);
   nonfinite = ab >= 0x7F80u;
   const float amax = __uint_as_float(ab << 16);
-  sbits = block_scale_bits_f32(amax);
+  sbits = block_scale_bits_bf16amax(amax);
   if (sbits == 0u) return make_uint2(0u, 0u);
   const float sc = e4m3_decode(sbits);
   const float r = __frcp_rn(sc);
@@ -183,7 +196,7 @@ __device__ __forceinline__ uint2 quant_block16_bf16vals(const float (&v)[16], ui
   float amax = 0.0f;
 #pragma unroll
   for (int i = 0; i < 16; ++i) amax = fmaxf(amax, fabsf(v[i]));
-  sbits = block_scale_bits_f32(amax);
+  sbits = block_scale_bits_bf16amax(amax);
   if (sbits == 0u) return make_uint2(0u, 0u);
   const float sc = e4m3_decode(sbits);
   const float r = __frcp_rn(sc);

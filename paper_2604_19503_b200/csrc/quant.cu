@@ -52,22 +52,29 @@ __device__ __forceinline__ void quant_tile_bf16(const __nv_bfloat16* __restrict_
                                                 int64_t cols, int64_t nkb, int64_t tm, int64_t tk,
                                                 uint8_t* __restrict__ codes,
                                                 uint8_t* __restrict__ sf, int32_t* flag) {
+  // thread -> (row r0 + 64h, k-block kb): the two blocks are 64 rows apart
+  const int r_in = threadIdx.x >> 2, kq = threadIdx.x & 3;
+  const int64_t r0 = tm * 128 + r_in, kb = tk * 4 + kq;
+  const bool kok = kb < nkb;
+  const __nv_bfloat16* xp = x + r0 * cols + kb * 16;
+  const int64_t xstep = 64 * cols;
   uint32_t w[2][8];
   bool ok[2];
-  int64_t rr[2], kk[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int b = threadIdx.x + h * 256;
-    rr[h] = tm * 128 + (b >> 2);
-    kk[h] = tk * 4 + (b & 3);
-    ok[h] = rr[h] < rows && kk[h] < nkb;
+    ok[h] = kok && r0 + 64 * h < rows;
     if (ok[h]) {
-      const uint4* q = reinterpret_cast<const uint4*>(x + rr[h] * cols + kk[h] * 16);
+      const uint4* q = reinterpret_cast<const uint4*>(xp + h * xstep);
       const uint4 a = __ldg(q), c = __ldg(q + 1);
       w[h][0] = a.x; w[h][1] = a.y; w[h][2] = a.z; w[h][3] = a.w;
       w[h][4] = c.x; w[h][5] = c.y; w[h][6] = c.z; w[h][7] = c.w;
     }
   }
+  uint8_t* cp = codes + r0 * (cols >> 1) + kb * 8;
+  const int64_t cstep = 64 * (cols >> 1);
+  // MMA layout: rows r and r+64 land in the same 512-B atom, byte +8 apart
+  const int64_t so0 = LAYOUT == REALB_SF_FLAT ? r0 * nkb + kb : sf_mma_offset(r0, kb, nkb);
+  const int64_t sstep = LAYOUT == REALB_SF_FLAT ? 64 * nkb : 8;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (!ok[h]) continue;
@@ -75,10 +82,8 @@ __device__ __forceinline__ void quant_tile_bf16(const __nv_bfloat16* __restrict_
     bool nf;
     const uint2 c = quant_block16_bf16(w[h], sbits, nf);
     if (nf) flag_nonfinite(flag);
-    *reinterpret_cast<uint2*>(codes + rr[h] * (cols >> 1) + kk[h] * 8) = c;
-    const int64_t so =
-        LAYOUT == REALB_SF_FLAT ? rr[h] * nkb + kk[h] : sf_mma_offset(rr[h], kk[h], nkb);
-    sf[so] = (uint8_t)sbits;
+    *reinterpret_cast<uint2*>(cp + h * cstep) = c;
+    sf[so0 + h * sstep] = (uint8_t)sbits;
   }
 }
 

@@ -114,3 +114,25 @@ def test_max_ctas_and_stream(q):
         out = q.quantize_nvfp4(w, max_ctas=16, stream=s)
     s.synchronize()
     assert torch.equal(ref[0], out[0]) and torch.equal(ref[1], out[1])
+
+
+def test_all_bf16_amax_bf16_path(q, golden):
+    """Every positive finite bf16 amax through the bf16 product path (the
+    division-free scale computation), vs the reference's scale bits."""
+    import torch
+
+    s_ref = np.load(golden / "fp4_bf16_amax.npz")["scale_bits"]
+    blocks = torch.from_numpy(gen.bf16_amax_blocks()).to(torch.bfloat16)
+    _, s = q.quantize_blocks(blocks)
+    assert (s == s_ref).all()
+
+
+def test_bf16_path_row_tail_and_flat_layout(q):
+    """Rows not a multiple of 128 and the 64-row pairing of the tile routine."""
+    import torch
+
+    for rows, cols in [(1, 16), (63, 48), (65, 64), (130, 208), (191, 1408)]:
+        w = (torch.randn(rows, cols) * 3).to(torch.bfloat16)
+        codes, sf = q.quantize_nvfp4(w.cuda(), layout="flat")
+        oc, osf = oracle.quantize_bf16(w.view(torch.int16).numpy().view(np.uint16))
+        assert (codes.cpu().numpy() == oc).all() and (sf.cpu().numpy() == osf).all(), (rows, cols)
