@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
                                                      int32_t* __restrict__ layout,
                                                      int32_t* __restrict__ expert_vt,
                                                      PlanParams pp, int32_t* plan_out, int ra) {
-  __shared__ int32_t s_v[1024], s_t[1024];
+  __shared__ int32_t s_v[1024], s_t[1024], s_scan[7 * 256];
   __shared__ int32_t s_cnt[256], s_start[256], s_vt[512];
   __shared__ uint8_t s_prec[256];
   const int G = blockDim.x / E;  // chunk groups per expert
@@ -94,34 +94,57 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
     s_prec[threadIdx.x] = prec[threadIdx.x];
   }
   __syncthreads();
-  // serial part on shared memory only (global writes are fire-and-forget)
-  if (threadIdx.x == 0) {
-    if (pp.enabled) plan_on_device(s_vt, E, pp, s_prec, plan_out);
-    int run = 0;
-    for (int i = 0; i < E; ++i) {
-      s_start[i] = run;
-      run += (s_cnt[i] + ra - 1) / ra * ra;
-    }
-    layout[0] = run;
-    for (int w = 3; w < 8; ++w) layout[w] = 0;  // GEMM tile counters (grouped.cuh)
-    for (int p = 0; p < 2; ++p) {
-      int32_t* gl = layout + LayoutView::off_glist(E, p);
-      int32_t* pf = layout + LayoutView::off_prefix(E, p);
-      int32_t* pp2 = layout + LayoutView::off_pprefix(E, p);
-      int gg = 0, mt = 0, np = 0;
-      for (int i = 0; i < E; ++i) {
-        if ((int)s_prec[i] != p) continue;
-        gl[gg] = i;
-        pf[gg] = mt;
-        pp2[gg] = np;
-        const int m = (s_cnt[i] + 127) / 128;
-        mt += m;
-        np += (m + 1) / 2;
-        ++gg;
+  if (pp.enabled) {
+    if (threadIdx.x == 0) plan_on_device(s_vt, E, pp, s_prec, plan_out);
+    __syncthreads();
+  }
+  // Parallel scans over the E <= 256 experts (threads 0..255): padded row starts
+  // and, per precision class, the compacted group list with m-tile and m-tile-pair
+  // prefixes. Hillis-Steele in shared memory; one value set per precision.
+  {
+    const int e = threadIdx.x;
+    const bool in = e < E;
+    const int cnt = in ? s_cnt[e] : 0;
+    const int padded = in ? (cnt + ra - 1) / ra * ra : 0;
+    const int m = in ? (cnt + 127) / 128 : 0;
+    const int pe = in ? (int)s_prec[e] : -1;
+    // 4 scanned quantities: padded rows, and for p in {0,1}: (flag, m-tiles, pairs)
+    int v[7] = {padded, pe == 0, pe == 0 ? m : 0, pe == 0 ? (m + 1) / 2 : 0,
+                pe == 1, pe == 1 ? m : 0, pe == 1 ? (m + 1) / 2 : 0};
+    int incl[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) incl[j] = v[j];
+    for (int off = 1; off < 256; off <<= 1) {
+      if (e < 256) {
+#pragma unroll
+        for (int j = 0; j < 7; ++j) s_scan[j * 256 + e] = incl[j];
       }
-      pf[gg] = mt;
-      pp2[gg] = np;
-      layout[1 + p] = gg;
+      __syncthreads();
+      if (e < 256 && e >= off) {
+#pragma unroll
+        for (int j = 0; j < 7; ++j) incl[j] += s_scan[j * 256 + e - off];
+      }
+      __syncthreads();
+    }
+    if (in) {
+      s_start[e] = incl[0] - v[0];
+      for (int p = 0; p < 2; ++p) {
+        if (pe != p) continue;
+        const int g = incl[1 + 3 * p] - 1;  // exclusive rank among experts of class p
+        layout[LayoutView::off_glist(E, p) + g] = e;
+        layout[LayoutView::off_prefix(E, p) + g] = incl[2 + 3 * p] - v[2 + 3 * p];
+        layout[LayoutView::off_pprefix(E, p) + g] = incl[3 + 3 * p] - v[3 + 3 * p];
+      }
+    }
+    if (e == E - 1) {
+      layout[0] = incl[0];
+      for (int w = 3; w < 8; ++w) layout[w] = 0;  // GEMM tile counters (grouped.cuh)
+      for (int p = 0; p < 2; ++p) {
+        const int G = incl[1 + 3 * p];
+        layout[1 + p] = G;
+        layout[LayoutView::off_prefix(E, p) + G] = incl[2 + 3 * p];
+        layout[LayoutView::off_pprefix(E, p) + G] = incl[3 + 3 * p];
+      }
     }
   }
   __syncthreads();

@@ -316,7 +316,13 @@ class MoELayer:
         sp = _lib.stream_ptr(main)
         self.route(x, modality)
         self.align_plan(T, strategy, params)
-        mixed = _STRATEGY_CODE[strategy] != 0
+        # NVFP4 launches are needed unless the plan provably stays all-W16A16: the
+        # baseline strategies, or realb on one rank with C >= 1 (a rank's load is
+        # then exactly the mean, never > C x mean; balancers.py:103-104). This is a
+        # static property of (strategy, R, C), not of the data.
+        code = _STRATEGY_CODE[strategy]
+        mixed = code == 1 or (code == 2 and not (self.cluster.num_ranks == 1
+                                                 and params.capacity_factor >= 1.0))
         if mixed:
             ws = self._fp4_ws()
             self.side.wait_stream(main)
