@@ -8,11 +8,15 @@ experts' rows). The layer's compute-only latency is the max over ranks, the
 definition of ``LayerTiming.compute_only_ns`` (engine.py:156) and of the
 paper's layer latency with dispatch/combine excluded.
 
-Communication is not executed on one GPU; the full-path figure fills the
-reference ``RankPhases`` schema with the measured compute / transform times
-and a stated NVLink projection for dispatch/combine (bytes each rank receives
-/ 770 GB/s measured peer bandwidth + 10 us), i.e. engine.py's overlap rule with
-measured terms where measurement exists. It is labelled a projection.
+Communication is not executed on one GPU. The full-path figure fills the
+reference ``RankPhases`` schema with the measured compute / transform times and
+a stated NVLink projection for dispatch and combine: the exact per-rank send and
+receive bytes of this batch's routing (token t lives on rank t // T_local,
+pair (t, e) goes to rank e // experts_per_rank) over 770 GB/s measured peer
+bandwidth + 10 us, every all-to-all finishing with its slowest rank; then
+engine.py's overlap rule (RankPhases.total, engine.py:63-76). It is labelled a
+projection. With ``fp4_dispatch`` the rows bound for W4A4 ranks travel as NVFP4
+(H/2 code bytes + H/16 scale bytes instead of 2H).
 """
 
 from __future__ import annotations
@@ -38,86 +42,170 @@ def _median_ms(torch, fn, reps=7):
     return float(sorted(ts)[len(ts) // 2])
 
 
-def virtual_ep_report(args, torch, R: int = 8) -> dict:
-    from . import _lib
-    from .workload import WorkloadSpec, make_batch, make_experts
+def traffic_matrix(idx: np.ndarray, T_local: int, epr: int, R: int) -> np.ndarray:
+    """pairs[src_rank, dst_rank] of one layer's dispatch (DP tokens, contiguous EP)."""
+    src = np.repeat(np.arange(idx.shape[0]) // T_local, idx.shape[1])
+    dst = idx.reshape(-1).astype(np.int64) // epr
+    return np.bincount(src * R + dst, minlength=R * R).reshape(R, R)
 
-    shape = SHAPES[args.config]
-    E, H = shape.num_experts, shape.hidden
-    if E % R:
-        return {"skipped": f"{E} experts not divisible by {R}"}
-    T = args.tokens * R
-    spec = WorkloadSpec(tokens=T, vision_frac=args.vision_frac, num_ranks=R)
-    x, mod, router, _ = make_batch(shape, spec)
-    gu, dn = make_experts(shape)
-    bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
-    w = MoEWeights.from_hf(shape, router, gu, dn, bias=bias)
-    del gu, dn
-    epr = E // R
-    cluster = ClusterConfig(R, 1, epr, 1, shape.modality_isolated)
-    layer = MoELayer(w, max_tokens=T, cluster=cluster)
-    params = RealbParams()
 
-    res = layer.forward(x, mod, "realb", params)
-    torch.cuda.synchronize()
-    plan = res.plan
-    prec = plan.expert_precision(layer.placement).astype(np.int64)
-    vt = res.expert_vt.astype(np.int64)
-    rank_vt = vt.reshape(R, epr, 2).sum(1)
+def a2a_ms(pairs: np.ndarray, row_bytes_to: np.ndarray) -> float:
+    """One all-to-all over NVLink: every rank's max(send, receive) bytes (self
+    traffic excluded) / peer bandwidth, finishing with the slowest rank."""
+    R = pairs.shape[0]
+    off = pairs * (1 - np.eye(R, dtype=pairs.dtype))
+    bytes_ = off * row_bytes_to[None, :]
+    per_rank = np.maximum(bytes_.sum(1), bytes_.sum(0))
+    return ALPHA_US / 1e3 + float(per_rank.max()) / (NVLINK_GBPS * 1e9) * 1e3
 
-    def per_rank(p_full):
-        out = []
-        for r in range(R):
+
+def measure_rank_compute(torch, layer, T: int, precs, R: int, epr: int, reps: int = 7):
+    """Per virtual rank, the expert compute of that rank's experts alone (their
+    grouped-GEMM launches over the rows the last forward dispatched), for each
+    expert-precision vector in ``precs`` (codes 0 W16A16 / 1 W4A4). Arms are
+    interleaved per repetition; returns one [R] list of median ms per arm."""
+    E = R * epr
+    out = [[0.0] * R for _ in precs]
+    for r in range(R):
+        masks = []
+        for p in precs:
             m = np.full(E, 2, np.int64)
-            m[r * epr:(r + 1) * epr] = p_full[r * epr:(r + 1) * epr]
-            out.append(_median_ms(torch, lambda: layer.expert_compute(T, m)))
-        return out
+            m[r * epr:(r + 1) * epr] = p[r * epr:(r + 1) * epr]
+            masks.append(m)
+        ts = [[] for _ in precs]
+        for _ in range(reps):
+            for a, m in enumerate(masks):
+                ts[a].append(_median_ms(torch, lambda: layer.expert_compute(T, m), reps=1))
+        for a in range(len(precs)):
+            out[a][r] = float(sorted(ts[a])[len(ts[a]) // 2])
+    return out
 
-    realb_ms = per_rank(prec)
-    transform_ms = [0.0] * R
+
+def measure_transform(torch, layer, prec, R: int, epr: int) -> list[float]:
+    """K3 time per rank: quantising that rank's experts (0 on W16A16 ranks)."""
+    out = [0.0] * R
     for r in range(R):
         if prec[r * epr] == 1:
-            transform_ms[r] = _median_ms(torch, lambda: layer.quantize_experts(range(r * epr, (r + 1) * epr)))
-    whole_realb = _median_ms(torch, lambda: layer.forward(x, mod, "realb", params), reps=5)
-    layer.forward(x, mod, "baseline")
-    torch.cuda.synchronize()
-    bf16_ms = per_rank(np.zeros(E, np.int64))
-    whole_bf16 = _median_ms(torch, lambda: layer.forward(x, mod, "baseline"), reps=5)
+            out[r] = _median_ms(torch, lambda: layer.quantize_experts(range(r * epr, (r + 1) * epr)))
+    return out
 
-    # projected full path: engine.py:120-159 overlap rule with measured compute/transform
-    recv_bytes = rank_vt.sum(1) * (R - 1) / R * H * 2  # pairs from remote ranks, bf16 rows
-    disp_ms = [ALPHA_US / 1e3 + b / (NVLINK_GBPS * 1e9) * 1e3 for b in recv_bytes]
-    sched_ms = ALPHA_US / 1e3
 
-    def timing(comp, trans, accelerated, mode):
-        phases, totals = [], []
-        worst = max(disp_ms)  # globally synchronised all-to-all: every rank waits for the slowest
-        for r in range(R):
-            ph = RankPhases(int(sched_ms * 1e6), int(trans[r] * 1e6), int(worst * 1e6), int(comp[r] * 1e6),
-                            int(worst * 1e6))
-            phases.append(ph)
-            totals.append(ph.total(mode, accelerated[r]))
-        lat = max(totals)
-        return LayerTiming(tuple(phases), tuple(totals), lat, max(p.compute_ns for p in phases),
-                           totals.index(lat), mode)
+def layer_timing(comp_ms, trans_ms, accelerated, mode: PipelineMode, disp_ms: float, comb_ms: float,
+                 sched_ms: float = ALPHA_US / 1e3) -> LayerTiming:
+    """LayerTiming (engine.py:79-86, :141-159) from per-rank measured compute and
+    transform and a globally synchronised dispatch/combine time."""
+    phases, totals = [], []
+    for r in range(len(comp_ms)):
+        ph = RankPhases(int(sched_ms * 1e6), int(trans_ms[r] * 1e6), int(disp_ms * 1e6), int(comp_ms[r] * 1e6),
+                        int(comb_ms * 1e6))
+        phases.append(ph)
+        totals.append(ph.total(mode, accelerated[r]))
+    lat = max(totals)
+    return LayerTiming(tuple(phases), tuple(totals), lat, max(p.compute_ns for p in phases),
+                       totals.index(lat), mode)
 
-    acc = [bool(prec[r * epr] == 1) for r in range(R)]
-    lt_realb = timing(realb_ms, transform_ms, acc, PipelineMode.OVERLAPPED if plan.active else PipelineMode.SEQUENTIAL)
-    lt_bf16 = timing(bf16_ms, [0.0] * R, [False] * R, PipelineMode.SEQUENTIAL)
-    return {
-        "what": f"EP{R} emulated on 1 GPU: global batch {T} tokens, plan over {R} virtual ranks, "
-                "per-rank expert compute timed in isolation (layer = max over ranks)",
-        "plan_w4a4_ranks": sorted(plan.accelerated_ranks), "hot_ranks": sorted(plan.hot_ranks),
-        "vision_heavy_ranks": sorted(plan.vision_heavy_ranks),
-        "rank_pairs": rank_vt.sum(1).tolist(),
-        "rank_vision_ratio": [round(float(a / max(1, a + b)), 3) for a, b in rank_vt],
-        "per_rank_compute_ms": {"bf16": bf16_ms, "realb": realb_ms},
-        "transform_ms": transform_ms,
-        "compute_only_ms": {"bf16": max(bf16_ms), "realb": max(realb_ms)},
-        "compute_only_speedup": max(bf16_ms) / max(realb_ms),
-        "one_gpu_whole_layer_ms": {"bf16": whole_bf16, "realb": whole_realb},
-        "projected_full_path_ms": {"bf16": lt_bf16.layer_latency_ns / 1e6, "realb": lt_realb.layer_latency_ns / 1e6,
-                                   "model": f"dispatch=combine={ALPHA_US}us + max_r recv_bytes_r/{NVLINK_GBPS}GB/s"},
-        "projected_full_path_speedup": lt_bf16.layer_latency_ns / lt_realb.layer_latency_ns,
-        "transform_hidden": all(t <= max(disp_ms) for t in transform_ms),
-    }
+
+class VirtualEP:
+    """One model shape at EP degree R emulated on cuda:0; weights built once,
+    batches (vision fraction, routing skew) regenerated per report."""
+
+    def __init__(self, torch, config: str, R: int, tokens_per_rank: int):
+        from . import _lib
+        from .workload import make_experts
+
+        self.torch = torch
+        self.shape = shape = SHAPES[config]
+        E = shape.num_experts
+        if E % R:
+            raise ValueError(f"{E} experts not divisible by {R}")
+        self.R, self.T_local, self.T = R, tokens_per_rank, tokens_per_rank * R
+        gu, dn = make_experts(shape)
+        self.bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
+        self.gu, self.dn = gu, dn
+        self.epr = E // R
+        self.cluster = ClusterConfig(R, 1, self.epr, 1, shape.modality_isolated)
+        self.layer = None
+
+    def _layer_for(self, router):
+        w = MoEWeights.from_hf(self.shape, router, self.gu, self.dn, bias=self.bias)
+        if self.layer is None:
+            self.layer = MoELayer(w, max_tokens=self.T, cluster=self.cluster)
+        else:
+            self.layer.w = w
+        return self.layer
+
+    def report(self, vision_frac: float = 0.7, zipf_s: float = 0.57, seed: int = 2024,
+               params: RealbParams | None = None) -> dict:
+        from .workload import WorkloadSpec, make_batch
+
+        torch, shape, R, T, epr = self.torch, self.shape, self.R, self.T, self.epr
+        E, H = shape.num_experts, shape.hidden
+        spec = WorkloadSpec(tokens=T, vision_frac=vision_frac, num_ranks=R, zipf_s=zipf_s, seed=seed)
+        x, mod, router, _ = make_batch(shape, spec)
+        layer = self._layer_for(router)
+        params = params or RealbParams()
+
+        # baseline first (bf16 rows of every expert), then realb (NVFP4 rows and weights
+        # of its W4A4 experts): both arms' per-rank compute then reads valid operands
+        layer.forward(x, mod, "baseline")
+        res = layer.forward(x, mod, "realb", params)
+        torch.cuda.synchronize()
+        plan = res.plan
+        prec = plan.expert_precision(layer.placement).astype(np.int64)
+        vt = res.expert_vt.astype(np.int64)
+        rank_vt = vt.reshape(R, epr, 2).sum(1)
+        idx = layer.topk_idx[:T].cpu().numpy()
+
+        # every rank's compute under both plans, measured interleaved (clock / power drift
+        # hits both arms alike), then the whole one-GPU layer under each strategy
+        bf16_ms, realb_ms = measure_rank_compute(torch, layer, T, [np.zeros(E, np.int64), prec], R, epr)
+        transform_ms = measure_transform(torch, layer, prec, R, epr)
+        whole_realb = _median_ms(torch, lambda: layer.forward(x, mod, "realb", params), reps=5)
+        whole_bf16 = _median_ms(torch, lambda: layer.forward(x, mod, "baseline"), reps=5)
+
+        # projected full path: engine.py:120-159 overlap rule, measured compute/transform
+        pairs = traffic_matrix(idx, self.T_local, epr, R)
+        acc = [bool(prec[r * epr] == 1) for r in range(R)]
+        disp_bf16, comb = a2a_ms(pairs, np.full(R, 2.0 * H)), a2a_ms(pairs.T.copy(), np.full(R, 2.0 * H))
+        disp_fp4 = a2a_ms(pairs, np.where(acc, H / 2 + H / 16, 2.0 * H))
+        mode = PipelineMode.OVERLAPPED if plan.active else PipelineMode.SEQUENTIAL
+        lt_realb = layer_timing(realb_ms, transform_ms, acc, mode, disp_bf16, comb)
+        lt_realb4 = layer_timing(realb_ms, transform_ms, acc, mode, disp_fp4, comb)
+        lt_bf16 = layer_timing(bf16_ms, [0.0] * R, [False] * R, PipelineMode.SEQUENTIAL, disp_bf16, comb)
+        text_total = int(rank_vt[:, 1].sum())
+        text_fp4 = int(sum(rank_vt[r, 1] for r in range(R) if acc[r]))
+        return {
+            "what": f"EP{R} emulated on 1 GPU: global batch {T} tokens, plan over {R} virtual ranks, "
+                    "per-rank expert compute timed in isolation (layer = max over ranks)",
+            "config": shape.name, "ep_ranks": R, "tokens_per_rank": self.T_local,
+            "vision_frac": vision_frac, "zipf_s": zipf_s,
+            "plan_active": bool(plan.active),
+            "plan_w4a4_ranks": sorted(plan.accelerated_ranks), "hot_ranks": sorted(plan.hot_ranks),
+            "vision_heavy_ranks": sorted(plan.vision_heavy_ranks),
+            "rank_pairs": rank_vt.sum(1).tolist(),
+            "device_imbalance": float(rank_vt.sum(1).max() / rank_vt.sum(1).mean()),
+            "rank_vision_ratio": [round(float(a / max(1, a + b)), 3) for a, b in rank_vt],
+            "text_exposure": text_fp4 / text_total if text_total else 0.0,
+            "per_rank_compute_ms": {"bf16": bf16_ms, "realb": realb_ms},
+            "transform_ms": transform_ms,
+            "compute_only_ms": {"bf16": max(bf16_ms), "realb": max(realb_ms)},
+            "compute_only_speedup": max(bf16_ms) / max(realb_ms),
+            "one_gpu_whole_layer_ms": {"bf16": whole_bf16, "realb": whole_realb},
+            "projected_dispatch_ms": {"bf16_rows": disp_bf16, "fp4_rows_to_w4a4": disp_fp4, "combine": comb},
+            "projected_full_path_ms": {"bf16": lt_bf16.layer_latency_ns / 1e6,
+                                       "realb": lt_realb.layer_latency_ns / 1e6,
+                                       "realb_fp4_dispatch": lt_realb4.layer_latency_ns / 1e6,
+                                       "model": f"a2a = {ALPHA_US}us + max_r max(send_r, recv_r) bytes / "
+                                                f"{NVLINK_GBPS} GB/s; RankPhases.total overlap rule"},
+            "projected_full_path_speedup": lt_bf16.layer_latency_ns / lt_realb.layer_latency_ns,
+            "projected_full_path_speedup_fp4_dispatch": lt_bf16.layer_latency_ns / lt_realb4.layer_latency_ns,
+            "transform_hidden": all(t <= disp_bf16 for t in transform_ms),
+        }
+
+
+def virtual_ep_report(args, torch, R: int = 8) -> dict:
+    """bench.py's virtual-EP8 block at the bench workload."""
+    shape = SHAPES[args.config]
+    if shape.num_experts % R:
+        return {"skipped": f"{shape.num_experts} experts not divisible by {R}"}
+    return VirtualEP(torch, args.config, R, args.tokens).report(args.vision_frac)

@@ -1,0 +1,50 @@
+"""Replay reference-generated routing traces on the B200 and write the run
+directories in the reference's schemas (layers.csv / ranks.csv / events.csv /
+summary.json), plus the speedup report `moesim compare` would compute.
+
+  python scripts/replay_trace.py [--trace tests/golden/trace_prefill_ep8.csv] [--out gpurun_out/replay]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--trace", default="tests/golden/trace_prefill_ep8.csv")
+    p.add_argument("--config", default="kimi")
+    p.add_argument("--out", default="gpurun_out/replay")
+    a = p.parse_args()
+    import torch
+
+    from paper_2604_19503_b200.policy import ClusterConfig
+    from paper_2604_19503_b200.replay import TraceReplay, file_sha256, read_trace, speedup_report, write_run
+
+    meta = json.load(open("tests/golden/trace_plans.json"))
+    cluster = ClusterConfig(**meta["cluster"])
+    trace = read_trace(a.trace, cluster)
+    rep = TraceReplay(torch, a.config, trace)
+    runs, checks = rep.run(strategies=("baseline", "fp4all", "realb"))
+    digest = file_sha256(a.trace)
+    name = os.path.splitext(os.path.basename(a.trace))[0]
+    summaries = {s: write_run(r, trace, os.path.join(a.out, name, s), digest, ranks_iters=(0,))
+                 for s, r in runs.items()}
+    report = speedup_report(summaries)
+    ok = all(c["routing_equal"] and c["counts_equal"] and c["plan_equal_pairs"] and c["plan_equal_trace"]
+             for c in checks)
+    out = {"trace": a.trace, "trace_sha256": digest, "config": a.config, "layers": len(checks) // 3,
+           "parity_all_layers": ok, "report": report,
+           "failed_checks": [c for c in checks if not (c["routing_equal"] and c["counts_equal"]
+                                                        and c["plan_equal_pairs"] and c["plan_equal_trace"])][:6],
+           "w4a4_ranks_per_layer": {f"{c['iter']},{c['layer']}": c["w4a4_ranks"] for c in checks
+                                    if c["strategy"] == "realb"}}
+    with open(os.path.join(a.out, name, "report.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
