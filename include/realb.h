@@ -187,6 +187,32 @@ REALB_API int realb_ep_regroup(const int32_t* d_cnt, int R, int El, const uint8_
                                int64_t n_recv, int32_t* d_layout, int32_t* d_base,
                                int32_t* d_row_expert, int32_t* d_row_pos, void* stream);
 
+/* EP send side (C2 pack), with the NVFP4 activation dispatch of SURVEY.md
+ * §8f-1: expert-sorted positions of every (token, slot) pair (as
+ * realb_dispatch_permute over d_layout built with row_align 1), then each row is
+ * written into the send buffer segment of its destination rank d = e/(E/R):
+ *   byte offset h_rank_byte0[d] + (pos - h_rank_row0[d]) * row_bytes(d)
+ *   h_rank_fmt[d] = 0: bf16 row, row_bytes = 2H
+ *   h_rank_fmt[d] = 1: NVFP4 row quantised with the reference block rule along H
+ *                      (fp4.py:173-227, the K4 rule), packed as [H/2 code bytes]
+ *                      [H/16 E4M3 scale bytes], row_bytes = H/2 + H/16
+ * h_* are HOST arrays of R entries (read during the call; the plan and the
+ * split sizes are host-known after the C1 count exchange); byte offsets 16-byte
+ * aligned. R <= 64. Replaces the dispatch term of costmodel.dispatch_latency
+ * (costmodel.py:71-76) — bytes to W4A4 ranks drop 3.6x. */
+REALB_API int realb_ep_pack(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                            const int32_t* d_layout, int nchunks, int R, const uint8_t* h_rank_fmt,
+                            const int32_t* h_rank_row0, const int64_t* h_rank_byte0,
+                            int32_t* d_pair_pos, uint8_t* d_send, int32_t* d_nonfinite_flag,
+                            void* stream);
+
+/* EP receive side of the NVFP4 dispatch: n packed rows (format of
+ * realb_ep_pack, fmt 1) -> codes at row d_pos[i] of d_a_codes [rows][H/2] and
+ * scales into the REALB_SF_MMA128x4 layout of d_a_sf. H % 256 == 0. */
+REALB_API int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_t* d_pos, int64_t n,
+                                             int H, uint8_t* d_a_codes, uint8_t* d_a_sf,
+                                             void* stream);
+
 /* dst[i] = src[idx[i]] for bf16 rows of H (EP return path before C3). */
 REALB_API int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t n, int H,
                                void* d_dst, void* stream);

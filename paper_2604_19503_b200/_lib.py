@@ -60,6 +60,9 @@ SIGNATURES: dict[str, tuple] = {
         _i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _vp]),
     "realb_combine": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "realb_plan": (_i32, [_vp, _i32, _f64, _f64, _i64, _i32, _vp, _vp]),
+    "realb_ep_pack": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                             _vp]),
+    "realb_gather_rows_nvfp4_packed": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),
 }
 
 _lib: C.CDLL | None = None
@@ -71,6 +74,7 @@ LAUNCHES_KERNEL = {
     "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_nvfp4": 1, "realb_combine": 1,
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
+    "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 

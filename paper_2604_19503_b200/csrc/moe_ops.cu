@@ -400,6 +400,85 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
   }
 }
 
+// ----------------------------------------------------------------- EP pack (send side, C2)
+// One warp per (token, slot) pair: the row goes to destination rank d = e / El,
+// at byte offset byte0[d] + (pos - row0[d]) * row_bytes(fmt[d]) of the send
+// buffer (pos = the pair's place in the expert-sorted, unpadded order, so each
+// destination's rows are one contiguous segment). fmt 0: the bf16 row (2H
+// bytes); fmt 1: the row quantised to NVFP4 with the reference block rule along
+// H (K4 moved before dispatch) as one packed row:
+// [H/2 code bytes][H/16 E4M3 scale bytes] — 0.5625 H bytes instead of 2 H.
+constexpr int kMaxEpRanks = 64;
+struct EpPackMeta {
+  int R, El;
+  uint8_t fmt[kMaxEpRanks];
+  int32_t row0[kMaxEpRanks];
+  int64_t byte0[kMaxEpRanks];
+};
+
+__global__ void __launch_bounds__(256) ep_pack_rows_kernel(
+    const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ topk_idx,
+    const int32_t* __restrict__ pair_pos, int64_t P, int H, int k, const EpPackMeta m,
+    uint8_t* __restrict__ dst, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int nkb = H / 16;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = p / k;
+    const int d = topk_idx[p] / m.El;
+    const int64_t rel = (int64_t)pair_pos[p] - m.row0[d];
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+    if (m.fmt[d] == 0) {
+      uint4* o = reinterpret_cast<uint4*>(dst + m.byte0[d] + rel * (2 * (int64_t)H));
+      for (int i = lane; i < H / 8; i += 32) o[i] = __ldg(src + i);
+    } else {
+      uint8_t* row = dst + m.byte0[d] + rel * (int64_t)(H / 2 + H / 16);
+      for (int g = lane; g < nkb / 4; g += 32) {
+        uint32_t sfw = 0;
+        uint2 cw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint4 u0 = __ldg(src + (g * 4 + b) * 2), u1 = __ldg(src + (g * 4 + b) * 2 + 1);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          uint32_t sb;
+          bool nf;
+          cw[b] = quant_block16_bf16(w, sb, nf);
+          if (nf && flag) atomicOr(flag, 1);
+          sfw |= sb << (8 * b);
+        }
+        uint4* cdst = reinterpret_cast<uint4*>(row + g * 32);
+        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
+        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
+        reinterpret_cast<uint32_t*>(row + H / 2)[g] = sfw;
+      }
+    }
+  }
+}
+
+// EP receive side of the NVFP4 dispatch: packed rows -> grouped NVFP4 operand
+// (codes row-major at the row's grouped position, scales into the tcgen05
+// block-scale layout). Pure byte movement: the codes are the sender's.
+__global__ void __launch_bounds__(256) gather_packed_fp4_kernel(const uint8_t* __restrict__ src,
+                                                                const int32_t* __restrict__ row_pos,
+                                                                int64_t n, int H,
+                                                                uint8_t* __restrict__ a_codes,
+                                                                uint8_t* __restrict__ a_sf) {
+  const int lane = threadIdx.x & 31;
+  const int nkb = H / 16;
+  const int64_t rb = H / 2 + H / 16;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t pos = row_pos[i];
+    const uint8_t* row = src + i * rb;
+    const uint4* c4 = reinterpret_cast<const uint4*>(row);
+    uint4* o4 = reinterpret_cast<uint4*>(a_codes + pos * (H / 2));
+    for (int j = lane; j < H / 32; j += 32) o4[j] = __ldg(c4 + j);
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(row + H / 2);
+    for (int g = lane; g < nkb / 4; g += 32)
+      *reinterpret_cast<uint32_t*>(a_sf + sf_mma_offset(pos, (int64_t)g * 4, nkb)) = __ldg(s4 + g);
+  }
+}
+
 }  // namespace realb
 
 using namespace realb;
@@ -546,4 +625,56 @@ extern "C" int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t
       reinterpret_cast<const __nv_bfloat16*>(d_src), d_idx, n, H,
       reinterpret_cast<__nv_bfloat16*>(d_dst));
   return check_launch("realb_index_rows");
+}
+
+extern "C" int realb_ep_pack(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                             const int32_t* d_layout, int nchunks, int R, const uint8_t* h_rank_fmt,
+                             const int32_t* h_rank_row0, const int64_t* h_rank_byte0,
+                             int32_t* d_pair_pos, uint8_t* d_send, int32_t* d_flag, void* stream) {
+  if (!d_x || !d_topk_idx || !d_layout || !d_pair_pos || !d_send || !h_rank_fmt || !h_rank_row0 ||
+      !h_rank_byte0 || T < 0 || H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || R < 1 ||
+      R > kMaxEpRanks || E % R || nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
+    set_error("realb_ep_pack: bad arguments (T=%d H=%d E=%d k=%d R=%d nchunks=%d)", T, H, E, k, R,
+              nchunks);
+    return REALB_EINVAL;
+  }
+  EpPackMeta m{};
+  m.R = R;
+  m.El = E / R;
+  for (int d = 0; d < R; ++d) {
+    if (h_rank_fmt[d] > 1 || (h_rank_byte0[d] & 15)) {
+      set_error("realb_ep_pack: rank %d: format must be 0/1 and byte offsets 16-byte aligned", d);
+      return REALB_EINVAL;
+    }
+    m.fmt[d] = h_rank_fmt[d];
+    m.row0[d] = h_rank_row0[d];
+    m.byte0[d] = h_rank_byte0[d];
+  }
+  if (T == 0) return REALB_OK;
+  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout,
+                                                                d_pair_pos);
+  int rc = check_launch("realb_ep_pack (positions)");
+  if (rc) return rc;
+  const int64_t P = (int64_t)T * k;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  ep_pack_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, m, d_send, d_flag);
+  return check_launch("realb_ep_pack (rows)");
+}
+
+extern "C" int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_t* d_pos, int64_t n,
+                                              int H, uint8_t* d_a_codes, uint8_t* d_a_sf,
+                                              void* stream) {
+  if (!d_src || !d_pos || !d_a_codes || !d_a_sf || n < 0 || H <= 0 || H % 256) {
+    set_error("realb_gather_rows_nvfp4_packed: bad arguments (H=%d; H %% 256 == 0)", H);
+    return REALB_EINVAL;
+  }
+  if (n == 0) return REALB_OK;
+  int64_t grid = (n + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  gather_packed_fp4_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(d_src, d_pos, n, H,
+                                                                             d_a_codes, d_a_sf);
+  return check_launch("realb_gather_rows_nvfp4_packed");
 }

@@ -9,10 +9,13 @@ Per layer on rank r of R (contiguous placement: rank r hosts experts
          NCCL's all_to_allv needs anyway for its split sizes
   P1     plan_for(strategy) on the global loads (policy.py -> C realb_plan,
          balancers.py:89-122); my precision = plan[r]
-  pack   rows sorted by global expert (unpadded): rank-contiguous send buffer
+  pack   rows sorted by global expert (unpadded): rank-contiguous send buffer;
+         rows bound for W4A4 ranks are quantised to packed NVFP4 on the sender
+         (fp4_dispatch, SURVEY.md §8f-1: 0.5625 H instead of 2 H bytes per row;
+         same codes the receiver's K4 would produce, so results are unchanged)
   K3     [side stream] quantise my experts' weights if plan[r] is W4A4 — issued
          before C2 so it runs under the dispatch
-  C2     all_to_all_v of bf16 token rows
+  C2     all_to_all_v of the token rows (bytes)
   regroup + K4 + K5/K6   grouped expert MLPs over the received rows
   C3     all_to_all_v back, then the weighted top-k combine
 
@@ -90,11 +93,11 @@ class CudaEPOps:
         self.vt_local = torch.empty(E, 2, dtype=i32, device=dev)
         self.zero_prec = torch.zeros(E, dtype=u8, device=dev)
         self.send_pos = torch.empty(T, k, dtype=i32, device=dev)
-        self.send_buf = torch.empty(T * k, H, dtype=bf, device=dev)
+        self.send_buf = torch.empty(T * k * 2 * H, dtype=u8, device=dev)  # byte segments per rank
         self.ret_buf = torch.empty(T * k, H, dtype=bf, device=dev)
         recv_cap = world * T * k  # every token of every rank could pick my experts
         self.recv_cap = recv_cap
-        self.recv_buf = torch.empty(recv_cap, H, dtype=bf, device=dev)
+        self.recv_buf = torch.empty(recv_cap * 2 * H, dtype=u8, device=dev)
         self.back_buf = torch.empty(recv_cap, H, dtype=bf, device=dev)
         self.row_expert = torch.empty(recv_cap, dtype=i32, device=dev)
         self.row_pos = torch.empty(recv_cap, dtype=i32, device=dev)
@@ -141,20 +144,28 @@ class CudaEPOps:
                   1, self.send_layout.data_ptr(), self.vt_local.data_ptr(), sp)
         return self.topk_idx[:T], self.topk_w[:T], self.vt_local
 
-    # rows sorted by global expert id (unpadded) -> rank-contiguous send buffer
-    def pack(self, x, topk_idx):
-        T = x.shape[0]
-        _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, self.H, self.E,
-                  self.k, self.zero_prec.data_ptr(), self.send_layout.data_ptr(), (T + 63) // 64,
-                  T * self.k, self.send_pos.data_ptr(), self.send_buf.data_ptr(), None, None,
-                  self.flag.data_ptr(), _lib.stream_ptr())
-        return self.send_buf, self.send_pos[:T]
+    # rows sorted by global expert id (unpadded) -> rank-contiguous byte segments
+    def pack(self, x, topk_idx, fp4_rows, send_counts):
+        """-> (send bytes, send positions [T, k], bytes per row for each destination)."""
+        T, H, R = x.shape[0], self.H, self.R
+        units = np.array([H // 2 + H // 16 if f else 2 * H for f in fp4_rows], np.int64)
+        counts = np.asarray(send_counts, np.int64)
+        row0 = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int32)
+        byte0 = np.concatenate([[0], np.cumsum(counts * units)[:-1]]).astype(np.int64)
+        fmt = np.array(fp4_rows, np.uint8)
+        _lib.call("realb_ep_pack", x.data_ptr(), self.topk_idx.data_ptr(), T, H, self.E, self.k,
+                  self.send_layout.data_ptr(), (T + 63) // 64, R, fmt.ctypes.data, row0.ctypes.data,
+                  byte0.ctypes.data, self.send_pos.data_ptr(), self.send_buf.data_ptr(), self.flag.data_ptr(),
+                  _lib.stream_ptr())
+        return self.send_buf, self.send_pos[:T], units
 
-    def quantize_local_weights_async(self):
+    def quantize_local_weights_async(self, timer=None):
         ws = self._fp4_ws()
         main = torch.cuda.current_stream()
         self.side.wait_stream(main)
         with torch.cuda.stream(self.side):
+            if timer is not None:
+                timer.mark("k3_start", self.side)
             sp = _lib.stream_ptr(self.side)
             El, H, I = self.El, self.H, self.I
             _lib.call("realb_quantize_nvfp4", self.local.w_gu.data_ptr(), _lib.DT_BF16, El * 2 * I, H,
@@ -163,12 +174,14 @@ class CudaEPOps:
             _lib.call("realb_quantize_nvfp4", self.local.w_d.data_ptr(), _lib.DT_BF16, El * H, I,
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), _lib.SF_MMA128x4,
                       self.flag.data_ptr(), self.quant_max_ctas, sp)
+            if timer is not None:
+                timer.mark("k3_end", self.side)
 
     def recv_buffer(self):
         return self.recv_buf
 
     # regroup received rows + local expert MLPs
-    def expert_compute(self, recv_buf, cnt: np.ndarray, w4a4: bool):
+    def expert_compute(self, recv_buf, cnt: np.ndarray, w4a4: bool, packed_fp4: bool = False):
         El, H, I = self.El, self.H, self.I
         n = int(cnt.sum())
         sp = _lib.stream_ptr()
@@ -179,10 +192,14 @@ class CudaEPOps:
                   self.local_layout.data_ptr(), self.base.data_ptr(), self.row_expert.data_ptr(),
                   self.row_pos.data_ptr(), sp)
         ws = self._fp4_ws() if w4a4 else None
-        _lib.call("realb_gather_rows", recv_buf.data_ptr(), self.row_expert.data_ptr(), self.row_pos.data_ptr(),
-                  n, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(),
-                  _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
-                  self.flag.data_ptr(), sp)
+        if packed_fp4:  # rows arrived as NVFP4 (sender-side K4): byte movement only
+            _lib.call("realb_gather_rows_nvfp4_packed", recv_buf.data_ptr(), self.row_pos.data_ptr(), n, H,
+                      ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(), sp)
+        else:
+            _lib.call("realb_gather_rows", recv_buf.data_ptr(), self.row_expert.data_ptr(), self.row_pos.data_ptr(),
+                      n, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(),
+                      _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
+                      self.flag.data_ptr(), sp)
         lay = self.local_layout.data_ptr()
         if not w4a4:
             _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.local.w_gu.data_ptr(),
@@ -206,6 +223,31 @@ class CudaEPOps:
     def ret_buffer(self):
         return self.ret_buf
 
+    def time_gate_up(self, reps: int = 5):
+        """(median ms, algorithmic flops, is_fp4) of the local gate_up grouped GEMM
+        over the rows of the last forward (valid rows only, padding excluded)."""
+        El, H, I = self.El, self.H, self.I
+        n = int(self.cnt_host.numpy().sum())
+        w4a4 = bool(self.prec_local[0].item() == _lib.PREC_W4A4)
+        lay, sp = self.local_layout.data_ptr(), _lib.stream_ptr()
+        ts = []
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            if w4a4:
+                ws = self._fp4_ws()
+                _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
+                          ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, El,
+                          lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
+            else:
+                _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.local.w_gu.data_ptr(),
+                          self.rows_cap, 2 * I, H, El, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                          self.h_bf16.data_ptr(), 0, sp)
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e))
+        return float(sorted(ts)[len(ts) // 2]), 2.0 * n * (2 * I) * H, w4a4
+
     def combine(self, ret_buf, send_pos, topk_w):
         T = send_pos.shape[0]
         y = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.dev)
@@ -216,34 +258,76 @@ class CudaEPOps:
 
 # ----------------------------------------------------------------------------- the EP layer
 class EPMoELayer:
-    """One EP rank of a ReaLB MoE layer (host orchestration, backend-agnostic)."""
+    """One EP rank of a ReaLB MoE layer (host orchestration, backend-agnostic).
 
-    def __init__(self, shape: MoEShape, comm: EPComm, ops):
+    ``fp4_dispatch``: rows bound for W4A4 ranks travel as packed NVFP4
+    (SURVEY.md §8f-1). ``timer`` (optional) gets ``mark(phase)`` calls at the
+    phase boundaries of engine.py's RankPhases (schedule / transform /
+    dispatch / compute / combine)."""
+
+    def __init__(self, shape: MoEShape, comm: EPComm, ops, fp4_dispatch: bool = False):
         if shape.num_experts % comm.world:
             raise ValueError("experts must divide evenly over the EP ranks")
         self.shape, self.comm, self.ops = shape, comm, ops
         self.R, self.rank = comm.world, comm.rank
         self.El = shape.num_experts // self.R
         self.cluster = ClusterConfig(self.R, 1, self.El, 1, shape.modality_isolated)
+        self.fp4_dispatch = fp4_dispatch
 
-    def forward(self, x, mod, strategy: str = "realb", params: RealbParams | None = None):
+    def forward(self, x, mod, strategy: str = "realb", params: RealbParams | None = None, timer=None):
         R, r, El, E = self.R, self.rank, self.El, self.shape.num_experts
+        mark = timer.mark if timer is not None else (lambda *a, **k: None)
+        mark("start")
         topk_idx, topk_w, vt_local = self.ops.route(x, mod)
         vt_all = self.comm.all_gather_counts(vt_local)                      # C1 (host sync)
         plan = plan_for(strategy, rank_loads_from_counts(vt_all.sum(0), self.cluster), self.cluster,
                         params or RealbParams())                             # P1
         w4a4 = plan.per_rank_precision[r] is Precision.W4A4
+        fp4_rows = [self.fp4_dispatch and p is Precision.W4A4 for p in plan.per_rank_precision]
         send_counts = vt_all[r].reshape(R, El, 2).sum(axis=(1, 2))
         cnt = vt_all[:, r * El:(r + 1) * El, :].sum(axis=2)                 # [R, El]
         recv_counts = cnt.sum(axis=1)
-        send_buf, send_pos = self.ops.pack(x, topk_idx)
+        mark("schedule")
         if w4a4:
-            self.ops.quantize_local_weights_async()                          # K3 under C2
-        recv_buf = self.comm.all_to_all_rows(self.ops.recv_buffer(), send_buf, recv_counts, send_counts)
-        back = self.ops.expert_compute(recv_buf, cnt, w4a4)
+            self.ops.quantize_local_weights_async(timer)                     # K3 under C2
+        send_buf, send_pos, units = self.ops.pack(x, topk_idx, fp4_rows, send_counts)
+        recv_buf = self.comm.all_to_all_rows(self.ops.recv_buffer(), send_buf, recv_counts * units[r],
+                                             send_counts * units)            # C2
+        mark("dispatch")
+        back = self.ops.expert_compute(recv_buf, cnt, w4a4, fp4_rows[r])
+        mark("compute")
         ret = self.comm.all_to_all_rows(self.ops.ret_buffer(), back, send_counts, recv_counts)  # C3
         y = self.ops.combine(ret, send_pos, topk_w)
+        mark("combine")
         return y, plan, vt_all
+
+
+class CudaPhaseTimer:
+    """CUDA events at the EP layer's phase boundaries, on the main stream (and the
+    side stream for K3) -> RankPhases in ns (engine.py:55-76)."""
+
+    PHASES = ("start", "schedule", "dispatch", "compute", "combine")
+
+    def __init__(self):
+        self.ev = {}
+
+    def mark(self, name, stream=None):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        self.ev[name] = e
+
+    def phases(self):
+        from .moe import RankPhases
+
+        self.ev["combine"].synchronize()
+        ms = lambda a, b: self.ev[a].elapsed_time(self.ev[b]) if a in self.ev and b in self.ev else 0.0
+        ns = lambda v: int(round(v * 1e6))
+        return RankPhases(ns(ms("start", "schedule")), ns(ms("k3_start", "k3_end")),
+                          ns(ms("schedule", "dispatch")), ns(ms("dispatch", "compute")),
+                          ns(ms("compute", "combine")))
+
+    def total_ns(self):
+        return int(round(self.ev["start"].elapsed_time(self.ev["combine"]) * 1e6))
 
 
 def split_weights(shape: MoEShape, router, gate_up_hf, down_hf, rank: int, world: int, bias=None,
@@ -259,9 +343,14 @@ def split_weights(shape: MoEShape, router, gate_up_hf, down_hf, rank: int, world
 
 # ----------------------------------------------------------------------------- bench (N > 1)
 def run_bench(args):
-    """bench.py under torchrun: one rank per GPU, NCCL, weak scaling (tokens/GPU fixed)."""
+    """bench.py under torchrun: one rank per GPU, NCCL, weak scaling (tokens/GPU
+    fixed). Prints bench.py's JSON line on rank 0: value = all ranks' tokens /
+    max-over-ranks device time; speedup vs the all-BF16 EP run of the same
+    kernels; e2e with host buffers; per-phase RankPhases of every rank; the
+    critical rank's gate_up GEMM against its precision's peak."""
     import json
 
+    from .clocks import FP4_TFLOPS_MEASURED, ClockSampler, measured_peaks
     from .moe import SHAPES
     from .workload import WorkloadSpec, make_batch, make_experts
 
@@ -287,41 +376,103 @@ def run_bench(args):
     del gu, dn
     comm = EPComm(staged=staged)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
-    layer = EPMoELayer(shape, comm, ops)
+    fp4_dispatch = not getattr(args, "bf16_dispatch", False)
+    layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
+    dev_t = "cpu" if staged else "cuda"
 
-    def timed(strategy):
-        for _ in range(args.warmup):
-            layer.forward(x, mod, strategy)
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device=dev_t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(strategy, steps, warmup, e2e=False):
+        """ms per step (max over ranks). e2e: every step uploads x/modality from
+        pinned host memory and downloads y, inside the timed region."""
+        xh, mh = x.cpu().pin_memory(), mod.cpu().pin_memory()
+        yh = torch.empty(T, shape.hidden, dtype=torch.bfloat16).pin_memory()
+        xd, md = torch.empty_like(x), torch.empty_like(mod)
+
+        def step():
+            if e2e:
+                xd.copy_(xh, non_blocking=True)
+                md.copy_(mh, non_blocking=True)
+                y, _, _ = layer.forward(xd, md, strategy)
+                yh.copy_(y, non_blocking=True)
+            else:
+                layer.forward(x, mod, strategy)
+
+        for _ in range(warmup):
+            step()
         torch.cuda.synchronize()
         dist.barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        for _ in range(args.steps):
-            layer.forward(x, mod, strategy)
+        for _ in range(steps):
+            step()
         e.record()
         torch.cuda.synchronize()
         dist.barrier()
-        t = torch.tensor([s.elapsed_time(e)], device="cpu" if staged else "cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks of the device-timed region
-        return float(t.item()) / args.steps
+        return max_over_ranks(s.elapsed_time(e)) / steps
 
     _lib.launch_count = 0
-    ms = timed("realb")
+    with ClockSampler(local_rank) as clk:
+        ms = timed("realb", args.steps, args.warmup)
     launches = _lib.launch_count * args.steps // (args.steps + args.warmup)
-    ms_bf16 = timed("baseline")
-    _, plan, vt_all = layer.forward(x, mod, "realb")
+    ms_bf16 = timed("baseline", args.steps, args.warmup)
+    ms_e2e = timed("realb", args.steps, max(1, args.warmup // 2), e2e=True)
+
+    # per-rank phases (engine.py RankPhases) of one extra step of each strategy
+    phases = {}
+    for strategy in ("realb", "baseline"):
+        tm = CudaPhaseTimer()
+        _, plan_s, vt_all = layer.forward(x, mod, strategy, timer=tm)
+        ph = tm.phases()
+        row = [ph.schedule_ns, ph.transform_ns, ph.dispatch_ns, ph.compute_ns, ph.combine_ns, tm.total_ns()]
+        allrows = [None] * world
+        dist.all_gather_object(allrows, row)
+        phases[strategy] = allrows
+        if strategy == "realb":
+            plan = plan_s
+    # critical rank's gate_up GEMM (the dominant kernel) against its precision's peak
+    layer.forward(x, mod, "realb")
+    torch.cuda.synchronize()
+    g_ms, g_flops, g_fp4 = ops.time_gate_up()
+    allg = [None] * world
+    dist.all_gather_object(allg, (g_ms, g_flops, g_fp4))
     if rank == 0:
+        peaks, src = measured_peaks()
+        crit = max(range(world), key=lambda i: allg[i][0])
+        gm, gf, g4 = allg[crit]
+        peak = FP4_TFLOPS_MEASURED if g4 else float(peaks.get("bf16_tflops", 1641.1))
+        achieved = gf / (gm / 1e3) / 1e12
+        names = ("schedule_ns", "transform_ns", "dispatch_ns", "compute_ns", "combine_ns", "total_ns")
         out = {"metric": "MoE-layer prefill tokens/s and speedup vs all-BF16 EP at 1/2/4/8 B200",
                "value": world * T / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "bf16 (nvfp4 on W4A4 ranks)", "data": "synthetic",
-               "config": {"workload": f"{shape.name} MoE layer prefill, {T} tokens/GPU, EP{world}",
+               "config": {"workload": f"{shape.name} MoE layer prefill, {T} tokens/GPU, EP{world}, "
+                                      f"{args.vision_frac:.0%} vision",
                           "strategy": "realb", "ep_ranks": world, "tokens_per_gpu": T,
-                          "parallelism": f"ep{world}"},
+                          "parallelism": f"ep{world}",
+                          "dispatch_rows_to_w4a4": "nvfp4" if fp4_dispatch else "bf16",
+                          "l2": "inputs + weights per GPU exceed L2 (not flushed)"},
                "speedup_vs_bf16": ms_bf16 / ms, "ms_per_step_bf16": ms_bf16,
+               "e2e": {"value": world * T / (ms_e2e / 1e3), "unit": "tokens/s",
+                       "h2d_bytes_per_step": int(world * (x.numel() * 2 + mod.numel())),
+                       "d2h_bytes_per_step": int(world * T * shape.hidden * 2),
+                       "pipeline": "serial per step (the C1 count exchange syncs the host)"},
+               "roofline": {"kernel": f"grouped GEMM gate_up on the critical rank {crit} "
+                                      f"({'NVFP4 K6' if g4 else 'BF16 K5'})",
+                            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                            "frac": achieved / peak, "traffic": None,
+                            "peak_source": "measured cuBLASLt NVFP4 (DESIGN.md §4)" if g4
+                            else f"{src} bf16_tflops (burst)",
+                            "algorithmic_flops_per_launch": gf, "launch_ms": gm},
                "plan_w4a4_ranks": sorted(plan.accelerated_ranks),
                "rank_pairs": vt_all.sum(0).reshape(world, -1, 2).sum(axis=(1, 2)).tolist(),
+               "rank_phases_ns": {s: [dict(zip(names, r)) for r in rows] for s, rows in phases.items()},
                "gpu_launches": int(launches),
+               "clocks": clk.summary(),
                "comm": "gloo-staged on one shared GPU (validation only)" if staged else "nccl"}
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()

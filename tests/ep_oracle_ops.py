@@ -22,7 +22,9 @@ class OracleEPOps:
         vt = moe_ref.expert_counts(idx, mod.numpy(), s.num_experts)
         return idx, w, torch.from_numpy(vt.astype(np.int32))
 
-    def pack(self, x, idx):
+    def pack(self, x, idx, fp4_rows, send_counts):
+        """float rows (the oracle backend sends fp32 rows; NVFP4 rows would be
+        re-quantised to the same codes on the receiver); 1 row unit per row."""
         T, k = idx.shape
         flat = idx.reshape(-1)
         order = np.lexsort((np.arange(T * k), flat))      # by expert, then (token, slot)
@@ -30,15 +32,15 @@ class OracleEPOps:
         pos = np.empty(T * k, np.int64)
         pos[order] = np.arange(T * k)
         self.send_expert = flat[order]
-        return torch.from_numpy(send.astype(np.float32)), pos.reshape(T, k)
+        return torch.from_numpy(send.astype(np.float32)), pos.reshape(T, k), np.ones(self.R, np.int64)
 
-    def quantize_local_weights_async(self):
+    def quantize_local_weights_async(self, timer=None):
         pass
 
     def recv_buffer(self):
         return torch.empty(self.R * 100000, self.s.hidden, dtype=torch.float32)
 
-    def expert_compute(self, recv_buf, cnt, w4a4):
+    def expert_compute(self, recv_buf, cnt, w4a4, packed_fp4=False):
         I = self.s.intermediate
         rows = recv_buf[: int(cnt.sum())].numpy()
         out = np.zeros_like(rows)

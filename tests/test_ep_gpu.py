@@ -36,7 +36,7 @@ def _setup(shape_name, E, T, world, rank, device="cuda"):
     return shape, x, mod, router, gu, dn
 
 
-def _worker(rank, world, port, shape_name, E, T, strategy, outdir):
+def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir):
     import sys
     from pathlib import Path
 
@@ -53,7 +53,7 @@ def _worker(rank, world, port, shape_name, E, T, strategy, outdir):
     bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
     local = split_weights(shape, router, gu, dn, rank, world)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
-    layer = EPMoELayer(shape, EPComm(staged=True), ops)
+    layer = EPMoELayer(shape, EPComm(staged=True), ops, fp4_dispatch=fp4_dispatch)
     y, plan, vt = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
     torch.cuda.synchronize()
     np.savez(os.path.join(outdir, f"r{rank}.npz"), y=y.float().cpu().numpy(),
@@ -61,11 +61,16 @@ def _worker(rank, world, port, shape_name, E, T, strategy, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape_name,E,T,strategy", [("tiny", 8, 512, "realb"), ("kimi", 16, 384, "realb"),
-                                                     ("qwen", 16, 256, "fp4all"), ("kimi", 16, 384, "baseline")])
-def test_ep2_on_one_gpu_equals_single_gpu_layer(tmp_path, shape_name, E, T, strategy):
+@pytest.mark.parametrize("shape_name,E,T,strategy,fp4_dispatch", [
+    ("tiny", 8, 512, "realb", False), ("kimi", 16, 384, "realb", False), ("qwen", 16, 256, "fp4all", False),
+    ("kimi", 16, 384, "baseline", False),
+    # NVFP4 rows on the wire to W4A4 ranks (§8f-1): sender-side K4 gives the receiver
+    # the same codes it would compute itself, so the layer output is unchanged
+    ("kimi", 16, 384, "realb", True), ("qwen", 16, 256, "fp4all", True), ("tiny", 8, 512, "realb", True)])
+def test_ep2_on_one_gpu_equals_single_gpu_layer(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, str(tmp_path)), nprocs=world)
+    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path)),
+             nprocs=world)
     from paper_2604_19503_b200 import _lib
     from paper_2604_19503_b200.moe import MoELayer, MoEWeights
     from paper_2604_19503_b200.policy import ClusterConfig, RealbParams
