@@ -64,7 +64,7 @@ struct Fp4Args {
   uint8_t* out_codes;   // SWIGLU: E2M1 [rows][N/4]
   uint8_t* out_sf;      // SWIGLU: MMA-layout scales of the [rows][N/2] result
   uint32_t sf_lbo, sf_sbo;
-  uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies
+  uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies, 4 skip MMAs
 };
 
 __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              if (j < nmma)
+              if (j < nmma && !(args.dbg & 4u))
                 umma_nvfp4(tbase + kTmemAcc, adesc0 + soff + 2 * j, bdesc0 + soff + 2 * j, idesc,
                            tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
             tc_commit(&empty[stage]);
@@ -295,10 +295,12 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             const int col = b * 16 + i;  // 0..63
             const float g = __uint_as_float(v[col >> 5][col & 31]);
             const float u = __uint_as_float(v[2 + (col >> 5)][col & 31]);
-            h[i] = __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u));
+            h[i] = (args.dbg & 8u) ? g * u
+                                   : __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u));
           }
-          uint32_t sb;
-          cw[b] = quant_block16_bf16vals(h, sb);
+          uint32_t sb = 0;
+          if (args.dbg & 16u) cw[b] = make_uint2(__float_as_uint(h[0]), __float_as_uint(h[15]));
+          else cw[b] = quant_block16_bf16vals(h, sb);
           sfw |= sb << (8 * b);
         }
         uint4* cdst = reinterpret_cast<uint4*>(args.out_codes + r * (I / 2) + ocol / 2);

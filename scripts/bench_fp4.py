@@ -32,7 +32,7 @@ for label, N, K, epi in [("gate_up", 2816, 2048, _lib.EPI_SWIGLU), ("down", 2048
     hc = torch.empty(rows, N // 4, dtype=torch.uint8, device="cuda")
     hsf = torch.empty(rows * N // 32, dtype=torch.uint8, device="cuda")
     flops = 2.0 * counts.sum() * N * K
-    for dbg in (0, 1, 2, 3):
+    for dbg in (0, 1, 2, 3, 7, 8, 16, 24):
         os.environ["REALB_DBG_FP4"] = str(dbg)
         f = lambda: _lib.call("realb_grouped_gemm_nvfp4", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(),
                               rows, N, K, E, lt.data_ptr(), epi, o.data_ptr(), hc.data_ptr(), hsf.data_ptr(), 0, _lib.stream_ptr())

@@ -45,7 +45,16 @@ for label, E, N, K, per in [("kimi_gate_up_ep8hot", 8, 2816, 2048, 13000), ("kim
         tg = timeit(g)
     except Exception as e:
         tg = repr(e)[:100]
-    out[label] = dict(rows=rows, ms=t, tflops=flops / t / 1e9, ms_swiglu=t_swiglu, ms_no_epi=dbgt[1],
+    cl = {}
+    for c in ("1", "2"):
+        os.environ["REALB_GEMM_CLUSTER"] = c
+        cl[c] = (timeit(f), timeit(fs))
+    del os.environ["REALB_GEMM_CLUSTER"]
+    valid = 2.0 * counts.sum() * N * K
+    out[label] = dict(rows=rows, ms=t, tflops=flops / t / 1e9, valid_tflops=valid / t / 1e9,
+                      cluster_ms={c: v for c, v in cl.items()},
+                      cluster_valid_tflops={c: (valid / v[0] / 1e9, valid / v[1] / 1e9) for c, v in cl.items()},
+                      ms_swiglu=t_swiglu, ms_no_epi=dbgt[1],
                       ms_no_mma=dbgt[4], ms_tma_only=dbgt[5], torch_ms=tg,
                       torch_tflops=(flops / tg / 1e9) if isinstance(tg, float) else None)
     print(label, out[label], flush=True)
