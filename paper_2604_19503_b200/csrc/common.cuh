@@ -364,6 +364,25 @@ __device__ __forceinline__ void umma_nvfp4(uint32_t tmem_d, uint64_t adesc, uint
       "[%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
 }
+// pair (cta_group::2) block-scaled MMA, M = 256: each CTA contributes its 128 A
+// rows, half of the N rows of W, and its own TMEM scale columns (its A scales and
+// the full W scales); issued by the pair leader
+__device__ __forceinline__ void umma_nvfp4_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t tmem_sfa, uint32_t tmem_sfb,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4nvf4.block_scale.scale_vec::4X "
+      "[%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
+}
+// pair form of the scale copy: each CTA of the pair copies ITS smem block at this
+// offset into ITS TMEM (issued once, by the pair leader)
+__device__ __forceinline__ void utccp_32x128b_warpx4_2sm(uint32_t tmem_dst, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(tmem_dst), "l"(sdesc)
+               : "memory");
+}
 // smem -> TMEM copy of one 32-row x 128-bit block, broadcast to the 4 lane
 // quadrants (the "4x1 duplicated" scale-factor placement).
 __device__ __forceinline__ void utccp_32x128b_warpx4(uint32_t tmem_dst, uint64_t sdesc) {

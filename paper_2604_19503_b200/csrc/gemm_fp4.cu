@@ -4,11 +4,11 @@
 //
 // Persistent, warp-specialised, one CTA per SM, 384 threads:
 //   warp 0     TMA producer: A 128x256 and W 256x256 E2M1 tiles (128-B rows,
-//              SWIZZLE_128B) + their scale-factor atoms (cp.async.bulk; the
-//              quantisers write scales directly in the 128x4-atom layout, so a
-//              stage's scales are contiguous 2 KB runs)
+//              SWIZZLE_128B) + their scale-factor atoms (TMA over the scale
+//              bytes viewed as 256-byte rows; the quantisers write scales directly
+//              in the 128x4-atom layout, so a stage's scales are contiguous 2 KB runs)
 //   warp 1     MMA issuer: tcgen05.cp (smem -> TMEM, 32x128b.warpx4) of the
-//              stage's scale atoms, then 4 x tcgen05.mma (M=128, N=256, K=64)
+//              stage's scale atoms, then 4 x tcgen05.mma (K=64 each)
 //   warp 2     TMEM allocator (512 columns: 256 accumulator, the m-tile's A
 //              scales for the whole K (K/16 columns, RESIDENT across the unit's
 //              n-tiles) and 2 x 32 columns of streamed W scales)
@@ -20,6 +20,14 @@
 //              to the MMA warp at once, then run SwiGLU (+ NVFP4 re-quantisation
 //              of the bf16 result with the reference block rule, K4 fused) or the
 //              bf16 store from registers while the next tile's mainloop runs.
+//
+// CL = 2 (large experts): a 2-CTA cluster is one tcgen05 CTA pair, M = 256
+// (cta_group::2). CTA r stages ITS 128 A rows, HALF of the W tile (rows
+// 128r..128r+127 of the 256), its A scales and the full W scales; the leader
+// issues the pair's scale copies (each CTA's smem -> its own TMEM) and MMAs.
+// Halving the W bytes each SM receives per stage (54 -> 38 KB per 512 MMA cycles)
+// lifts the TMA-feed bound the 1-CTA kernel runs into (TMA-only time was 0.67 of
+// the kernel on the EP8 hot rank's gate_up).
 // Roofline: tensor-bound at the dense FP4 rate (4x BF16 per MMA cycle).
 #include <cstdlib>
 
@@ -31,20 +39,17 @@ namespace realb {
 
 constexpr int kF4BM = 128, kF4BN = 256;
 constexpr int kF4BKB = 128;               // bytes of K per stage = 256 E2M1 values
-// STORE (bf16 out) needs 32 KB of TMA-store staging, so it runs 3 stages
-template <int EPI>
-struct F4Cfg {
-  static constexpr int STAGES = EPI == REALB_EPI_STORE ? 3 : 4;
-};
 constexpr int kF4Threads = 384;
+constexpr int kSfBoxRows = 8;             // scale TMA box: 8 x 256 B = 2 KB = 4 atoms
 
-template <int EPI>
+template <int EPI, int CL>
 struct SmemFp4 {
-  static constexpr int STAGES = F4Cfg<EPI>::STAGES;
-  static constexpr int A_BYTES = kF4BM * kF4BKB;    // 16 KB
-  static constexpr int B_BYTES = kF4BN * kF4BKB;    // 32 KB
-  static constexpr int SFA_BYTES = 4 * 512;         // 128 rows x 16 scales
-  static constexpr int SFB_BYTES = 2 * 4 * 512;     // 256 rows x 16 scales
+  // STORE (bf16 out) needs 32 KB of TMA-store staging
+  static constexpr int STAGES = CL == 1 ? (EPI == REALB_EPI_STORE ? 3 : 4) : (EPI == REALB_EPI_STORE ? 4 : 5);
+  static constexpr int A_BYTES = kF4BM * kF4BKB;              // 16 KB
+  static constexpr int B_BYTES = (kF4BN / CL) * kF4BKB;       // 32 KB (16 KB per CTA of a pair)
+  static constexpr int SFA_BYTES = 4 * 512;                   // 128 rows x 16 scales
+  static constexpr int SFB_BYTES = 2 * 4 * 512;               // 256 rows x 16 scales (full W tile)
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
   static constexpr int EPI_OFF = STAGES * STAGE;    // 8 warps x 2 x 2 KB (STORE only)
   static constexpr int EPI_BYTES = EPI == REALB_EPI_STORE ? 8 * 4096 : 0;
@@ -76,12 +81,14 @@ __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32
   return d;
 }
 
-template <int EPI>
+template <int EPI, int CL>
 __global__ void __launch_bounds__(kF4Threads, 1)
     grouped_gemm_fp4_kernel(const __grid_constant__ CUtensorMap tmA,
                             const __grid_constant__ CUtensorMap tmB,
+                            const __grid_constant__ CUtensorMap tmSfa,
+                            const __grid_constant__ CUtensorMap tmSfb,
                             const __grid_constant__ CUtensorMap tmOut, const Fp4Args args) {
-  using S = SmemFp4<EPI>;
+  using S = SmemFp4<EPI, CL>;
   constexpr int kF4Stages = S::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -96,36 +103,60 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_tile + kF4Ring);
 
   const int warp = warp_id(), lane = lane_id();
+  const uint32_t crank = CL == 2 ? cluster_ctarank() : 0u;
   const int N = args.N, K = args.K;
   const GroupedSched sched = GroupedSched::make(args.layout, args.E, REALB_PREC_W4A4, N, kF4BN);
   const int n_tiles = N / kF4BN;
   const int nchunks = (n_tiles + kNPerUnit - 1) / kNPerUnit;
-  const int total_units = sched.G > 0 ? sched.prefix[sched.G] * nchunks : 0;
+  const int m_units = sched.G > 0 ? (CL == 2 ? sched.pprefix[sched.G] : sched.prefix[sched.G]) : 0;
+  const int total_units = m_units * nchunks;
   const uint32_t sfa_cols = (uint32_t)(K / 16);  // resident A scales: 4 columns per K=64
   const int kbytes = K / 2;
   const int nkb = (kbytes + kF4BKB - 1) / kF4BKB;
   const int atoms_per_row_tile = K / 64;  // 4-scale atoms per 128-row tile
+  constexpr uint16_t kBoth = 0x3;
+  // consumers of a unit slot: 1-CTA: MMA + 8 epilogue warps; pair: leader MMA + 8
+  // leader epilogue warps + peer producer + 8 peer epilogue warps
+  constexpr uint32_t kSlotConsumers = CL == 2 ? 18 : 9;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmSfa);
+    tma_prefetch_desc(&tmSfb);
     for (int s = 0; s < kF4Stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    mbar_init(tempty, 8 * CL);
     for (int i = 0; i < kF4Ring; ++i) {
       mbar_init(&slot_full[i], 1);
-      mbar_init(&slot_empty[i], 9);  // MMA thread + 8 epilogue warps
+      mbar_init(&slot_empty[i], kSlotConsumers);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CL == 2) tmem_alloc_2sm<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // peer barriers / TMEM ready before any remote op
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  // m-unit index -> this CTA's 128-row m-tile (dummy: the pair's expert has an odd
+  // m-tile count and this rank-1 CTA has no rows of its own in this unit)
+  auto mtile_of = [&](int mu, int rank, bool& dummy) -> TileCoord {
+    if constexpr (CL == 2) return sched.coord_pair(mu * n_tiles, rank, dummy);
+    dummy = false;
+    return sched.coord(mu * n_tiles);
+  };
+  auto arrive_leader = [&](uint64_t* bar) {
+    if constexpr (CL == 2) mbar_arrive_cluster(mapa_shared(bar, 0));
+    else mbar_arrive(bar);
+  };
 
   // Producer and MMA roles run on their WHOLE warp: every lane computes the same
   // (hence provably warp-uniform) values and one elected lane issues the TMA /
@@ -135,59 +166,91 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   if (warp == 0) {  // ---------------- producer + dynamic unit fetch
     const bool leader = elect_one();
     int* ctr = GroupedSched::counters(args.layout, REALB_PREC_W4A4);
+    const uint32_t full0 = CL == 2 ? mapa_shared(&full[0], 0) : smem_u32(&full[0]);
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0;; ++i) {
       const int slot = i % kF4Ring;
-      mbar_wait(&slot_empty[slot], ((i / kF4Ring) & 1) ^ 1);
       int u = 0;
-      if (leader) {
-        u = atomicAdd(ctr, 1);
-        if (u >= total_units) u = -1;
-        slot_tile[slot] = u;
-        mbar_arrive(&slot_full[slot]);
+      if (crank == 0) {  // the (pair) leader fetches and publishes the unit
+        mbar_wait(&slot_empty[slot], ((i / kF4Ring) & 1) ^ 1);
+        if (leader) {
+          u = atomicAdd(ctr, 1);
+          if (u >= total_units) u = -1;
+          slot_tile[slot] = u;
+          if constexpr (CL == 2) {
+            st_cluster_u32(mapa_shared(&slot_tile[slot], 1), (uint32_t)u);
+            mbar_arrive_cluster(mapa_shared(&slot_full[slot], 1));
+          }
+          mbar_arrive(&slot_full[slot]);
+        }
+        u = __shfl_sync(0xffffffffu, u, 0);
+      } else {
+        mbar_wait(&slot_full[slot], (i / kF4Ring) & 1);
+        u = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
+        __syncwarp();
+        if (leader) arrive_leader(&slot_empty[slot]);
       }
-      u = __shfl_sync(0xffffffffu, u, 0);
       if (u < 0) break;
-      const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+      const int mu = u / nchunks, nt0 = (u - mu * nchunks) * kNPerUnit;
       const int nt1 = min(n_tiles, nt0 + kNPerUnit);
-      const TileCoord c = sched.coord(mt * n_tiles);
+      bool dummy = false, dummy1 = false;
+      const TileCoord c = mtile_of(mu, (int)crank, dummy);
+      if constexpr (CL == 2) {
+        if (crank == 0) { bool d1; (void)mtile_of(mu, 1, d1); dummy1 = d1; }
+      }
       const int a_row = __shfl_sync(0xffffffffu, c.a_row, 0);
       const int group = __shfl_sync(0xffffffffu, c.group, 0);
+      dummy = __shfl_sync(0xffffffffu, (int)dummy, 0) != 0;
+      dummy1 = __shfl_sync(0xffffffffu, (int)dummy1, 0) != 0;
+      const int sfa_row = (a_row >> 7) * atoms_per_row_tile * 2;  // 256-byte rows of the A-scale view
       for (int nt = nt0; nt < nt1; ++nt) {
         const int brow = group * N + nt * kF4BN;
+        const int sfb_row = (brow >> 7) * atoms_per_row_tile * 2;
         const bool load_a_sf = nt == nt0;
         for (int kb = 0; kb < nkb; ++kb) {
-          const int kval = min(kF4BKB, kbytes - kb * kF4BKB);  // bytes of K in this stage
-          const uint32_t sfbytes = (uint32_t)(kval / 32) * 512;
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) {
             uint8_t* sa = smem + stage * S::STAGE;
             uint8_t* sb = sa + S::A_BYTES;
             uint8_t* ssfa = sb + S::B_BYTES;
             uint8_t* ssfb = ssfa + S::SFA_BYTES;
-            mbar_arrive_expect_tx(&full[stage],
-                                  S::A_BYTES + S::B_BYTES + (load_a_sf ? 3 : 2) * sfbytes);
-            tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, a_row);
-            tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
-            const int64_t atom_k = (int64_t)kb * 4;
-            if (load_a_sf)
-              bulk_load(ssfa, args.a_sf + ((int64_t)(a_row >> 7) * atoms_per_row_tile + atom_k) * 512,
-                        sfbytes, &full[stage]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              bulk_load(ssfb + h * 2048,
-                        args.w_sf + ((int64_t)((brow >> 7) + h) * atoms_per_row_tile + atom_k) * 512,
-                        sfbytes, &full[stage]);
+            const int k_sf_row = kb * 8;  // 4 atoms of 512 B per stage = 8 rows of 256 B
+            if constexpr (CL == 2) {
+              const uint32_t fb = full0 + (uint32_t)stage * 8u;
+              if (crank == 0) {
+                const uint32_t a_cnt = 1 + (dummy1 ? 0 : 1);
+                mbar_arrive_expect_tx(&full[stage], 2 * S::B_BYTES + 2 * S::SFB_BYTES +
+                                                        a_cnt * S::A_BYTES +
+                                                        (load_a_sf ? a_cnt * S::SFA_BYTES : 0));
+              }
+              if (!dummy) {
+                tma_load_2d_2sm(sa, &tmA, fb, kb * kF4BKB, a_row);
+                if (load_a_sf) tma_load_2d_2sm(ssfa, &tmSfa, fb, 0, sfa_row + k_sf_row);
+              }
+              tma_load_2d_2sm(sb, &tmB, fb, kb * kF4BKB, brow + (int)crank * (kF4BN / 2));
+              tma_load_2d_2sm(ssfb, &tmSfb, fb, 0, sfb_row + k_sf_row);
+              tma_load_2d_2sm(ssfb + 2048, &tmSfb, fb, 0, sfb_row + atoms_per_row_tile * 2 + k_sf_row);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES + S::SFB_BYTES +
+                                                      (load_a_sf ? S::SFA_BYTES : 0));
+              // 1-CTA: the scale runs are plain bulk copies (no 2-SM signalling needed)
+              tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, a_row);
+              tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
+              if (load_a_sf) bulk_load(ssfa, args.a_sf + (int64_t)(sfa_row + k_sf_row) * 256, 2048, &full[stage]);
+              bulk_load(ssfb, args.w_sf + (int64_t)(sfb_row + k_sf_row) * 256, 2048, &full[stage]);
+              bulk_load(ssfb + 2048, args.w_sf + (int64_t)(sfb_row + atoms_per_row_tile * 2 + k_sf_row) * 256,
+                        2048, &full[stage]);
+            }
           }
           __syncwarp();
           if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer
+  } else if (warp == 1 && crank == 0) {  // ---------------- MMA issuer (pair leader)
     const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_nvfp4(kF4BM, kF4BN);
+    constexpr uint32_t idesc = idesc_nvfp4(kF4BM * CL, kF4BN);
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t tsfa = tbase + kTmemSfa;
     const uint32_t tsfb0 = tsfa + sfa_cols;
@@ -197,6 +260,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
     const uint64_t sfadesc0 = sf_desc(s0 + S::A_BYTES + S::B_BYTES, args.sf_lbo, args.sf_sbo);
     const uint64_t sfbdesc0 = sf_desc(s0 + S::A_BYTES + S::B_BYTES + S::SFA_BYTES, args.sf_lbo, args.sf_sbo);
     const bool copy_sf = !(args.dbg & 2u);
+    auto utccp = [&](uint32_t t, uint64_t d) {
+      if constexpr (CL == 2) utccp_32x128b_warpx4_2sm(t, d);
+      else utccp_32x128b_warpx4(t, d);
+    };
     int stage = 0;
     uint32_t phase = 0, sfsel = 0;
     int tile_it = 0;  // accumulator use count (one per n-tile)
@@ -207,10 +274,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       __syncwarp();
       if (leader) mbar_arrive(&slot_empty[slot]);
       if (u < 0) break;
-      const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+      const int mu = u / nchunks, nt0 = (u - mu * nchunks) * kNPerUnit;
       const int nt1 = min(n_tiles, nt0 + kNPerUnit);
       for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
-        // previous n-tile drained by the epilogue => every earlier MMA completed,
+        // previous n-tile drained by the epilogue(s) => every earlier MMA completed,
         // so the resident A scales may be rewritten at the start of a new unit
         mbar_wait(tempty, (tile_it & 1) ^ 1);
         tc_fence_after();
@@ -225,27 +292,36 @@ __global__ void __launch_bounds__(kF4Threads, 1)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               if (j < nmma && copy_sf) {
-                if (load_a_sf) utccp_32x128b_warpx4(tsfa + (kb * 4 + j) * 4, sfadesc0 + soff + 32 * j);
-                utccp_32x128b_warpx4(tsfb + 8 * j, sfbdesc0 + soff + 32 * j);
-                utccp_32x128b_warpx4(tsfb + 8 * j + 4, sfbdesc0 + soff + 128 + 32 * j);
+                if (load_a_sf) utccp(tsfa + (kb * 4 + j) * 4, sfadesc0 + soff + 32 * j);
+                utccp(tsfb + 8 * j, sfbdesc0 + soff + 32 * j);
+                utccp(tsfb + 8 * j + 4, sfbdesc0 + soff + 128 + 32 * j);
               }
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              if (j < nmma && !(args.dbg & 4u))
-                umma_nvfp4(tbase + kTmemAcc, adesc0 + soff + 2 * j, bdesc0 + soff + 2 * j, idesc,
-                           tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
-            tc_commit(&empty[stage]);
+              if (j < nmma && !(args.dbg & 4u)) {
+                if constexpr (CL == 2)
+                  umma_nvfp4_2sm(tbase + kTmemAcc, adesc0 + soff + 2 * j, bdesc0 + soff + 2 * j, idesc,
+                                 tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
+                else
+                  umma_nvfp4(tbase + kTmemAcc, adesc0 + soff + 2 * j, bdesc0 + soff + 2 * j, idesc,
+                             tsfa + (kb * 4 + j) * 4, tsfb + 8 * j, (kb | j) != 0);
+              }
+            if constexpr (CL == 2) tc_commit_2sm_mc(&empty[stage], kBoth);
+            else tc_commit(&empty[stage]);
           }
           __syncwarp();
           sfsel ^= 1;
           if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
         }
-        if (leader) tc_commit(tfull);
+        if (leader) {
+          if constexpr (CL == 2) tc_commit_2sm_mc(tfull, kBoth);
+          else tc_commit(tfull);
+        }
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue (8 warps)
+  } else if (warp >= 4) {  // ---------------- epilogue (8 warps per CTA)
     const int q = warp & 3, half = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
     int tile_it = 0;
@@ -254,11 +330,12 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
       const int u = slot_tile[slot];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&slot_empty[slot]);
+      if (lane == 0) arrive_leader(&slot_empty[slot]);
       if (u < 0) break;
-      const int mt = u / nchunks, nt0 = (u - mt * nchunks) * kNPerUnit;
+      const int mu = u / nchunks, nt0 = (u - mu * nchunks) * kNPerUnit;
       const int nt1 = min(n_tiles, nt0 + kNPerUnit);
-      const TileCoord cm = sched.coord(mt * n_tiles);
+      bool dummy;
+      const TileCoord cm = mtile_of(mu, (int)crank, dummy);
       for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
       TileCoord c = cm;
       c.n0 = nt * kF4BN;
@@ -278,8 +355,8 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);  // accumulator free: next mainloop may start
-      if (args.dbg & 1u) continue;
+      if (lane == 0) arrive_leader(tempty);  // accumulator free: next mainloop may start
+      if ((args.dbg & 1u) || dummy) continue;
       const int64_t r = (int64_t)c.a_row + row_in_tile;
       if constexpr (EPI == REALB_EPI_SWIGLU) {
         // outputs [n0/2 + half*64, +64): h = bf16(silu(g) * u), then NVFP4
@@ -295,12 +372,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             const int col = b * 16 + i;  // 0..63
             const float g = __uint_as_float(v[col >> 5][col & 31]);
             const float u = __uint_as_float(v[2 + (col >> 5)][col & 31]);
-            h[i] = (args.dbg & 8u) ? g * u
-                                   : __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u));
+            h[i] = __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u));
           }
-          uint32_t sb = 0;
-          if (args.dbg & 16u) cw[b] = make_uint2(__float_as_uint(h[0]), __float_as_uint(h[15]));
-          else cw[b] = quant_block16_bf16vals(h, sb);
+          uint32_t sb;
+          cw[b] = quant_block16_bf16vals(h, sb);
           sfw |= sb << (8 * b);
         }
         uint4* cdst = reinterpret_cast<uint4*>(args.out_codes + r * (I / 2) + ocol / 2);
@@ -340,8 +415,12 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // no peer may still load / arrive / read our smem
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<512>(tmem_base);
+  if (warp == 2) {
+    if constexpr (CL == 2) tmem_dealloc_2sm<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
+  }
   if (threadIdx.x == 0) GroupedSched::finish(args.layout, REALB_PREC_W4A4);
 }
 
@@ -350,16 +429,27 @@ static uint32_t env_u32(const char* name, uint32_t dflt) {
   return s ? (uint32_t)strtoul(s, nullptr, 0) : dflt;
 }
 
-template <int EPI>
+// scale bytes of `rows` x K/16 viewed as [bytes/256][256] for the TMA loads
+static int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int K) {
+  const uint64_t bytes = (uint64_t)rows * (uint64_t)(K / 16);
+  return make_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, sf, 256, bytes / 256, 256, 256, kSfBoxRows,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+template <int EPI, int CL>
 static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, const uint8_t* w_sf,
                       int64_t rows_cap, int N, int K, int E, const int32_t* layout, void* out,
                       uint8_t* out_codes, uint8_t* out_sf, int max_ctas, cudaStream_t st) {
-  CUtensorMap ta, tb, to;
+  CUtensorMap ta, tb, tsa, tsb, to;
   int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, a, (uint64_t)K / 2, rows_cap,
                         (uint64_t)K / 2, kF4BKB, kF4BM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, (uint64_t)K / 2, (uint64_t)E * N,
-                    (uint64_t)K / 2, kF4BKB, kF4BN, CU_TENSOR_MAP_SWIZZLE_128B);
+                    (uint64_t)K / 2, kF4BKB, kF4BN / CL, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_sf_map(&tsa, a_sf, rows_cap, K);
+  if (rc) return rc;
+  rc = make_sf_map(&tsb, w_sf, (int64_t)E * N, K);
   if (rc) return rc;
   if (EPI == REALB_EPI_STORE) {
     rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, rows_cap, (uint64_t)N * 2, 32, 32,
@@ -381,13 +471,29 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   args.sf_lbo = env_u32("REALB_DBG_SF_LBO", 128);
   args.sf_sbo = env_u32("REALB_DBG_SF_SBO", 128);
   args.dbg = env_u32("REALB_DBG_FP4", 0);
-  auto kern = grouped_gemm_fp4_kernel<EPI>;
-  const int smem = SmemFp4<EPI>::TOTAL;
+  auto kern = grouped_gemm_fp4_kernel<EPI, CL>;
+  const int smem = SmemFp4<EPI, CL>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_nvfp4: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, kF4Threads, smem, st>>>(ta, tb, to, args);
+  grid = grid / CL * CL;
+  if (grid < CL) grid = CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kF4Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = cuda_status(cudaLaunchKernelEx(&cfg, kern, ta, tb, tsa, tsb, to, args),
+                   "realb_grouped_gemm_nvfp4 launch");
+  if (rc) return rc;
   return check_launch("realb_grouped_gemm_nvfp4");
 }
 
@@ -412,18 +518,28 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  // 1-CTA tiles by default: the 2-CTA pair form (same results) measured slower on the
+  // EP8 hot rank (scripts/bench_fp4.py, interleaved: gate_up 0.44 vs 0.37 ms) — its
+  // TMA-only pipeline time did not drop with the halved W bytes, so the 1-CTA kernel
+  // is not feed-bound. REALB_GEMM_CLUSTER=2 selects the pair kernel.
+  const char* cl_env = getenv("REALB_GEMM_CLUSTER");
+  const bool pair = cl_env && cl_env[0] == '2';
   if (epilogue == REALB_EPI_STORE) {
     if (!d_out) { set_error("realb_grouped_gemm_nvfp4: STORE needs d_out"); return REALB_EINVAL; }
-    return launch_fp4<REALB_EPI_STORE>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
-                                       d_layout, d_out, nullptr, nullptr, max_ctas, st);
+    return pair ? launch_fp4<REALB_EPI_STORE, 2>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
+                                                 d_layout, d_out, nullptr, nullptr, max_ctas, st)
+                : launch_fp4<REALB_EPI_STORE, 1>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
+                                                 d_layout, d_out, nullptr, nullptr, max_ctas, st);
   }
   if (epilogue == REALB_EPI_SWIGLU) {
     if (!d_out_codes || !d_out_sf || (N / 2) % 64) {
       set_error("realb_grouped_gemm_nvfp4: SWIGLU needs d_out_codes/d_out_sf and (N/2) %% 64 == 0");
       return REALB_EINVAL;
     }
-    return launch_fp4<REALB_EPI_SWIGLU>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
-                                        d_layout, nullptr, d_out_codes, d_out_sf, max_ctas, st);
+    return pair ? launch_fp4<REALB_EPI_SWIGLU, 2>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
+                                                  d_layout, nullptr, d_out_codes, d_out_sf, max_ctas, st)
+                : launch_fp4<REALB_EPI_SWIGLU, 1>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
+                                                  d_layout, nullptr, d_out_codes, d_out_sf, max_ctas, st);
   }
   set_error("realb_grouped_gemm_nvfp4: unknown epilogue %d", epilogue);
   return REALB_EINVAL;

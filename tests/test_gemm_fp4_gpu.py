@@ -39,14 +39,23 @@ def make_problem(E, N, K, counts, seed, a_scale=1.0):
     return lay, rows, A, W, ac, asf, wc, wsf
 
 
+@pytest.fixture(params=["1", "2"], ids=["cta1", "pair"])
+def cluster(request, monkeypatch):
+    """Both kernel forms: one CTA per tile, and 2-CTA pairs (cta_group::2, M = 256,
+    odd m-tile counts give the rank-1 CTA a dummy slot)."""
+    monkeypatch.setenv("REALB_GEMM_CLUSTER", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("E,N,K,counts", [
     (1, 256, 256, [128]),
+    (3, 512, 1408, [1500, 700, 2100]),       # pair units with odd and even m-tile counts
     (1, 256, 64, [100]),
     (3, 512, 2048, [300, 0, 700]),
     (4, 2048, 1408, [513, 129, 1, 260]),     # Kimi down: K tail (1408 = 5.5 x 256)
     (4, 2816, 2048, [513, 129, 1, 260]),     # Kimi gate_up
 ])
-def test_fp4_store_vs_dequant_oracle(E, N, K, counts):
+def test_fp4_store_vs_dequant_oracle(E, N, K, counts, cluster):
     lay, rows, A, W, ac, asf, wc, wsf = make_problem(E, N, K, counts, seed=E + N + K)
     out = torch.full((rows, N), float("nan"), dtype=torch.bfloat16, device="cuda")
     lt = torch.from_numpy(lay).cuda()
@@ -65,8 +74,9 @@ def test_fp4_store_vs_dequant_oracle(E, N, K, counts):
         assert err < 5e-3, (e, err)  # fp32 accumulation order + bf16 output rounding
 
 
-def test_fp4_swiglu_requant_epilogue():
-    E, N, K, counts = 2, 512, 512, [200, 77]
+@pytest.mark.parametrize("counts", [[200, 77], [1100, 390]])
+def test_fp4_swiglu_requant_epilogue(counts, cluster):
+    E, N, K = 2, 512, 512
     lay, rows, A, W, ac, asf, wc, wsf = make_problem(E, N, K, counts, seed=5, a_scale=4.0)
     I = N // 2
     hc = torch.zeros(rows, I // 2, dtype=torch.uint8, device="cuda")

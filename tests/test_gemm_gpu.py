@@ -38,6 +38,13 @@ def ref_rows(A, W, lay, E, N, counts, prec_sel, prec, epi):
     return outs
 
 
+@pytest.fixture(params=["1", "2"], ids=["cta1", "pair"])
+def cluster(request, monkeypatch):
+    """Both kernel forms: one CTA per tile, and 2-CTA pairs (cta_group::2, M = 256)."""
+    monkeypatch.setenv("REALB_GEMM_CLUSTER", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("E,N,K,counts", [
     (1, 256, 64, [128]),
     (1, 256, 128, [77]),
@@ -46,7 +53,7 @@ def ref_rows(A, W, lay, E, N, counts, prec_sel, prec, epi):
     (8, 2048, 1408, [513, 129, 1, 0, 777, 256, 2048, 90]),   # Kimi down shape
 ])
 @pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_SWIGLU])
-def test_grouped_bf16(E, N, K, counts, epi):
+def test_grouped_bf16(E, N, K, counts, epi, cluster):
     torch.manual_seed(E * 31 + N + K)
     prec_sel = np.zeros(E, np.int64)
     lay, rows = host_layout(counts, prec_sel)
