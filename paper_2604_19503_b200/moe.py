@@ -60,6 +60,32 @@ SHAPES = {
 }
 
 
+def host_layout(counts, prec, nchunks: int = 1) -> tuple[np.ndarray, int]:
+    """Host construction of the int32 grouped-row layout words realb_moe_align
+    builds on the device (include/realb.h) from per-expert row counts and
+    precision codes: used to run the grouped GEMMs on an arbitrary (expert ->
+    rows) assignment, e.g. an EPLB rank's replica shares. -> (layout, rows used)."""
+    counts = np.asarray(counts, np.int64)
+    prec = np.asarray(prec, np.int64)
+    E = len(counts)
+    lay = np.zeros(int(_lib.load().realb_layout_words(E, nchunks)), np.int32)
+    padded = (counts + 127) // 128 * 128
+    row_start = np.concatenate([[0], np.cumsum(padded)[:-1]])
+    lay[8:8 + E] = row_start
+    lay[8 + E:8 + 2 * E] = counts
+    for p in (0, 1):
+        g = np.flatnonzero(prec == p)
+        base = 8 + 3 * E + p * (2 * E + 1)
+        lay[base:base + len(g)] = g
+        mt = padded[g] // 128
+        lay[base + E:base + E + len(g) + 1] = np.concatenate([[0], np.cumsum(mt)])
+        pbase = 8 + 3 * E + 2 * (2 * E + 1) + p * (E + 1)
+        lay[pbase:pbase + len(g) + 1] = np.concatenate([[0], np.cumsum((mt + 1) // 2)])
+        lay[1 + p] = len(g)
+    lay[0] = int(padded.sum())
+    return lay, int(padded.sum())
+
+
 # ----------------------------------------------------------------- timing schema
 class PipelineMode(enum.Enum):
     SEQUENTIAL = "sequential"
@@ -409,6 +435,20 @@ class MoELayer:
             _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+
+    def bf16_compute_on(self, layout_dev: torch.Tensor) -> None:
+        """The BF16 expert GEMMs (gate_up + SwiGLU, down) over an explicit layout
+        (host_layout): times an arbitrary per-expert row assignment (an EPLB
+        rank's hosted replicas) on this layer's weights; reads whatever rows the
+        activation buffers hold."""
+        E, H, I = self.E, self.H, self.I
+        sp, lay = _lib.stream_ptr(), layout_dev.data_ptr()
+        _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
+                  self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                  self.h_bf16.data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
+                  self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
+                  self.rows_out.data_ptr(), 0, sp)
 
     def check_flag(self):
         from .quant import QuantizationDomainError

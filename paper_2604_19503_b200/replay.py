@@ -35,8 +35,8 @@ from typing import Mapping
 import numpy as np
 
 from .moe import LayerTiming, PipelineMode
-from .policy import (ClusterConfig, Precision, PrecisionPlan, RankLoad, RealbParams, STRATEGIES,
-                     aggregate_rank_loads, place_experts_static, plan_for)
+from .policy import (ClusterConfig, Precision, PrecisionPlan, RankLoad, RealbParams,
+                     STRATEGIES, aggregate_rank_loads, place_experts_static, plan_for)
 
 TRACE_HEADER = "iter,layer,expert,vision_tokens,text_tokens"  # tracegen.py:30
 
@@ -193,6 +193,16 @@ def pair_loads(loads: Mapping[int, tuple[int, int]], k: int) -> dict[int, tuple[
 
 
 # ----------------------------------------------------------------------------- measured run
+@dataclass(frozen=True)
+class MigrationEvent:
+    """engine.py:89-94: one EPLB rebalance's replica moves and the stall charged."""
+
+    iteration: int
+    replicas_moved: int
+    volume_bytes: int
+    charged_ns: int
+
+
 @dataclass
 class MeasuredRun:
     """``RunResult`` (engine.py:89-115) filled from measurements."""
@@ -231,6 +241,14 @@ def text_exposure(run: MeasuredRun, trace: IterationTrace) -> float:
     return exposed / total if total else 0.0
 
 
+def _mem_delta(run: MeasuredRun, config: ClusterConfig) -> int:
+    """metrics.summarize_run's memory delta (metrics.py:105-129 via
+    costmodel.memory_overhead): it depends only on the replica count."""
+    per = config.num_layers * config.bytes_per_expert / config.num_ranks
+    E = config.total_experts
+    return round(per * (E + run.max_redundant_count)) - round(per * E)
+
+
 def write_run(run: MeasuredRun, trace: IterationTrace, out_dir, trace_sha256: str,
               ranks_iters=(0,)) -> dict:
     """layers.csv / ranks.csv / events.csv / summary.json in the reference's
@@ -262,7 +280,7 @@ def write_run(run: MeasuredRun, trace: IterationTrace, out_dir, trace_sha256: st
         "trace_sha256": trace_sha256,
         "e2e_time_ns": run.e2e_time_ns,
         "compute_only_total_ns": run.compute_only_total_ns,
-        "mem_delta_bytes": 0,
+        "mem_delta_bytes": _mem_delta(run, trace.cluster),
         "migration_bytes": run.migration_volume_bytes,
         "text_exposure": text_exposure(run, trace),
         "timing_source": run.timing_source,
@@ -330,25 +348,55 @@ class TraceReplay:
         x = make_hidden(self.shape, spec, self.unit, idx)
         return x, self.torch.from_numpy(mod).cuda(), idx
 
-    def run(self, strategies=("baseline", "fp4all", "realb"), iterations=None, check=True):
-        """-> ({strategy: MeasuredRun}, [per-layer parity checks])."""
-        from .virtual_ep import a2a_ms, layer_timing, measure_rank_compute, measure_transform, traffic_matrix
+    def run(self, strategies=("baseline", "fp4all", "realb"), iterations=None, check=True,
+            eplb_state: dict | None = None):
+        """-> ({strategy: MeasuredRun}, [per-layer parity checks]).
+
+        "eplb" / "async-eplb" run the reference's replication balancer
+        (eplb.py, balancers.py:143-199) on the replayed loads: at an iteration
+        whose rebalance is due (engine.py:181-205) the placement is rebuilt and
+        the moved replicas' weight bytes are charged as a migration over NVLink
+        (all of it for eplb, the part exceeding that iteration's dispatch time for
+        async-eplb, engine.py:217-228); each rank's BF16 compute over its hosted
+        replica shares (rank_expert_rows) is measured on the GPU. ``eplb_state``:
+        EplbState keyword arguments (default: the reference's, window 100 /
+        interval 100 / budget 8)."""
+        from .eplb import EplbState, eplb_schedule, rank_expert_rows
+        from .virtual_ep import (NVLINK_GBPS, a2a_ms, layer_timing, measure_arms, measure_rank_compute,
+                                 measure_transform, placement_compute_arm, traffic_matrix)
 
         torch, cl, shape = self.torch, self.cluster, self.shape
         for s in strategies:
             if s not in STRATEGIES:
                 raise ValueError(f"unknown strategy {s!r}; valid: {', '.join(STRATEGIES)}")
-        runs = {s: MeasuredRun(s, timing_source="measured per-rank compute + K3 (CUDA events, virtual EP "
-                                                "on one B200) + NVLink model for dispatch/combine")
-                for s in strategies}
+        src = ("measured per-rank compute + K3 (CUDA events, virtual EP on one B200) + NVLink model for "
+               "dispatch/combine/migration")
+        runs = {s: MeasuredRun(s, timing_source=src) for s in strategies}
         checks = []
         R, epr, E, H, k = cl.num_ranks, cl.experts_per_rank, shape.num_experts, shape.hidden, shape.top_k
-        placement = place_experts_static(cl)
+        static = place_experts_static(cl)
         its = range(self.trace.num_iterations) if iterations is None else iterations
+        precision_strats = [s for s in strategies if s not in ("eplb", "async-eplb")]
+        eplb_strats = [s for s in strategies if s in ("eplb", "async-eplb")]
         # forward order: all-BF16 rows first, then the NVFP4 strategies, so every
         # strategy's per-rank compute reads operands a forward actually produced
-        order = sorted(strategies, key=lambda s: {"fp4all": 1, "realb": 2, "realb-seq": 2}.get(s, 0))
+        order = sorted(set(precision_strats) | ({"baseline"} if eplb_strats else set()),
+                       key=lambda s: {"fp4all": 1, "realb": 2, "realb-seq": 2}.get(s, 0))
+        # placements per iteration (a pure function of the trace's totals)
+        sched = {s: dict(zip(its, eplb_schedule(self.trace, EplbState(**(eplb_state or {})), its)))
+                 for s in eplb_strats}
+        eplace = {}
+        # a migrated replica moves the expert's real weights: gate, up, down in bf16
+        bytes_per_expert = 3 * H * shape.intermediate * 2
         for it in its:
+            pending = {}
+            for s in eplb_strats:  # engine.py:181-205
+                eplace[s], moved = sched[s][it]
+                runs[s].max_redundant_count = max(runs[s].max_redundant_count, eplace[s].redundant_count)
+                if moved is not None:
+                    vol = moved * bytes_per_expert
+                    pending[s] = (moved, vol, int(round(vol / (NVLINK_GBPS * 1e9) * 1e9)))
+            dispatch_total = {s: 0 for s in eplb_strats}
             for la in range(self.trace.cluster.num_layers):
                 loads = self.trace.layer_loads(it, la)
                 if not loads:
@@ -361,11 +409,11 @@ class TraceReplay:
                     res = self.layer.forward(x, mod, s, self.pair_params)
                     torch.cuda.synchronize()
                     plans[s] = plan = res.plan
-                    precs[s] = plan.expert_precision(placement).astype(np.int64)
+                    precs[s] = plan.expert_precision(static).astype(np.int64)
                     if check:
-                        host_pairs = plan_for(s, aggregate_rank_loads(pair_loads(loads, k), placement, R), cl,
+                        host_pairs = plan_for(s, aggregate_rank_loads(pair_loads(loads, k), static, R), cl,
                                               self.pair_params)
-                        host_trace = plan_for(s, aggregate_rank_loads(loads, placement, R), cl, self.params)
+                        host_trace = plan_for(s, aggregate_rank_loads(loads, static, R), cl, self.params)
                         checks.append({"iter": it, "layer": la, "strategy": s, "tokens": T,
                                        "counts_equal": bool((res.expert_vt.astype(np.int64) == want).all()),
                                        "routing_equal": bool((np.sort(self.layer.topk_idx[:T].cpu().numpy(), 1)
@@ -375,18 +423,43 @@ class TraceReplay:
                                        "plan": [p.value for p in plan.per_rank_precision],
                                        "host_plan": [p.value for p in host_trace.per_rank_precision],
                                        "w4a4_ranks": sorted(plan.accelerated_ranks)})
+                # per-rank compute of every arm, interleaved per rank
                 comp = dict(zip(order, measure_rank_compute(torch, self.layer, T, [precs[s] for s in order],
                                                             R, epr, reps=5)))
+                T_local = max(1, -(-T // R))
+                pairs = traffic_matrix(idx, T_local, epr, R)
+                if eplb_strats:
+                    expert_pairs = want.sum(1)
+                    rows = {s: rank_expert_rows(expert_pairs, eplace[s], R) for s in eplb_strats}
+                    ecomp = measure_arms(torch, [placement_compute_arm(torch, self.layer, rows[s])
+                                                 for s in eplb_strats], reps=5)
+                    comp.update(zip(eplb_strats, ecomp))
                 any_fp4 = np.max([precs[s] for s in order], axis=0)
                 trans = measure_transform(torch, self.layer, any_fp4, R, epr)
-                pairs = traffic_matrix(idx, max(1, -(-T // R)), epr, R)
                 disp = a2a_ms(pairs, np.full(R, 2.0 * H))
                 comb = a2a_ms(pairs.T.copy(), np.full(R, 2.0 * H))
-                for s in order:
+                for s in precision_strats:
                     acc = [bool(precs[s][r * epr] == 1) for r in range(R)]
                     mode = PipelineMode.OVERLAPPED if s in ("fp4all", "realb") and plans[s].active \
                         else PipelineMode.SEQUENTIAL  # engine.py:162-167
                     tr = [trans[r] if acc[r] else 0.0 for r in range(R)]
                     runs[s].plans[(it, la)] = plans[s]
                     runs[s].layer_timings[(it, la)] = layer_timing(comp[s], tr, acc, mode, disp, comb)
-        return runs, checks
+                for s in eplb_strats:
+                    # source rank x expert pairs, sent to the expert's hosts in their shares
+                    src_e = np.zeros((R, E), np.float64)
+                    np.add.at(src_e, (np.repeat(np.arange(T) // T_local, k), idx.reshape(-1)), 1.0)
+                    share = rows[s] / np.maximum(expert_pairs, 1)[None, :]      # [R_dst, E]
+                    traffic = src_e @ share.T                                      # [R_src, R_dst]
+                    d_s = a2a_ms(traffic, np.full(R, 2.0 * H))
+                    c_s = a2a_ms(traffic.T.copy(), np.full(R, 2.0 * H))
+                    lt = layer_timing(comp[s], [0.0] * R, [False] * R, PipelineMode.SEQUENTIAL, d_s, c_s)
+                    runs[s].plans[(it, la)] = plan_for(s, aggregate_rank_loads(loads, static, R), cl, self.params)
+                    runs[s].layer_timings[(it, la)] = lt
+                    dispatch_total[s] += lt.per_rank[0].dispatch_ns
+            for s in eplb_strats:  # migration charge (engine.py:217-228), then observe
+                if s in pending:
+                    moved, vol, mig_ns = pending[s]
+                    charged = max(0, mig_ns - dispatch_total[s]) if s == "async-eplb" else mig_ns
+                    runs[s].migration_events.append(MigrationEvent(it, moved, vol, charged))
+        return {s: runs[s] for s in strategies}, checks

@@ -59,26 +59,49 @@ def a2a_ms(pairs: np.ndarray, row_bytes_to: np.ndarray) -> float:
     return ALPHA_US / 1e3 + float(per_rank.max()) / (NVLINK_GBPS * 1e9) * 1e3
 
 
+def measure_arms(torch, arms, reps: int = 7):
+    """arms[a][r]: a callable launching arm a's work for virtual rank r. Per rank,
+    the arms are timed interleaved per repetition (clock / power drift hits every
+    arm alike); returns [arm][rank] median ms."""
+    R = len(arms[0])
+    out = [[0.0] * R for _ in arms]
+    for r in range(R):
+        ts = [[] for _ in arms]
+        for _ in range(reps):
+            for a, arm in enumerate(arms):
+                ts[a].append(_median_ms(torch, arm[r], reps=1))
+        for a in range(len(arms)):
+            out[a][r] = float(sorted(ts[a])[len(ts[a]) // 2])
+    return out
+
+
 def measure_rank_compute(torch, layer, T: int, precs, R: int, epr: int, reps: int = 7):
     """Per virtual rank, the expert compute of that rank's experts alone (their
     grouped-GEMM launches over the rows the last forward dispatched), for each
-    expert-precision vector in ``precs`` (codes 0 W16A16 / 1 W4A4). Arms are
-    interleaved per repetition; returns one [R] list of median ms per arm."""
+    expert-precision vector in ``precs`` (codes 0 W16A16 / 1 W4A4)."""
     E = R * epr
-    out = [[0.0] * R for _ in precs]
-    for r in range(R):
-        masks = []
-        for p in precs:
+    arms = []
+    for p in precs:
+        arm = []
+        for r in range(R):
             m = np.full(E, 2, np.int64)
             m[r * epr:(r + 1) * epr] = p[r * epr:(r + 1) * epr]
-            masks.append(m)
-        ts = [[] for _ in precs]
-        for _ in range(reps):
-            for a, m in enumerate(masks):
-                ts[a].append(_median_ms(torch, lambda: layer.expert_compute(T, m), reps=1))
-        for a in range(len(precs)):
-            out[a][r] = float(sorted(ts[a])[len(ts[a]) // 2])
-    return out
+            arm.append(lambda m=m: layer.expert_compute(T, m))
+        arms.append(arm)
+    return measure_arms(torch, arms, reps)
+
+
+def placement_compute_arm(torch, layer, rank_rows: np.ndarray):
+    """Callables timing each rank's BF16 expert compute over its hosted expert
+    instances (rank_rows [R, E] pairs, e.g. eplb.rank_expert_rows)."""
+    from .moe import host_layout
+
+    arm = []
+    for r in range(rank_rows.shape[0]):
+        lay, _ = host_layout(rank_rows[r], np.zeros(rank_rows.shape[1], np.int64))
+        lt = torch.from_numpy(lay).to(layer.device)
+        arm.append(lambda lt=lt: layer.bf16_compute_on(lt))
+    return arm
 
 
 def measure_transform(torch, layer, prec, R: int, epr: int) -> list[float]:

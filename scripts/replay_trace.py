@@ -27,7 +27,12 @@ def main():
     cluster = ClusterConfig(**meta["cluster"])
     trace = read_trace(a.trace, cluster)
     rep = TraceReplay(torch, a.config, trace)
-    runs, checks = rep.run(strategies=("baseline", "fp4all", "realb"))
+    # EPLB comparator: the reference's balancer with a one-iteration window and a
+    # rebalance every iteration (the fixtures hold 2-3 iterations; the reference's
+    # default 100/100 would never rebalance inside them)
+    strategies = ("baseline", "fp4all", "realb", "eplb", "async-eplb")
+    runs, checks = rep.run(strategies=strategies,
+                           eplb_state=dict(window_size=1, interval=1, redundant_budget=8))
     digest = file_sha256(a.trace)
     name = os.path.splitext(os.path.basename(a.trace))[0]
     summaries = {s: write_run(r, trace, os.path.join(a.out, name, s), digest, ranks_iters=(0,))
@@ -35,7 +40,11 @@ def main():
     report = speedup_report(summaries)
     ok = all(c["routing_equal"] and c["counts_equal"] and c["plan_equal_pairs"] and c["plan_equal_trace"]
              for c in checks)
-    out = {"trace": a.trace, "trace_sha256": digest, "config": a.config, "layers": len(checks) // 3,
+    out = {"trace": a.trace, "trace_sha256": digest, "config": a.config,
+           "layers": len({(c["iter"], c["layer"]) for c in checks}),
+           "eplb": {"window_size": 1, "interval": 1, "redundant_budget": 8,
+                    "migrations": {s: [(e.iteration, e.replicas_moved, e.volume_bytes, e.charged_ns)
+                                       for e in runs[s].migration_events] for s in ("eplb", "async-eplb")}},
            "parity_all_layers": ok, "report": report,
            "failed_checks": [c for c in checks if not (c["routing_equal"] and c["counts_equal"]
                                                         and c["plan_equal_pairs"] and c["plan_equal_trace"])][:6],
