@@ -22,14 +22,17 @@ namespace realb {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B rows = one SWIZZLE_128B atom width
+// TMA-store staging buffers per epilogue warp: a warp reuses a buffer only after
+// the store issued kEpiBufs chunks earlier has read it (bulk wait_group.read)
+constexpr int kEpiBufs = 4;
 
 template <int BN, int STAGES, int CL>
 struct SmemBf16 {
   static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int B_BYTES = (BN / CL) * kBK * 2;  // a pair stages half of W per CTA
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;       // 4 warps x 2 x (32 rows x 64 B)
-  static constexpr int EPI_BYTES = 4 * 2 * 2048;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;       // 4 warps x kEpiBufs x (32 rows x 64 B)
+  static constexpr int EPI_BYTES = 4 * kEpiBufs * 2048;
   static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
   static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // + barriers/slots + alignment slack
 };
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> smem -> TMA store
     const int q = warp & 3;  // TMEM lane quadrant = 32-row slice of this CTA's 128 rows
-    const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + q * 4096);
+    const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + q * (kEpiBufs * 2048));
     int nbuf = 0;
     for (int i = 0;; ++i) {
       const int slot = i % kTileRing;
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(256, 1)
                                silu_mul(__uint_as_float(g[2 * j + 1]), __uint_as_float(u[2 * j + 1])));
         }
         // the buffer about to be reused must have been read out by its TMA store
-        if (lane == 0) bulk_wait_group_read<1>();
+        if (lane == 0) bulk_wait_group_read<kEpiBufs - 1>();
         __syncwarp();
         const uint32_t buf = ebuf + nbuf * 2048;
         stage_row64(buf, lane, p);
@@ -286,10 +289,10 @@ __global__ void __launch_bounds__(256, 1)
         __syncwarp();
         if (lane == 0) {
           const int col = EPI == REALB_EPI_STORE ? c.n0 + ch * 32 : c.n0 / 2 + ch * 32;
-          tma_store_2d(&tmOut, smem + S::EPI_OFF + q * 4096 + nbuf * 2048, col, row0);
+          tma_store_2d(&tmOut, smem + S::EPI_OFF + q * (kEpiBufs * 2048) + nbuf * 2048, col, row0);
           bulk_commit_group();
         }
-        nbuf ^= 1;
+        nbuf = nbuf + 1 == kEpiBufs ? 0 : nbuf + 1;
       }
       tc_fence_before();
       __syncwarp();
@@ -368,12 +371,13 @@ extern "C" int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // 2-CTA pairs (cta_group::2, 6 stages) when experts are large: a pair needs an
-  // even number of 128-row m-tiles per expert and wastes half a pair otherwise,
-  // so small-expert launches (avg < 8 m-tiles per expert) stay 1-CTA.
-  // REALB_GEMM_CLUSTER=1|2 forces the choice.
+  // 1-CTA tiles by default. The 2-CTA pair form (cta_group::2, 6 stages; same
+  // results) halves the W bytes per SM and its TMA-only time drops, but measured
+  // interleaved against the 1-CTA kernel it was slower on every shape
+  // (scripts/bench_gemm.py: Kimi EP8 hot rank gate_up 0.876 vs 0.840 ms, 1-GPU
+  // layer 0.493 vs 0.469 ms). REALB_GEMM_CLUSTER=2 selects it.
   const char* cl_env = getenv("REALB_GEMM_CLUSTER");
-  const bool pair = cl_env ? cl_env[0] == '2' : (rows_cap / E) >= 1024;
+  const bool pair = cl_env && cl_env[0] == '2';
   if (epilogue == REALB_EPI_STORE)
     return pair ? launch_grouped_bf16<256, 6, REALB_EPI_STORE, 2>(d_a, d_w, rows_cap, N, K, E,
                                                                    d_layout, prec, d_out, max_ctas, st)

@@ -41,6 +41,7 @@ constexpr int kF4BM = 128, kF4BN = 256;
 constexpr int kF4BKB = 128;               // bytes of K per stage = 256 E2M1 values
 constexpr int kF4Threads = 384;
 constexpr int kSfBoxRows = 8;             // scale TMA box: 8 x 256 B = 2 KB = 4 atoms
+constexpr int kF4EpiBufs = 3;             // TMA-store staging buffers per epilogue warp (STORE)
 
 template <int EPI, int CL>
 struct SmemFp4 {
@@ -51,8 +52,8 @@ struct SmemFp4 {
   static constexpr int SFA_BYTES = 4 * 512;                   // 128 rows x 16 scales
   static constexpr int SFB_BYTES = 2 * 4 * 512;               // 256 rows x 16 scales (full W tile)
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-  static constexpr int EPI_OFF = STAGES * STAGE;    // 8 warps x 2 x 2 KB (STORE only)
-  static constexpr int EPI_BYTES = EPI == REALB_EPI_STORE ? 8 * 4096 : 0;
+  static constexpr int EPI_OFF = STAGES * STAGE;    // 8 warps x kF4EpiBufs x 2 KB (STORE only)
+  static constexpr int EPI_BYTES = EPI == REALB_EPI_STORE ? 8 * kF4EpiBufs * 2048 : 0;
   static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
     const int q = warp & 3, half = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
     int tile_it = 0;
+    int sbuf = 0;  // next STORE staging buffer of this warp
     for (int it = 0;; ++it) {
       const int slot = it % kF4Ring;
       mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
@@ -384,16 +386,16 @@ __global__ void __launch_bounds__(kF4Threads, 1)
         *reinterpret_cast<uint32_t*>(args.out_sf + sf_mma_offset(r, ocol / 16, I / 16)) = sfw;
       } else {  // bf16 out via smem staging (SWIZZLE_64B) + TMA store, 32 columns at a time
         const int wi = warp - 4;
-        const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + wi * 4096);
+        const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + wi * (kF4EpiBufs * 2048));
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           uint32_t p[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             p[j] = pack_bf16x2(__uint_as_float(v[i][2 * j]), __uint_as_float(v[i][2 * j + 1]));
-          if (lane == 0) bulk_wait_group_read<1>();
+          if (lane == 0) bulk_wait_group_read<kF4EpiBufs - 1>();
           __syncwarp();
-          const uint32_t buf = ebuf + (i & 1) * 2048;
+          const uint32_t buf = ebuf + (uint32_t)(sbuf * 2048);
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc)
             st_shared_v4(buf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), p[4 * cc], p[4 * cc + 1],
@@ -401,10 +403,11 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmOut, smem + S::EPI_OFF + wi * 4096 + (i & 1) * 2048,
+            tma_store_2d(&tmOut, smem + S::EPI_OFF + wi * (kF4EpiBufs * 2048) + sbuf * 2048,
                          c.n0 + half * 128 + 32 * i, c.a_row + q * 32);
             bulk_commit_group();
           }
+          sbuf = sbuf + 1 == kF4EpiBufs ? 0 : sbuf + 1;
         }
       }
       }
