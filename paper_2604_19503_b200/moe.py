@@ -456,3 +456,34 @@ class MoELayer:
         if int(self.flag.item()):
             self.flag.zero_()
             raise QuantizationDomainError("non-finite value reached the NVFP4 quantiser")
+
+
+class ModalitySplitMoELayer:
+    """A modality-split MoE layer (ERNIE-4.5-VL: separate text and vision expert
+    groups; BASELINE configs[3]). Text tokens go through the text group at
+    W16A16; vision tokens through the vision group, where ReaLB applies with the
+    modality-isolated policy (every loaded hot rank is eligible,
+    balancers.py:105-106). The split is boolean-mask indexing on the token-type
+    mask — the surrounding model does the same (a host sync, as there) — and the
+    two groups' outputs are scattered back into token order."""
+
+    def __init__(self, text: MoELayer, vision: MoELayer):
+        if not vision.cluster.modality_isolated:
+            raise ValueError("the vision group must use a modality_isolated cluster")
+        self.text, self.vision = text, vision
+
+    def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
+                params: RealbParams | None = None, out: torch.Tensor | None = None):
+        """-> (y [T, H] bf16, text LayerResult or None, vision LayerResult or None)"""
+        vis = modality.bool()
+        iv = vis.nonzero().squeeze(1)
+        it = (~vis).nonzero().squeeze(1)
+        y = torch.empty_like(x) if out is None else out
+        rt = rv = None
+        if it.numel():
+            rt = self.text.forward(x.index_select(0, it), modality.index_select(0, it), "baseline")
+            y.index_copy_(0, it, rt.y)
+        if iv.numel():
+            rv = self.vision.forward(x.index_select(0, iv), modality.index_select(0, iv), strategy, params)
+            y.index_copy_(0, iv, rv.y)
+        return y, rt, rv

@@ -120,3 +120,26 @@ def make_batch(shape: MoEShape, spec: WorkloadSpec, device="cuda"):
     unit, router = make_router(shape, spec, device)
     x = make_hidden(shape, spec, unit, idx)
     return x, torch.from_numpy(modality).to(device), router, idx
+
+
+def make_split_batch(text_shape: MoEShape, vision_shape: MoEShape, spec: WorkloadSpec, device="cuda"):
+    """A modality-split (ERNIE) batch: vision tokens routed with margins over the
+    vision group's router, text tokens over the text group's (separate router
+    seeds), interleaved by a seeded token-type mask. -> (x, modality, router_text,
+    router_vision, planned_text, planned_vision)."""
+    from dataclasses import replace
+
+    T = spec.tokens
+    n_vis = int(round(T * spec.vision_frac))
+    rng = np.random.default_rng(np.random.SeedSequence(spec.seed, spawn_key=(4, spec.layer, spec.rank)))
+    modality = np.zeros(T, np.uint8)
+    modality[rng.permutation(T)[:n_vis]] = 1
+    xt, _, rt, pt = make_batch(text_shape, replace(spec, tokens=T - n_vis, vision_frac=0.0), device)
+    xv, _, rv, pv = make_batch(vision_shape, replace(spec, tokens=n_vis, vision_frac=1.0, seed=spec.seed + 1),
+                               device)
+    x = torch.empty(T, text_shape.hidden, dtype=torch.bfloat16, device=device)
+    mod = torch.from_numpy(modality).to(device)
+    vis = mod.bool()
+    x[~vis] = xt
+    x[vis] = xv
+    return x, mod, rt, rv, pt, pv

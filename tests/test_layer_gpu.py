@@ -260,3 +260,37 @@ def test_cuda_graph_capture_matches_eager(strategy, R):
     x.copy_(x2)
     mod.copy_(m2)
     assert torch.equal(cap.replay(), eager2)
+
+
+@pytest.mark.parametrize("strategy", ["baseline", "fp4all"])
+def test_ernie_modality_split_layer_vs_oracle(strategy):
+    """BASELINE configs[3]: text tokens -> text group (W16A16), vision tokens ->
+    vision group (ReaLB / FP4 policy, modality-isolated), vs the oracle per group."""
+    from paper_2604_19503_b200.moe import ModalitySplitMoELayer
+    from paper_2604_19503_b200.workload import make_split_batch
+
+    st, sv = small(SHAPES["ernie_text"], 8), small(SHAPES["ernie_vision"], 8)
+    T = 768
+    x, mod, rt, rv, pt, pv = make_split_batch(st, sv, WorkloadSpec(tokens=T, vision_frac=0.7, num_ranks=2))
+    gt, dt = make_experts(st, seed=11)
+    gv, dv = make_experts(sv, seed=12)
+    text = MoELayer(MoEWeights.from_hf(st, rt, gt, dt), max_tokens=T, cluster=ClusterConfig(2, 1, 4, 1))
+    vision = MoELayer(MoEWeights.from_hf(sv, rv, gv, dv), max_tokens=T, cluster=ClusterConfig(2, 1, 4, 1, True))
+    layer = ModalitySplitMoELayer(text, vision)
+    y, res_t, res_v = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+    torch.cuda.synchronize()
+    vis = mod.bool().cpu().numpy()
+    xf = x.float().cpu().numpy()
+    for sel, shape, router, gu, dn, res, prec in (
+            (~vis, st, rt, gt, dt, res_t, np.zeros(8, np.int64)),
+            (vis, sv, rv, gv, dv, res_v, res_v.plan.expert_precision(vision.placement))):
+        ref = moe_ref.moe_layer(xf[sel], np.full(sel.sum(), int(shape is sv), np.uint8), router.float().cpu().numpy(),
+                                gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
+                                expert_prec=prec)
+        got = y.float().cpu().numpy()[sel]
+        err = np.linalg.norm(got - ref["y"]) / np.linalg.norm(ref["y"])
+        assert err < 2e-2, (shape.name, err)
+    # the vision group is modality-isolated: under fp4all every vision expert runs W4A4
+    if strategy == "fp4all":
+        assert res_v.plan.expert_precision(vision.placement).all()
+    assert res_t.plan.active is False
