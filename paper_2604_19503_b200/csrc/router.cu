@@ -26,30 +26,31 @@ constexpr int kRBK = 64;
 
 constexpr int kKMax = 8;
 
-template <int EPAD>
+template <int EPAD, int NSTAGE>
 struct RouterSmem {
   static constexpr int A_BYTES = 128 * kRBK * 2;          // MMA reads 128 rows
   static constexpr int A_LOAD = REALB_CHUNK_TOKENS * kRBK * 2;  // TMA fills 64
   static constexpr int B_BYTES = EPAD * kRBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGE_TX = A_LOAD + B_BYTES;
-  // as many stages as fit in ~200 KB: the router is latency-bound per SM (one CTA
-  // per 128 tokens), so bytes in flight set its HBM throughput
-  static constexpr int STAGES = 4;
+  // the router is latency-bound per SM (one CTA per 64 tokens), so bytes in flight
+  // set its HBM throughput: 8 stages when the grid fits one CTA per SM, 4 (two
+  // CTAs per SM) for larger grids
+  static constexpr int STAGES = NSTAGE * STAGE <= 200 * 1024 ? NSTAGE : (200 * 1024) / STAGE;
   static constexpr int HIST_OFF = STAGES * STAGE;
   static constexpr int BAR_OFF = HIST_OFF + 256 * 2 * 4;
   static constexpr int TOTAL = BAR_OFF + 128 + 1024;
   static constexpr uint32_t TMEM_COLS = EPAD <= 32 ? 32 : EPAD <= 64 ? 64 : EPAD <= 128 ? 128 : 256;
 };
 
-template <int EPAD, int KK>
+template <int EPAD, int KK, int NSTAGE>
 __global__ void __launch_bounds__(256, 1)
     router_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const float* __restrict__ bias, const uint8_t* __restrict__ modality, int T,
                   int H, int E, int scoring, float routed_scaling, float norm_min,
                   float* __restrict__ logits, int32_t* __restrict__ topk_idx,
                   float* __restrict__ topk_w, int32_t* __restrict__ chunk_counts, uint32_t dbg) {
-  using S = RouterSmem<EPAD>;
+  using S = RouterSmem<EPAD, NSTAGE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0) {  // ---------------- TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -116,8 +117,17 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_commit(done);
     }
-  } else if (warp >= 4 && warp < 4 + REALB_CHUNK_TOKENS / 32) {  // rows 0..63 = TMEM lanes 0..63
+  }
+  // ---------------- epilogue: rows 0..63 = TMEM lane quadrants 0 and 1. Each row is
+  // served by two warps of its quadrant — warp 4/5 ("primary", the low expert-column
+  // half) and warp 0/1 (the producer / MMA warps, free once the MMAs are done: the
+  // high half) — so a row's E logits are scanned by two threads in parallel (the scan
+  // is a dependent compare/insert chain; one thread per row left it latency-bound).
+  // The high half's partial top-k and softmax state goes through shared memory (the
+  // operand stages are dead by then) and the primary thread merges it.
+  if (warp == 0 || warp == 1 || warp == 4 || warp == 5) {
     const int q = warp & 3;
+    const bool primary = warp >= 4;
     const int row = q * 32 + lane;
     const int t = chunk * REALB_CHUNK_TOKENS + row;
     const bool valid = t < T;
@@ -125,79 +135,130 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16);
     if (dbg & 1u) {  // debug: no epilogue work
-      named_bar_sync(1, REALB_CHUNK_TOKENS);
+      named_bar_sync(1, 128);
       tc_fence_before();
       goto router_done;
     }
 
     constexpr int k = KK;
+    constexpr int NG = EPAD / 16;           // 16-column TMEM groups
+    constexpr int NG_LO = (NG + 1) / 2;     // groups of the primary (low) half
     float sval[KK], lsel[KK];
     int sid[KK];
 #pragma unroll
     for (int j = 0; j < KK; ++j) { sval[j] = -INFINITY; lsel[j] = 0.f; sid[j] = 0; }
-    float run_max = -INFINITY, run_sum = 0.f;  // online softmax over all E logits
+    float run_max = -INFINITY, run_sum = 0.f;  // online softmax over this half's logits
     float* lrow = logits + (int64_t)t * E;
+    auto insert = [&](float s, float l, int e) {
+      if (s > sval[k - 1]) {  // strict: an equal score keeps the lower expert id
+        bool placed = false;
+#pragma unroll
+        for (int j = KK - 1; j >= 0; --j) {
+          if (placed) continue;
+          if (j > 0 && sval[j - 1] < s) {
+            sval[j] = sval[j - 1]; lsel[j] = lsel[j - 1]; sid[j] = sid[j - 1];
+          } else {
+            sval[j] = s; lsel[j] = l; sid[j] = e; placed = true;
+          }
+        }
+      }
+    };
+    const int g0 = primary ? 0 : NG_LO, g1 = primary ? NG_LO : NG;
 #pragma unroll 1
-    for (int c0 = 0; c0 < EPAD; c0 += 16) {
+    for (int g = g0; g < g1; ++g) {
+      const int c0 = g * 16;
       uint32_t v[16];
       tmem_ld16(tb + c0, v);
       tmem_wait_ld();
+      if (valid) {
+        if (c0 + 16 <= E && (E & 3) == 0) {
+          float4* l4 = reinterpret_cast<float4*>(lrow + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            l4[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        } else {
+          for (int i = 0; i < 16 && c0 + i < E; ++i) lrow[c0 + i] = __uint_as_float(v[i]);
+        }
+      }
+      if (scoring != REALB_SCORE_SIGMOID_RENORM) {  // one rescale per 16 logits
+        float m = run_max;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < E) m = fmaxf(m, __uint_as_float(v[i]));
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < E) acc += __expf(__uint_as_float(v[i]) - m);
+        run_sum = run_sum * __expf(run_max - m) + acc;
+        run_max = m;
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int e = c0 + i;
         if (e >= E) break;
         const float l = __uint_as_float(v[i]);
-        if (valid) lrow[e] = l;
-        const float s = bias ? l + __ldg(bias + e) : l;
-        if (scoring != REALB_SCORE_SIGMOID_RENORM) {
-          const float m = fmaxf(run_max, l);
-          run_sum = run_sum * __expf(run_max - m) + __expf(l - m);
-          run_max = m;
-        }
-        if (s > sval[k - 1]) {  // strict: an equal score keeps the lower expert id
-          bool placed = false;
-#pragma unroll
-          for (int j = KK - 1; j >= 0; --j) {
-            if (placed) continue;
-            if (j > 0 && sval[j - 1] < s) {
-              sval[j] = sval[j - 1]; lsel[j] = lsel[j - 1]; sid[j] = sid[j - 1];
-            } else {
-              sval[j] = s; lsel[j] = l; sid[j] = e; placed = true;
-            }
-          }
-        }
+        insert(bias ? l + __ldg(bias + e) : l, l, e);
       }
     }
-    // routing weights from the selected logits
-    float w[KK];
-    float wsum = 0.f;
-#pragma unroll
-    for (int j = 0; j < KK; ++j) {
-      float p;
-      if (scoring == REALB_SCORE_SIGMOID_RENORM)
-        p = 1.0f / (1.0f + __expf(-lsel[j]));
-      else
-        p = __expf(lsel[j] - run_max) / run_sum;  // softmax probability
-      w[j] = p;
-      wsum += p;
-    }
-    float scale;
-    if (scoring == REALB_SCORE_SOFTMAX_RENORM) scale = 1.0f / wsum;
-    else if (scoring == REALB_SCORE_SIGMOID_RENORM) scale = routed_scaling / wsum;
-    else scale = 1.0f / fmaxf(wsum, norm_min);
-    if (valid) {
-      const int vis = modality[t] ? 0 : 1;  // hist[e][0] vision, [e][1] text
+    // hand the high half's state to the primary thread of the same row
+    float* xs = reinterpret_cast<float*>(smem);  // operand stages are free after `done`
+    constexpr int XS = 3 * KK + 2;
+    if (!primary) {
 #pragma unroll
       for (int j = 0; j < KK; ++j) {
-        topk_idx[(int64_t)t * k + j] = sid[j];
-        topk_w[(int64_t)t * k + j] = w[j] * scale;
-        atomicAdd(&hist[2 * sid[j] + vis], 1);
+        xs[row * XS + j] = sval[j];
+        xs[row * XS + KK + j] = lsel[j];
+        xs[row * XS + 2 * KK + j] = __int_as_float(sid[j]);
+      }
+      xs[row * XS + 3 * KK] = run_max;
+      xs[row * XS + 3 * KK + 1] = run_sum;
+    }
+    named_bar_sync(1, 128);
+    if (primary) {
+#pragma unroll
+      for (int j = 0; j < KK; ++j)  // high-half candidates: descending, higher ids than ours
+        insert(xs[row * XS + j], xs[row * XS + KK + j], __float_as_int(xs[row * XS + 2 * KK + j]));
+      if (scoring != REALB_SCORE_SIGMOID_RENORM) {
+        const float m2 = xs[row * XS + 3 * KK], s2 = xs[row * XS + 3 * KK + 1];
+        const float m = fmaxf(run_max, m2);
+        run_sum = (run_sum > 0.f ? run_sum * __expf(run_max - m) : 0.f) +
+                  (s2 > 0.f ? s2 * __expf(m2 - m) : 0.f);
+        run_max = m;
+      }
+      // routing weights from the selected logits
+      float w[KK];
+      float wsum = 0.f;
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        float p;
+        if (scoring == REALB_SCORE_SIGMOID_RENORM)
+          p = 1.0f / (1.0f + __expf(-lsel[j]));
+        else
+          p = __expf(lsel[j] - run_max) / run_sum;  // softmax probability
+        w[j] = p;
+        wsum += p;
+      }
+      float scale;
+      if (scoring == REALB_SCORE_SOFTMAX_RENORM) scale = 1.0f / wsum;
+      else if (scoring == REALB_SCORE_SIGMOID_RENORM) scale = routed_scaling / wsum;
+      else scale = 1.0f / fmaxf(wsum, norm_min);
+      if (valid) {
+        const int vis = modality[t] ? 0 : 1;  // hist[e][0] vision, [e][1] text
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          topk_idx[(int64_t)t * k + j] = sid[j];
+          topk_w[(int64_t)t * k + j] = w[j] * scale;
+          atomicAdd(&hist[2 * sid[j] + vis], 1);
+        }
       }
     }
     tc_fence_before();
-    named_bar_sync(1, REALB_CHUNK_TOKENS);
-    int32_t* out = chunk_counts + (int64_t)chunk * E * 2;
-    for (int i = row; i < 2 * E; i += REALB_CHUNK_TOKENS) out[i] = hist[i];
+    named_bar_sync(1, 128);
+    if (primary) {
+      int32_t* out = chunk_counts + (int64_t)chunk * E * 2;
+      for (int i = row; i < 2 * E; i += REALB_CHUNK_TOKENS) out[i] = hist[i];
+    }
   }
 router_done:
   tc_fence_before();
@@ -217,15 +278,19 @@ static int launch_router(const void* x, const void* wg, const float* bias, const
   rc = make_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, wg, H, E, (uint64_t)H * 2, kRBK, EPAD,
                     CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  auto kern = router_kernel<EPAD, KK>;
-  const int smem = RouterSmem<EPAD>::TOTAL;
-  rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "router smem attribute");
-  if (rc) return rc;
   const int grid = (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS;
   const char* dbg_env = getenv("REALB_DBG_ROUTER");
   const uint32_t dbg = dbg_env ? (uint32_t)strtoul(dbg_env, nullptr, 0) : 0u;
-  kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc, dbg);
-  return check_launch("realb_router_topk_stats");
+  const char* st_env = getenv("REALB_ROUTER_STAGES");
+  const bool deep = st_env ? atoi(st_env) >= 8 : grid <= num_sms();
+  auto launch = [&](auto kern, int smem) {
+    int r = set_smem_once(reinterpret_cast<const void*>(kern), smem, "router smem attribute");
+    if (r) return r;
+    kern<<<grid, 256, smem, st>>>(tx, tw, bias, mod, T, H, E, scoring, rs, nm, logits, idx, w, cc, dbg);
+    return check_launch("realb_router_topk_stats");
+  };
+  return deep ? launch(router_kernel<EPAD, KK, 8>, RouterSmem<EPAD, 8>::TOTAL)
+              : launch(router_kernel<EPAD, KK, 4>, RouterSmem<EPAD, 4>::TOTAL);
 }
 
 }  // namespace realb

@@ -13,13 +13,17 @@ for T in (8192, 65536):
     w = torch.empty(T, k, device="cuda"); cc = torch.empty((T + 63) // 64, E, 2, dtype=torch.int32, device="cuda")
     bias = torch.zeros(E, device="cuda")
     f = lambda: _lib.call("realb_router_topk_stats", x.data_ptr(), router.data_ptr(), bias.data_ptr(), mod.data_ptr(), T, H, E, k, 1, 2.446, 1e-12, logits.data_ptr(), idx.data_ptr(), w.data_ptr(), cc.data_ptr(), _lib.stream_ptr())
-    for dbg in (0, 1, 4, 5):
-        os.environ["REALB_DBG_ROUTER"] = str(dbg)
-        for _ in range(3): f()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(10):
-            a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-            a.record(); f(); b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
-        t = sorted(ts)[5]
-        print(f"T={T} dbg={dbg} {t*1e3:8.1f} us  {T*H*2/t/1e9:8.1f} GB/s", flush=True)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    for stages in ("4", "8"):
+        os.environ["REALB_ROUTER_STAGES"] = stages
+        for dbg in (0, 1):
+            os.environ["REALB_DBG_ROUTER"] = str(dbg)
+            for _ in range(3): f()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(15):
+                flush.zero_()  # x comes from HBM, as inside the layer step
+                a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+                a.record(); f(); b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
+            t = sorted(ts)[7]
+            print(f"T={T} stages={stages} dbg={dbg} {t*1e3:8.1f} us  {T*H*2/t/1e9:8.1f} GB/s", flush=True)
