@@ -191,6 +191,33 @@ __device__ __forceinline__ uint2 quant_block16_bf16(const uint32_t (&w)[8], uint
   return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
 }
 
+// quant_block16_bf16 with the decoded scale and its correctly rounded reciprocal
+// taken from a 128-entry (scale bits -> (sc, rn(1/sc))) table in shared memory
+// (sf_table_init): the same arithmetic, ~20 fewer instructions per block for the
+// HBM-bound weight quantiser.
+__device__ __forceinline__ void sf_table_init(float2* tab) {
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    const float sc = e4m3_decode((uint32_t)i);
+    tab[i] = make_float2(sc, i ? __frcp_rn(sc) : 0.0f);
+  }
+}
+__device__ __forceinline__ uint2 quant_block16_bf16_tab(const uint32_t (&w)[8], uint32_t& sbits,
+                                                        bool& nonfinite, const float2* tab) {
+  const uint32_t ab = amax_bits_bf16x16(w);
+  nonfinite = ab >= 0x7F80u;
+  const float amax = __uint_as_float(ab << 16);
+  sbits = block_scale_bits_bf16amax(amax);
+  if (sbits == 0u) return make_uint2(0u, 0u);
+  const float2 t = tab[sbits];
+  const float sc = t.x, r = t.y;
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    c[i] = cvt_e2m1x4(q1_div(bf16lo(w[2 * i]), sc, r), q1_div(bf16hi(w[2 * i]), sc, r),
+                      q1_div(bf16lo(w[2 * i + 1]), sc, r), q1_div(bf16hi(w[2 * i + 1]), sc, r));
+  return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
+}
+
 // same for 16 fp32 values that are known to be bf16-representable
 __device__ __forceinline__ uint2 quant_block16_bf16vals(const float (&v)[16], uint32_t& sbits) {
   float amax = 0.0f;

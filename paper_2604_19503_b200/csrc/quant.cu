@@ -51,7 +51,8 @@ template <int LAYOUT>
 __device__ __forceinline__ void quant_tile_bf16(const __nv_bfloat16* __restrict__ x, int64_t rows,
                                                 int64_t cols, int64_t nkb, int64_t tm, int64_t tk,
                                                 uint8_t* __restrict__ codes,
-                                                uint8_t* __restrict__ sf, int32_t* flag) {
+                                                uint8_t* __restrict__ sf, int32_t* flag,
+                                                const float2* tab) {
   // thread -> (row r0 + 64h, k-block kb): the two blocks are 64 rows apart
   const int r_in = threadIdx.x >> 2, kq = threadIdx.x & 3;
   const int64_t r0 = tm * 128 + r_in, kb = tk * 4 + kq;
@@ -80,7 +81,7 @@ __device__ __forceinline__ void quant_tile_bf16(const __nv_bfloat16* __restrict_
     if (!ok[h]) continue;
     uint32_t sbits;
     bool nf;
-    const uint2 c = quant_block16_bf16(w[h], sbits, nf);
+    const uint2 c = quant_block16_bf16_tab(w[h], sbits, nf, tab);
     if (nf) flag_nonfinite(flag);
     *reinterpret_cast<uint2*>(cp + h * cstep) = c;
     sf[so0 + h * sstep] = (uint8_t)sbits;
@@ -92,12 +93,15 @@ __global__ void __launch_bounds__(256) quant_kernel_bf16(const __nv_bfloat16* __
                                                           int64_t rows, int64_t cols,
                                                           uint8_t* __restrict__ codes,
                                                           uint8_t* __restrict__ sf, int32_t* flag) {
+  __shared__ float2 tab[128];
+  sf_table_init(tab);
+  __syncthreads();
   const int64_t nkb = cols >> 4;
   const int tiles_k = (int)((nkb + 3) >> 2);
   const int tiles = (int)((rows + 127) >> 7) * tiles_k;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int tm = tile / tiles_k, tk = tile - tm * tiles_k;
-    quant_tile_bf16<LAYOUT>(x, rows, cols, nkb, tm, tk, codes, sf, flag);
+    quant_tile_bf16<LAYOUT>(x, rows, cols, nkb, tm, tk, codes, sf, flag, tab);
   }
 }
 
@@ -115,6 +119,8 @@ __global__ void __launch_bounds__(256) quant_experts_kernel(
   // enumerate only the W4A4 experts' tiles: tile -> (j-th W4A4 expert, local tile)
   __shared__ int s_list[256];
   __shared__ int s_n;
+  __shared__ float2 tab[128];
+  sf_table_init(tab);
   if (threadIdx.x == 0) {
     int n = 0;
     for (int e = 0; e < E; ++e)
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(256) quant_experts_kernel(
     const int j = tile / tiles_per_expert, lt = tile - j * tiles_per_expert;
     const int lm = lt / tiles_k;
     quant_tile_bf16<REALB_SF_MMA128x4>(x, rows, cols, nkb, (int64_t)s_list[j] * mt_per_expert + lm,
-                                        lt - lm * tiles_k, codes, sf, flag);
+                                        lt - lm * tiles_k, codes, sf, flag, tab);
   }
 }
 

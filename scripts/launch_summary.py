@@ -6,7 +6,7 @@ ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Met
 agg = collections.OrderedDict()
 for r in rows:
     v = float(r[vi].replace(",", ""))
-    v = v / 1000 if r[ui] == "nsecond" else v * 1000 if r[ui] == "msecond" else v
+    v = v / 1000 if r[ui] in ("nsecond", "ns") else v * 1000 if r[ui] in ("msecond", "ms") else v
     agg.setdefault(r[ki][:70], []).append(v)
 for n, v in agg.items():
     if "realb" in n or "--all" in sys.argv:
