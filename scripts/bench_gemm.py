@@ -33,10 +33,10 @@ def main():
             epi = _lib.EPI_SWIGLU if "gate_up" in label else _lib.EPI_STORE
             f = lambda: _lib.call("realb_grouped_gemm_bf16", A.data_ptr(), W.data_ptr(), rows, N, K, E, lt.data_ptr(),
                                   0, epi, o.data_ptr(), 0, _lib.stream_ptr())
-            pfs = os.environ.get("BENCH_PF", "0").split(",")
-            variants = {f"cl{cl}_dbg{d}_pf{pf}": ({"REALB_GEMM_CLUSTER": cl, "REALB_DBG_BF16": str(d),
-                                                   "REALB_GEMM_L2PF": pf}, f)
-                        for cl in os.environ.get("BENCH_CL", "1,2").split(",") for d in dbgs for pf in pfs}
+            orders = os.environ.get("BENCH_ORDER", "m").split(",")
+            variants = {f"cl{cl}_dbg{d}_{o}": ({"REALB_GEMM_CLUSTER": cl, "REALB_DBG_BF16": str(d),
+                                                "REALB_GEMM_ORDER": o}, f)
+                        for cl in os.environ.get("BENCH_CL", "1,2").split(",") for d in dbgs for o in orders}
             offs = torch.tensor(np.cumsum((counts + 127) // 128 * 128), dtype=torch.int32, device="cuda")
             Wt = W.view(E, N, K).transpose(1, 2)
             variants["torch_grouped_mm"] = ({}, lambda: torch._grouped_mm(A, Wt, offs=offs))
