@@ -491,7 +491,8 @@ extern "C" int64_t realb_layout_words(int E, int nchunks) {
 extern "C" int realb_moe_align(const int32_t* d_cc, int nchunks, int E, const uint8_t* d_prec,
                                int row_align, int32_t* d_layout, int32_t* d_expert_vt,
                                void* stream) {
-  if (!d_cc || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 || nchunks < 0) {
+  if ((!d_cc && nchunks > 0) || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 ||
+      nchunks < 0) {
     set_error("realb_moe_align: bad arguments (E=%d nchunks=%d; E <= 256)", E, nchunks);
     return REALB_EINVAL;
   }
@@ -510,7 +511,8 @@ extern "C" int realb_moe_align_plan(const int32_t* d_cc, int nchunks, int E, int
                                     int64_t global_batch_threshold, int modality_isolated,
                                     uint8_t* d_prec, int32_t* d_plan_out, int32_t* d_layout,
                                     int32_t* d_expert_vt, void* stream) {
-  if (!d_cc || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 || nchunks < 0 || R < 1 ||
+  if ((!d_cc && nchunks > 0) || !d_prec || !d_layout || !d_expert_vt || E < 1 || E > 256 ||
+      nchunks < 0 || R < 1 ||
       R > 256 || E % R || strategy < 0 || strategy > 2) {
     set_error("realb_moe_align_plan: bad arguments (E=%d R=%d strategy=%d)", E, R, strategy);
     return REALB_EINVAL;
@@ -532,6 +534,7 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
                                       const int32_t* d_layout, int nchunks, int64_t rows_cap,
                                       int32_t* d_pair_pos, void* d_a_bf16, uint8_t* d_a_codes,
                                       uint8_t* d_a_sf, int32_t* d_flag, void* stream) {
+  if (T == 0 && nchunks == 0) return REALB_OK;
   if (!d_x || !d_topk_idx || !d_prec || !d_layout || !d_pair_pos || !d_a_bf16 || T < 0 ||
       H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
     set_error("realb_dispatch_permute: bad arguments (T=%d H=%d E=%d k=%d nchunks=%d)", T, H, E,
@@ -555,6 +558,7 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
 
 extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const float* d_w, int T,
                              int H, int k, void* d_y, void* stream) {
+  if (T == 0 && H > 0 && H % 8 == 0 && k >= 1 && k <= 8) return REALB_OK;
   if (!d_rows || !d_pos || !d_w || !d_y || T < 0 || H <= 0 || H % 8 || k < 1 || k > 8) {
     set_error("realb_combine: bad arguments (T=%d H=%d k=%d)", T, H, k);
     return REALB_EINVAL;

@@ -302,6 +302,7 @@ extern "C" int realb_router_topk_stats(const void* d_x, const void* d_wg, const 
                                        int scoring, float routed_scaling, float norm_min,
                                        float* d_logits, int32_t* d_topk_idx, float* d_topk_w,
                                        int32_t* d_chunk_counts, void* stream) {
+  if (T == 0 && E >= 1 && E <= 256 && k >= 1 && k <= kKMax && k <= E && H > 0) return REALB_OK;
   if (!d_x || !d_wg || !d_modality || !d_logits || !d_topk_idx || !d_topk_w || !d_chunk_counts ||
       T < 0 || E < 1 || E > 256 || k < 1 || k > kKMax || k > E || H <= 0 || scoring < 0 ||
       scoring > 2) {

@@ -294,3 +294,69 @@ def test_ernie_modality_split_layer_vs_oracle(strategy):
     if strategy == "fp4all":
         assert res_v.plan.expert_precision(vision.placement).all()
     assert res_t.plan.active is False
+
+
+@pytest.mark.parametrize("T", [1, 63, 64, 65, 129])
+@pytest.mark.parametrize("strategy", ["baseline", "fp4all"])
+def test_layer_ragged_token_counts(T, strategy):
+    """Token counts off the 64-token chunk and 128-row tile grids (partial chunks,
+    single-row experts, experts with no rows) match the oracle."""
+    shape = SHAPES["tiny"]
+    layer, x, mod, router, gu, dn, _ = build_layer(shape, T, R=2)
+    res = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+    torch.cuda.synchronize()
+    prec = res.plan.expert_precision(layer.placement)
+    ref = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                            gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
+                            expert_prec=prec, logits=layer.logits[:T].cpu().numpy())
+    assert (layer.topk_idx[:T].cpu().numpy() == ref["idx"]).all()
+    assert (res.expert_vt == ref["vt"]).all()
+    y = res.y.float().cpu().numpy()
+    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
+    assert err < 2e-2, err
+
+
+def test_layer_zero_tokens():
+    """An empty batch is a valid call: empty output, zero counts, inactive plan."""
+    shape = SHAPES["tiny"]
+    layer, x, mod, *_ = build_layer(shape, 64, R=2)
+    res = layer.forward(x[:0], mod[:0], "realb", RealbParams(global_batch_threshold=0))
+    torch.cuda.synchronize()
+    assert res.y.shape == (0, shape.hidden)
+    assert (res.expert_vt == 0).all() and not res.plan.active
+
+
+def test_layer_all_tokens_on_one_expert_set():
+    """Maximum skew: every token routes to the same k experts (one group holds all
+    T rows, the others none) — BF16 and W4A4 paths vs the oracle."""
+    shape = small(SHAPES["kimi"], 16)
+    T = 700
+    layer, x, mod, router, gu, dn, _ = build_layer(shape, T, R=2)
+    x = x[:1].expand(T, -1).contiguous()  # identical tokens -> identical top-k
+    for strategy in ("baseline", "fp4all"):
+        res = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+        torch.cuda.synchronize()
+        vt = res.expert_vt
+        assert (vt.sum(1) > 0).sum() == shape.top_k and vt.sum() == T * shape.top_k
+        prec = res.plan.expert_precision(layer.placement)
+        ref = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                                gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
+                                expert_prec=prec, routed_scaling=shape.routed_scaling,
+                                logits=layer.logits[:T].cpu().numpy())
+        y = res.y.float().cpu().numpy()
+        err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
+        assert err < 2e-2, (strategy, err)
+
+
+def test_nonfinite_weights_raise_quantization_domain_error():
+    """A non-finite bf16 weight reaching the quantiser sets the device flag; the
+    host raises the reference's QuantizationDomainError (fp4.py:22, :111-113)."""
+    from paper_2604_19503_b200.quant import QuantizationDomainError
+
+    shape = SHAPES["tiny"]
+    layer, x, mod, *_ = build_layer(shape, 256, R=2)
+    layer.w.w_gu[5, 7] = float("inf")
+    layer.forward(x, mod, "fp4all", RealbParams(global_batch_threshold=0))
+    torch.cuda.synchronize()
+    with pytest.raises(QuantizationDomainError):
+        layer.check_flag()
