@@ -33,7 +33,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="kimi", choices=["tiny", "kimi", "qwen", "ernie_vision"])
+    p.add_argument("--config", default="kimi", choices=["tiny", "kimi", "kimi_shared", "qwen", "ernie_vision"])
     p.add_argument("--tokens", type=int, default=8192, help="local tokens per GPU")
     p.add_argument("--vision-frac", type=float, default=0.7)
     p.add_argument("--cpu-sample-tokens", type=int, default=256)
@@ -49,7 +49,7 @@ def build_layer(args, torch, rank=0, world=1):
     from paper_2604_19503_b200 import _lib
     from paper_2604_19503_b200.moe import SHAPES, MoELayer, MoEWeights
     from paper_2604_19503_b200.policy import ClusterConfig
-    from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts
+    from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts, make_shared_expert
 
     shape = SHAPES[args.config]
     spec = WorkloadSpec(tokens=args.tokens, vision_frac=args.vision_frac,
@@ -57,7 +57,7 @@ def build_layer(args, torch, rank=0, world=1):
     x, mod, router, _ = make_batch(shape, spec)
     gu, dn = make_experts(shape)
     bias = torch.zeros(shape.num_experts, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
-    w = MoEWeights.from_hf(shape, router, gu, dn, bias=bias)
+    w = MoEWeights.from_hf(shape, router, gu, dn, bias=bias, shared=make_shared_expert(shape))
     del gu, dn
     cluster = ClusterConfig(world, 1, shape.num_experts // world, 1, shape.modality_isolated)
     return shape, w, x, mod, cluster

@@ -248,9 +248,11 @@ REALB_API int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t* 
                              int max_ctas, void* stream);
 
 /* C3 (local part) — weighted top-k combine:
- *   y[t][h] = sum_j topk_w[t][j] * rows[pair_pos[t][j]][h]   (fp32 acc, bf16 out) */
+ *   y[t][h] = addend[t][h] + sum_j topk_w[t][j] * rows[pair_pos[t][j]][h]
+ *   (fp32 accumulation, one bf16 rounding). d_addend: bf16 [T][H] or NULL —
+ *   the shared-expert output of models that have one (Kimi-VL, ERNIE-4.5-VL). */
 REALB_API int realb_combine(const void* d_rows, const int32_t* d_pair_pos, const float* d_topk_w,
-                  int T, int H, int k, void* d_y, void* stream);
+                  int T, int H, int k, const void* d_addend, void* d_y, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * P1 — host precision policy, identical fp64 operation order to

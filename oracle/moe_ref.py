@@ -93,9 +93,12 @@ def expert_mlp(xe, w_gate, w_up, w_down, w4a4: bool):
 
 
 def moe_layer(x, modality, wg, gate_up, down, k, scoring, expert_prec=None, bias=None,
-              routed_scaling=1.0, norm_min=1e-12, logits=None):
+              routed_scaling=1.0, norm_min=1e-12, logits=None, shared=None):
     """x [T,H] bf16 values (float32); gate_up [E,2I,H] (HF: gate rows first);
-    down [E,H,I]; expert_prec [E] 0/1. Returns dict with y and intermediates."""
+    down [E,H,I]; expert_prec [E] 0/1; shared: (gate_up [2Is,H], down [H,Is]) of a
+    shared-expert MLP added to every token (BF16 path, bf16 output, summed with the
+    routed contributions before the one final rounding). Returns dict with y and
+    intermediates."""
     T, H = x.shape
     E = wg.shape[0]
     I = down.shape[2]
@@ -108,5 +111,9 @@ def moe_layer(x, modality, wg, gate_up, down, k, scoring, expert_prec=None, bias
             continue
         ye = expert_mlp(x[tok], gate_up[e, :I], gate_up[e, I:], down[e], bool(prec[e]))
         y_pairs[tok, slot] = ye
-    out = bf16_round((w[:, :, None] * y_pairs).sum(axis=1, dtype=np.float32))
+    acc = (w[:, :, None] * y_pairs).sum(axis=1, dtype=np.float32)
+    if shared is not None:
+        Is = shared[1].shape[1]
+        acc = acc + expert_mlp(x, shared[0][:Is], shared[0][Is:], shared[1], False)
+    out = bf16_round(acc)
     return dict(y=out, logits=logits, idx=idx, w=w, vt=expert_counts(idx, modality, E))

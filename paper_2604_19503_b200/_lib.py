@@ -58,7 +58,7 @@ SIGNATURES: dict[str, tuple] = {
     "realb_grouped_gemm_bf16": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]),
     "realb_grouped_gemm_nvfp4": (
         _i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _vp]),
-    "realb_combine": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "realb_combine": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
     "realb_plan": (_i32, [_vp, _i32, _f64, _f64, _i64, _i32, _vp, _vp]),
     "realb_ep_pack": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp]),

@@ -363,7 +363,9 @@ using namespace realb;
 extern "C" int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t rows_cap, int N,
                                        int K, int E, const int32_t* d_layout, int prec,
                                        int epilogue, void* d_out, int max_ctas, void* stream) {
-  if (!d_a || !d_w || !d_layout || !d_out || rows_cap <= 0 || rows_cap % 128 || E <= 0 ||
+  // rows_cap only bounds the A / out tensor maps: rows past it read as zero (TMA
+  // OOB fill) and are never stored, so a dense operand of any row count works
+  if (!d_a || !d_w || !d_layout || !d_out || rows_cap <= 0 || E <= 0 ||
       (prec != REALB_PREC_W16A16 && prec != REALB_PREC_W4A4)) {
     set_error("realb_grouped_gemm_bf16: bad arguments");
     return REALB_EINVAL;

@@ -369,6 +369,7 @@ template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ rows,
                                                       const int32_t* __restrict__ pos,
                                                       const float* __restrict__ w, int T, int H,
+                                                      const __nv_bfloat16* __restrict__ addend,
                                                       __nv_bfloat16* __restrict__ y) {
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -385,6 +386,15 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
 #pragma unroll
     for (int j = 0; j < K; ++j) u[j] = __ldg(src[j] + c);  // all K loads in flight
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (addend) {  // shared-expert output (added in fp32 before the one bf16 rounding)
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(addend + (int64_t)t * H) + c);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] = bf16lo(av[i]);
+        acc[2 * i + 1] = bf16hi(av[i]);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const uint32_t v[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
@@ -557,7 +567,7 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
 }
 
 extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const float* d_w, int T,
-                             int H, int k, void* d_y, void* stream) {
+                             int H, int k, const void* d_addend, void* d_y, void* stream) {
   if (T == 0 && H > 0 && H % 8 == 0 && k >= 1 && k <= 8) return REALB_OK;
   if (!d_rows || !d_pos || !d_w || !d_y || T < 0 || H <= 0 || H % 8 || k < 1 || k > 8) {
     set_error("realb_combine: bad arguments (T=%d H=%d k=%d)", T, H, k);
@@ -567,13 +577,14 @@ extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const flo
   const dim3 grid((T + 7) / 8);
   cudaStream_t st = (cudaStream_t)stream;
   auto r = reinterpret_cast<const __nv_bfloat16*>(d_rows);
+  auto ad = reinterpret_cast<const __nv_bfloat16*>(d_addend);
   auto y = reinterpret_cast<__nv_bfloat16*>(d_y);
   switch (k) {
-    case 1: combine_kernel<1><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
-    case 2: combine_kernel<2><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
-    case 4: combine_kernel<4><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
-    case 6: combine_kernel<6><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
-    case 8: combine_kernel<8><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, y); break;
+    case 1: combine_kernel<1><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, ad, y); break;
+    case 2: combine_kernel<2><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, ad, y); break;
+    case 4: combine_kernel<4><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, ad, y); break;
+    case 6: combine_kernel<6><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, ad, y); break;
+    case 8: combine_kernel<8><<<grid, 256, 0, st>>>(r, d_pos, d_w, T, H, ad, y); break;
     default:
       set_error("realb_combine: top-k must be one of 1,2,4,6,8 (k=%d)", k);
       return REALB_EUNSUPPORTED;

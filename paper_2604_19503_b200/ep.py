@@ -252,7 +252,7 @@ class CudaEPOps:
         T = send_pos.shape[0]
         y = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.dev)
         _lib.call("realb_combine", ret_buf.data_ptr(), self.send_pos.data_ptr(), self.topk_w.data_ptr(),
-                  T, self.H, self.k, y.data_ptr(), _lib.stream_ptr())
+                  T, self.H, self.k, None, y.data_ptr(), _lib.stream_ptr())
         return y
 
 

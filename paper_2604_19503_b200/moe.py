@@ -44,6 +44,10 @@ class MoEShape:
     routed_scaling: float = 1.0
     norm_min: float = 1e-12
     modality_isolated: bool = False
+    # shared-expert MLP intermediate size (moe_intermediate x n_shared_experts; 0: none).
+    # Not part of ReaLB's policy (never quantised, not expert-parallel); computed on
+    # its own stream, overlapped with the routed path, added in the combine.
+    shared_intermediate: int = 0
 
 
 SHAPES = {
@@ -51,6 +55,10 @@ SHAPES = {
     "tiny": MoEShape("tiny-mmoe", 8, 2, 512, 1024, _lib.SCORE_SOFTMAX_RENORM),
     # Kimi-VL-A3B (DeepSeek-V3 family router: sigmoid, renorm, x routed_scaling)
     "kimi": MoEShape("kimi-vl-a3b", 64, 6, 2048, 1408, _lib.SCORE_SIGMOID_RENORM, 2.446),
+    # the same layer with Kimi-VL's 2 shared experts (DeepSeek-V3 family: one dense
+    # MLP of 2 x 1408 on every token, transformers deepseek_v3 DeepseekV3MoE)
+    "kimi_shared": MoEShape("kimi-vl-a3b+shared", 64, 6, 2048, 1408, _lib.SCORE_SIGMOID_RENORM, 2.446,
+                            shared_intermediate=2816),
     # Qwen3-VL-30B-A3B (softmax, top-k, renorm)
     "qwen": MoEShape("qwen3-vl-30b-a3b", 128, 8, 2048, 768, _lib.SCORE_SOFTMAX_RENORM),
     # ERNIE-4.5-VL-A3B modality-split MoE: vision group (ReaLB applies, isolated)
@@ -137,6 +145,8 @@ class MoEWeights:
     bias: torch.Tensor | None
     w_gu: torch.Tensor
     w_d: torch.Tensor
+    shared_gu: torch.Tensor | None = None  # bf16 [2*Is, H], 128-row gate/up interleave
+    shared_d: torch.Tensor | None = None   # bf16 [H, Is]
 
     @staticmethod
     def interleave_gate_up(gate_up_hf: torch.Tensor) -> torch.Tensor:
@@ -148,17 +158,28 @@ class MoEWeights:
         return torch.stack([g, u], dim=2).reshape(E * I2, H).contiguous()
 
     @classmethod
-    def from_hf(cls, shape: MoEShape, router, gate_up_proj, down_proj, bias=None, device="cuda"):
-        """router [E,H], gate_up_proj [E,2I,H], down_proj [E,H,I] (HF conventions)."""
+    def from_hf(cls, shape: MoEShape, router, gate_up_proj, down_proj, bias=None, device="cuda",
+                shared=None):
+        """router [E,H], gate_up_proj [E,2I,H], down_proj [E,H,I] (HF conventions);
+        shared: (gate_up [2Is,H], down [H,Is]) of the shared-expert MLP, or None."""
         E, H, I = shape.num_experts, shape.hidden, shape.intermediate
         assert tuple(gate_up_proj.shape) == (E, 2 * I, H) and tuple(down_proj.shape) == (E, H, I)
         bf = torch.bfloat16
+        sgu = sd = None
+        if shape.shared_intermediate:
+            if shared is None:
+                raise ValueError(f"{shape.name} has a shared expert: pass shared=(gate_up, down)")
+            Is = shape.shared_intermediate
+            assert tuple(shared[0].shape) == (2 * Is, H) and tuple(shared[1].shape) == (H, Is)
+            sgu = cls.interleave_gate_up(shared[0].to(device=device, dtype=bf)[None])
+            sd = shared[1].to(device=device, dtype=bf).contiguous()
         return cls(
             shape=shape,
             router=router.to(device=device, dtype=bf).contiguous(),
             bias=None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous(),
             w_gu=cls.interleave_gate_up(gate_up_proj.to(device=device, dtype=bf)),
             w_d=down_proj.to(device=device, dtype=bf).reshape(E * H, I).contiguous(),
+            shared_gu=sgu, shared_d=sd,
         )
 
 
@@ -257,6 +278,14 @@ class MoELayer:
         self.y_buf = torch.empty(T, H, dtype=bf, device=dev)
         self._fp4 = None  # lazily allocated W4A4 workspaces
         self.side = torch.cuda.Stream(device=dev, priority=0)
+        if s.shared_intermediate:
+            Is = s.shared_intermediate
+            if Is % 128:
+                raise ValueError("shared_intermediate must be a multiple of 128")
+            self.sh_h = torch.empty(T, Is, dtype=bf, device=dev)
+            self.sh_y = torch.empty(T, H, dtype=bf, device=dev)
+            self.sh_stream = torch.cuda.Stream(device=dev)
+            self._sh_layouts = {}
 
     # -- W4A4 workspaces (activations + quantised weights of every expert)
     def _fp4_ws(self):
@@ -321,6 +350,26 @@ class MoELayer:
                   int(bool(c.modality_isolated)), self.prec_dev.data_ptr(), self.plan_dev.data_ptr(),
                   self.layout.data_ptr(), self.expert_vt.data_ptr(), _lib.stream_ptr())
 
+    def _shared_layout(self, T: int) -> torch.Tensor:
+        """One dense group of T rows (cached per T; built before any graph capture,
+        capture() runs an eager forward first)."""
+        lay = self._sh_layouts.get(T)
+        if lay is None:
+            lay = torch.from_numpy(host_layout([T], [0])[0]).to(self.device)
+            self._sh_layouts[T] = lay
+        return lay
+
+    def shared_mlp(self, x: torch.Tensor, stream) -> None:
+        """The shared-expert MLP on every token (BF16 K5: SwiGLU gate_up, then down)
+        into self.sh_y, on `stream`."""
+        T, H, Is = x.shape[0], self.H, self.shape.shared_intermediate
+        lay = self._shared_layout(T)
+        sp = _lib.stream_ptr(stream)
+        _lib.call("realb_grouped_gemm_bf16", x.data_ptr(), self.w.shared_gu.data_ptr(), T, 2 * Is, H, 1,
+                  lay.data_ptr(), _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.sh_h.data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_bf16", self.sh_h.data_ptr(), self.w.shared_d.data_ptr(), T, H, Is, 1,
+                  lay.data_ptr(), _lib.PREC_W16A16, _lib.EPI_STORE, self.sh_y.data_ptr(), 0, sp)
+
     def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
                 params: RealbParams | None = None, out: torch.Tensor | None = None) -> LayerResult:
         """One MoE layer over the local tokens; stream-ordered, no host sync.
@@ -340,6 +389,12 @@ class MoELayer:
         nch = (T + 63) // 64
         main = torch.cuda.current_stream()
         sp = _lib.stream_ptr(main)
+        shared = bool(self.shape.shared_intermediate) and T > 0
+        if shared:  # overlapped with the whole routed path, joined before the combine
+            self._shared_layout(T)
+            self.sh_stream.wait_stream(main)
+            with torch.cuda.stream(self.sh_stream):
+                self.shared_mlp(x, self.sh_stream)
         self.route(x, modality)
         self.align_plan(T, strategy, params)
         # NVFP4 launches are needed unless the plan provably stays all-W16A16: the
@@ -384,8 +439,11 @@ class MoELayer:
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
         y = self.y_buf[:T] if out is None else out
+        if shared:
+            main.wait_stream(self.sh_stream)
         _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
-                  self.topk_w.data_ptr(), T, H, k, y.data_ptr(), sp)
+                  self.topk_w.data_ptr(), T, H, k, self.sh_y.data_ptr() if shared else None,
+                  y.data_ptr(), sp)
         if torch.cuda.is_current_stream_capturing():
             return LayerResult(y, self, self.plan_host, self.expert_vt_host, None, self.placement,
                                self.cluster)

@@ -150,7 +150,10 @@ class VirtualEP:
         self.layer = None
 
     def _layer_for(self, router):
-        w = MoEWeights.from_hf(self.shape, router, self.gu, self.dn, bias=self.bias)
+        from .workload import make_shared_expert
+
+        w = MoEWeights.from_hf(self.shape, router, self.gu, self.dn, bias=self.bias,
+                               shared=make_shared_expert(self.shape))
         if self.layer is None:
             self.layer = MoELayer(w, max_tokens=self.T, cluster=self.cluster)
         else:

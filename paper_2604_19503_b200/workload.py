@@ -113,6 +113,18 @@ def make_experts(shape: MoEShape, seed: int = 2024, std: float = 0.02, device="c
     return gu, dn
 
 
+def make_shared_expert(shape: MoEShape, seed: int = 2024, std: float = 0.02, device="cuda"):
+    """Random-init shared-expert MLP (HF layout): gate_up [2Is, H] (gate rows first),
+    down [H, Is], bf16 N(0, std); None when the shape has no shared expert."""
+    Is, H = shape.shared_intermediate, shape.hidden
+    if not Is:
+        return None
+    gen = torch.Generator(device=device).manual_seed(seed * 29 + 11)
+    gu = (torch.randn(2 * Is, H, generator=gen, device=device) * std).to(torch.bfloat16)
+    dn = (torch.randn(H, Is, generator=gen, device=device) * std).to(torch.bfloat16)
+    return gu, dn
+
+
 def make_batch(shape: MoEShape, spec: WorkloadSpec, device="cuda"):
     """Everything one layer invocation needs: (x bf16 [T,H], modality u8 [T],
     router bf16 [E,H], planned idx [T,k] numpy)."""

@@ -129,7 +129,7 @@ def test_combine_weighted_sum():
     pos = torch.randint(0, R, (T, k), generator=g, device="cuda", dtype=torch.int32)
     w = torch.rand(T, k, generator=g, device="cuda")
     y = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
-    _lib.call("realb_combine", rows.data_ptr(), pos.data_ptr(), w.data_ptr(), T, H, k, y.data_ptr(),
+    _lib.call("realb_combine", rows.data_ptr(), pos.data_ptr(), w.data_ptr(), T, H, k, None, y.data_ptr(),
               _lib.stream_ptr())
     ref = (w[:, :, None] * rows[pos.long()].float()).sum(1)
     assert ((y.float() - ref).abs() <= 1e-2 * ref.abs() + 1e-2).all()
@@ -360,3 +360,35 @@ def test_nonfinite_weights_raise_quantization_domain_error():
     torch.cuda.synchronize()
     with pytest.raises(QuantizationDomainError):
         layer.check_flag()
+
+
+@pytest.mark.parametrize("strategy,R", [("baseline", 1), ("fp4all", 2), ("realb", 8)])
+def test_layer_with_shared_expert_vs_oracle(strategy, R):
+    """Kimi-VL with its shared-expert MLP: computed on its own stream, overlapped
+    with the routed path and added in the combine; vs the oracle, eager and as a
+    CUDA graph."""
+    from paper_2604_19503_b200.workload import make_shared_expert
+
+    shape = small(SHAPES["kimi_shared"], 16)
+    T = 700
+    spec = WorkloadSpec(tokens=T, num_ranks=8)
+    x, mod, router, _ = make_batch(shape, spec)
+    gu, dn = make_experts(shape)
+    sh = make_shared_expert(shape)
+    w = MoEWeights.from_hf(shape, router, gu, dn, bias=torch.zeros(16, device="cuda"), shared=sh)
+    layer = MoELayer(w, max_tokens=T, cluster=ClusterConfig(R, 1, 16 // R, 1))
+    params = RealbParams(global_batch_threshold=0)
+    res = layer.forward(x, mod, strategy, params)
+    torch.cuda.synchronize()
+    prec = res.plan.expert_precision(layer.placement)
+    ref = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                            gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
+                            expert_prec=prec, routed_scaling=shape.routed_scaling,
+                            logits=layer.logits[:T].cpu().numpy(),
+                            shared=(sh[0].float().cpu().numpy(), sh[1].float().cpu().numpy()))
+    y = res.y.float().cpu().numpy()
+    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
+    assert err < 2e-2, err
+    eager = res.y.clone()
+    cap = layer.capture(x, mod, strategy, params)
+    assert torch.equal(cap.replay(), eager)
