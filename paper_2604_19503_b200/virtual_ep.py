@@ -128,6 +128,88 @@ def layer_timing(comp_ms, trans_ms, accelerated, mode: PipelineMode, disp_ms: fl
                        totals.index(lat), mode)
 
 
+def measure_ep_kernels(torch, layer, x, mod, T_local: int, recv_rows, w4a4):
+    """The EP layer's non-GEMM kernels of every virtual rank, timed on this GPU
+    (ep.CudaEPOps runs exactly these around the two all-to-alls):
+      send    router + send-side align + pack of the rank's T_local tokens
+      recv_r  regroup + row gather of the rows rank r receives (bf16 rows; K4
+              quantising gather on a W4A4 rank; packed-NVFP4 gather with fp4 dispatch)
+      back_r  index_rows of those rows for the return all-to-all
+      combine weighted combine of the rank's T_local tokens
+    -> dict of ms (recv* / back lists per rank)."""
+    from . import _lib
+
+    dev, H, E, k = layer.device, layer.H, layer.E, layer.k
+    n_max = max(1, int(max(recv_rows)))
+    u8, i32, bf = torch.uint8, torch.int32, torch.bfloat16
+    send = torch.empty(T_local * k * 2 * H, dtype=u8, device=dev)
+    pos = torch.empty(T_local, k, dtype=i32, device=dev)
+    lay1 = torch.zeros(int(_lib.load().realb_layout_words(E, (T_local + 63) // 64)), dtype=i32, device=dev)
+    vt = torch.empty(E, 2, dtype=i32, device=dev)
+    zero_prec = torch.zeros(E, dtype=u8, device=dev)
+    recv = torch.randn(n_max, H, device=dev).to(bf)
+    packed = torch.zeros(n_max, H // 2 + H // 16, dtype=u8, device=dev)
+    row_e = torch.zeros(n_max, dtype=i32, device=dev)
+    row_p = torch.arange(n_max, dtype=i32, device=dev)
+    precs = {0: torch.zeros(E, dtype=u8, device=dev), 1: torch.ones(E, dtype=u8, device=dev)}
+    a = torch.empty(n_max, H, dtype=bf, device=dev)
+    ac = torch.empty(n_max + 128, H // 2, dtype=u8, device=dev)
+    asf = torch.empty((n_max + 128) * H // 16, dtype=u8, device=dev)
+    back = torch.empty(n_max, H, dtype=bf, device=dev)
+    y = torch.empty(T_local, H, dtype=bf, device=dev)
+    fmt = np.zeros(1, np.uint8)
+    flag = layer.flag
+    xs, ms = x[:T_local], mod[:T_local]
+
+    def sender():
+        layer.route(xs, ms)
+        sp = _lib.stream_ptr()
+        _lib.call("realb_moe_align", layer.chunk_counts.data_ptr(), (T_local + 63) // 64, E,
+                  zero_prec.data_ptr(), 1, lay1.data_ptr(), vt.data_ptr(), sp)
+        _lib.call("realb_ep_pack", xs.data_ptr(), layer.topk_idx.data_ptr(), T_local, H, E, k,
+                  lay1.data_ptr(), (T_local + 63) // 64, 1, fmt.ctypes.data, np.zeros(1, np.int32).ctypes.data,
+                  np.zeros(1, np.int64).ctypes.data, pos.data_ptr(), send.data_ptr(), flag.data_ptr(), sp)
+
+    def gather(n, w4, packed_fp4):
+        sp = _lib.stream_ptr()
+        if packed_fp4:
+            return lambda: _lib.call("realb_gather_rows_nvfp4_packed", packed.data_ptr(), row_p.data_ptr(), n,
+                                     H, ac.data_ptr(), asf.data_ptr(), sp)
+        return lambda: _lib.call("realb_gather_rows", recv.data_ptr(), row_e.data_ptr(), row_p.data_ptr(), n,
+                                 H, 1, precs[int(w4)].data_ptr(), a.data_ptr(), ac.data_ptr(), asf.data_ptr(),
+                                 flag.data_ptr(), sp)
+
+    out = {"send": _median_ms(torch, sender, reps=5)}
+    out["recv_bf16"] = [_median_ms(torch, gather(int(n), False, False), reps=5) for n in recv_rows]
+    out["recv_w4a4"] = [_median_ms(torch, gather(int(n), True, False), reps=5) if w4a4[r] else 0.0
+                        for r, n in enumerate(recv_rows)]
+    out["recv_fp4_packed"] = [_median_ms(torch, gather(int(n), True, True), reps=5) if w4a4[r] else 0.0
+                              for r, n in enumerate(recv_rows)]
+    out["back"] = [_median_ms(torch, lambda n=int(n): _lib.call(
+        "realb_index_rows", layer.rows_out.data_ptr(), row_p.data_ptr(), n, H, back.data_ptr(),
+        _lib.stream_ptr()), reps=5) for n in recv_rows]
+    out["combine"] = _median_ms(torch, lambda: _lib.call(
+        "realb_combine", layer.rows_out.data_ptr(), pos.data_ptr(), layer.topk_w.data_ptr(), T_local, H, k,
+        None, y.data_ptr(), _lib.stream_ptr()), reps=5)
+    return out
+
+
+def ep_layer_timing(comp_ms, trans_ms, accelerated, mode, disp_a2a, comb_a2a, ek, recv_key_fn):
+    """LayerTiming of the EP layer per rank: schedule = router/align/pack + C1,
+    dispatch = all-to-all + the rank's receive-side gather, compute = the GEMMs,
+    combine = index_rows + return all-to-all + weighted combine."""
+    phases, totals = [], []
+    for r in range(len(comp_ms)):
+        ph = RankPhases(int((ek["send"] + ALPHA_US / 1e3) * 1e6), int(trans_ms[r] * 1e6),
+                        int((disp_a2a + recv_key_fn(r)) * 1e6), int(comp_ms[r] * 1e6),
+                        int((ek["back"][r] + comb_a2a + ek["combine"]) * 1e6))
+        phases.append(ph)
+        totals.append(ph.total(mode, accelerated[r]))
+    lat = max(totals)
+    return LayerTiming(tuple(phases), tuple(totals), lat, max(p.compute_ns for p in phases),
+                       totals.index(lat), mode)
+
+
 class VirtualEP:
     """One model shape at EP degree R emulated on cuda:0; weights built once,
     batches (vision fraction, routing skew) regenerated per report."""
@@ -198,6 +280,15 @@ class VirtualEP:
         lt_realb = layer_timing(realb_ms, transform_ms, acc, mode, disp_bf16, comb)
         lt_realb4 = layer_timing(realb_ms, transform_ms, acc, mode, disp_fp4, comb)
         lt_bf16 = layer_timing(bf16_ms, [0.0] * R, [False] * R, PipelineMode.SEQUENTIAL, disp_bf16, comb)
+        # with the EP layer's own kernels measured per rank (measure_ep_kernels)
+        recv_rows = rank_vt.sum(1)
+        ek = measure_ep_kernels(torch, layer, x, mod, self.T_local, recv_rows, acc)
+        ep_bf16 = ep_layer_timing(bf16_ms, [0.0] * R, [False] * R, PipelineMode.SEQUENTIAL, disp_bf16, comb, ek,
+                                  lambda r: ek["recv_bf16"][r])
+        ep_realb = ep_layer_timing(realb_ms, transform_ms, acc, mode, disp_bf16, comb, ek,
+                                   lambda r: ek["recv_w4a4"][r] if acc[r] else ek["recv_bf16"][r])
+        ep_realb4 = ep_layer_timing(realb_ms, transform_ms, acc, mode, disp_fp4, comb, ek,
+                                    lambda r: ek["recv_fp4_packed"][r] if acc[r] else ek["recv_bf16"][r])
         text_total = int(rank_vt[:, 1].sum())
         text_fp4 = int(sum(rank_vt[r, 1] for r in range(R) if acc[r]))
         return {
@@ -224,6 +315,16 @@ class VirtualEP:
                                        "model": f"a2a = {ALPHA_US}us + max_r max(send_r, recv_r) bytes / "
                                                 f"{NVLINK_GBPS} GB/s; RankPhases.total overlap rule"},
             "projected_full_path_speedup": lt_bf16.layer_latency_ns / lt_realb.layer_latency_ns,
+            "ep_kernels_ms": {k2: v for k2, v in ek.items()},
+            "projected_ep_layer_ms": {"bf16": ep_bf16.layer_latency_ns / 1e6,
+                                      "realb": ep_realb.layer_latency_ns / 1e6,
+                                      "realb_fp4_dispatch": ep_realb4.layer_latency_ns / 1e6,
+                                      "model": "RankPhases with the EP layer's measured kernels: schedule = "
+                                               "router/align/pack + C1 10us; dispatch = a2a model + receive "
+                                               "gather; compute = GEMMs; combine = index_rows + a2a model + "
+                                               "combine"},
+            "projected_ep_layer_speedup": ep_bf16.layer_latency_ns / ep_realb.layer_latency_ns,
+            "projected_ep_layer_speedup_fp4_dispatch": ep_bf16.layer_latency_ns / ep_realb4.layer_latency_ns,
             "projected_full_path_speedup_fp4_dispatch": lt_bf16.layer_latency_ns / lt_realb4.layer_latency_ns,
             "transform_hidden": all(t <= disp_bf16 for t in transform_ms),
         }

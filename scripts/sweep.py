@@ -47,6 +47,7 @@ def main():
                           f"w4a4={r['plan_w4a4_ranks']} compute x{r['compute_only_speedup']:.2f} "
                           f"full x{r['projected_full_path_speedup']:.2f} "
                           f"(fp4-dispatch x{r['projected_full_path_speedup_fp4_dispatch']:.2f}) "
+                          f"EP-layer x{r['projected_ep_layer_speedup']:.2f}/x{r['projected_ep_layer_speedup_fp4_dispatch']:.2f} "
                           f"text_exp={r['text_exposure']:.3f} [{time.time() - t0:.0f}s]", flush=True)
             del vep
             torch.cuda.empty_cache()
