@@ -213,6 +213,39 @@ REALB_API int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_t
                                              int H, uint8_t* d_a_codes, uint8_t* d_a_sf,
                                              void* stream);
 
+/* ------------------------------------------------------------------------ *
+ * Peer-memory EP transport (C2 / C3 without a collective library).
+ * Windows: realb_ipc_alloc cudaMallocs a zeroed device buffer and returns its
+ * 64-byte CUDA IPC handle; peers map it with realb_ipc_open (NVLink peer memory
+ * across GPUs of a node; plain device memory for processes sharing one GPU).
+ * These four are the only calls that allocate / map device memory: the
+ * communication windows (like a collective library's own buffers).
+ * realb_p2p_pack   : realb_ep_pack whose destination for peer d is the device
+ *                    address h_rank_dst[d] (in d's receive window) instead of a
+ *                    local send buffer; same row formats (bf16 / packed NVFP4).
+ * realb_p2p_return : received row i (source-major: source s owns rows
+ *                    [h_recv_prefix[s], h_recv_prefix[s+1])) copied from my
+ *                    grouped row d_row_pos[i] to h_src_dst[s] + (i - prefix[s])
+ *                    rows in source s's return window (replaces C3 + index_rows).
+ * realb_p2p_signal : after this stream's earlier writes are visible system-wide,
+ *                    atomically add 1 to each of the R peer counters.
+ * realb_p2p_wait   : stream waits until *d_counter (acquire, system scope)
+ *                    reaches target (modular uint32 compare).
+ * h_* are host arrays (read during the call); addresses 16-byte aligned.
+ * ------------------------------------------------------------------------ */
+REALB_API int realb_ipc_alloc(int64_t bytes, void** d_ptr, uint8_t* handle64);
+REALB_API int realb_ipc_open(const uint8_t* handle64, void** d_ptr);
+REALB_API int realb_ipc_close(void* d_ptr);
+REALB_API int realb_ipc_free(void* d_ptr);
+REALB_API int realb_p2p_pack(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                             const int32_t* d_layout, int nchunks, int R, const uint8_t* h_rank_fmt,
+                             const int32_t* h_rank_row0, const uint64_t* h_rank_dst,
+                             int32_t* d_pair_pos, int32_t* d_nonfinite_flag, void* stream);
+REALB_API int realb_p2p_return(const void* d_rows, const int32_t* d_row_pos, int64_t n, int H, int R,
+                               const int32_t* h_recv_prefix, const uint64_t* h_src_dst, void* stream);
+REALB_API int realb_p2p_signal(const uint64_t* h_peer_counters, int R, void* stream);
+REALB_API int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, void* stream);
+
 /* dst[i] = src[idx[i]] for bf16 rows of H (EP return path before C3). */
 REALB_API int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t n, int H,
                                void* d_dst, void* stream);

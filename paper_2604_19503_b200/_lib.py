@@ -36,7 +36,7 @@ class RealbError(RuntimeError):
         self.status = status
 
 
-_vp, _i32, _i64, _f32, _f64 = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_double
+_vp, _i32, _i64, _f32, _f64, _u32 = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_double, C.c_uint32
 
 # name -> (restype, argtypes); must list every function of include/realb.h
 SIGNATURES: dict[str, tuple] = {
@@ -63,6 +63,15 @@ SIGNATURES: dict[str, tuple] = {
     "realb_ep_pack": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp]),
     "realb_gather_rows_nvfp4_packed": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),
+    "realb_ipc_alloc": (_i32, [_i64, _vp, _vp]),
+    "realb_ipc_open": (_i32, [_vp, _vp]),
+    "realb_ipc_close": (_i32, [_vp]),
+    "realb_ipc_free": (_i32, [_vp]),
+    "realb_p2p_pack": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                              _vp]),
+    "realb_p2p_return": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "realb_p2p_signal": (_i32, [_vp, _i32, _vp]),
+    "realb_p2p_wait": (_i32, [_vp, _u32, _vp]),
 }
 
 _lib: C.CDLL | None = None
@@ -75,6 +84,7 @@ LAUNCHES_KERNEL = {
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_nvfp4": 1, "realb_combine": 1,
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
+    "realb_p2p_pack": 2, "realb_p2p_return": 1, "realb_p2p_signal": 1, "realb_p2p_wait": 1,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 

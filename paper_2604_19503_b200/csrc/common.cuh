@@ -28,6 +28,9 @@ int set_smem_once(const void* kernel, int bytes, const char* where);
 int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
                  uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
                  CUtensorMapSwizzle swz);
+// moe_ops.cu: expert-sorted (token, slot) positions over a row_align-1 layout
+int ep_positions(const int32_t* topk_idx, int T, int E, int k, const int32_t* layout, int nchunks,
+                 int32_t* pair_pos, void* stream);
 
 // ---------------------------------------------------------------- layout words
 // int32 layout workspace produced by realb_moe_align (include/realb.h).

@@ -489,6 +489,15 @@ __global__ void __launch_bounds__(256) gather_packed_fp4_kernel(const uint8_t* _
   }
 }
 
+// expert-sorted positions of every (token, slot) pair (the permute step shared by
+// dispatch, the EP pack and the peer-memory pack)
+int ep_positions(const int32_t* topk_idx, int T, int E, int k, const int32_t* layout, int nchunks,
+                 int32_t* pair_pos, void* stream) {
+  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(topk_idx, T, E, k, layout, pair_pos);
+  return check_launch("pair positions");
+}
+
 }  // namespace realb
 
 using namespace realb;

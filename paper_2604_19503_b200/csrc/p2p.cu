@@ -1,0 +1,233 @@
+// p2p.cu — peer-memory transport of the EP layer (C2 dispatch / C3 return
+// without a collective library): every rank exposes a receive window and a
+// return window (cudaMalloc'd, shared through CUDA IPC handles: NVLink peer
+// memory on a multi-GPU node, plain device memory when the processes share one
+// GPU), and the pack / return kernels write rows straight into the peers'
+// windows. Completion is signalled with system-scope counters in the
+// receiver's window and awaited by a spin kernel, all stream-ordered: no host
+// synchronisation and no NCCL call on the data path.
+//
+// Window offsets are a pure function of the [R][R] pair-count matrix every
+// rank holds after C1 (source-major receive order, expert-sorted send order),
+// so senders and receivers agree on every row's address without a handshake.
+#include <cstring>
+
+#include "common.cuh"
+#include "fp4_rule.cuh"
+
+namespace realb {
+
+constexpr int kMaxPeers = 64;
+
+struct PeerRows {
+  uint8_t* base[kMaxPeers];  // destination address of the first row bound for peer d
+  int32_t row0[kMaxPeers];   // expert-sorted send position of that first row
+  uint8_t fmt[kMaxPeers];    // 0 bf16 rows (2H bytes), 1 packed NVFP4 rows (H/2 + H/16)
+  int R, El;
+};
+
+// one warp per (token, slot) pair: the row goes to peer d = e / El at
+// base[d] + (pos - row0[d]) * row_bytes(fmt[d])
+__global__ void __launch_bounds__(256) p2p_pack_kernel(const __nv_bfloat16* __restrict__ x,
+                                                       const int32_t* __restrict__ topk_idx,
+                                                       const int32_t* __restrict__ pair_pos, int64_t P,
+                                                       int H, int k, const PeerRows m, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int nkb = H / 16;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = p / k;
+    const int d = topk_idx[p] / m.El;
+    const int64_t rel = (int64_t)pair_pos[p] - m.row0[d];
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+    if (m.fmt[d] == 0) {
+      uint4* o = reinterpret_cast<uint4*>(m.base[d] + rel * (2 * (int64_t)H));
+      for (int i = lane; i < H / 8; i += 32) o[i] = __ldg(src + i);
+    } else {
+      uint8_t* row = m.base[d] + rel * (int64_t)(H / 2 + H / 16);
+      for (int g = lane; g < nkb / 4; g += 32) {
+        uint32_t sfw = 0;
+        uint2 cw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint4 u0 = __ldg(src + (g * 4 + b) * 2), u1 = __ldg(src + (g * 4 + b) * 2 + 1);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          uint32_t sb;
+          bool nf;
+          cw[b] = quant_block16_bf16(w, sb, nf);
+          if (nf && flag) atomicOr(flag, 1);
+          sfw |= sb << (8 * b);
+        }
+        uint4* cdst = reinterpret_cast<uint4*>(row + g * 32);
+        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
+        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
+        reinterpret_cast<uint32_t*>(row + H / 2)[g] = sfw;
+      }
+    }
+  }
+}
+
+struct PeerReturn {
+  __nv_bfloat16* base[kMaxPeers];  // peer s's return window + its first row's offset
+  int32_t recv0[kMaxPeers + 1];    // source-major prefix of my received rows
+  int R;
+};
+
+// received row i (from source s, its j-th) goes back to s's return window at
+// row j of the block s expects from me; its data is my grouped row row_pos[i]
+__global__ void __launch_bounds__(256) p2p_return_kernel(const __nv_bfloat16* __restrict__ rows,
+                                                         const int32_t* __restrict__ row_pos, int64_t n,
+                                                         int H, const PeerReturn m) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int s = 0;
+    while (s + 1 < m.R && m.recv0[s + 1] <= i) ++s;
+    const uint4* src = reinterpret_cast<const uint4*>(rows + (int64_t)row_pos[i] * H);
+    uint4* dst = reinterpret_cast<uint4*>(m.base[s] + (i - m.recv0[s]) * (int64_t)H);
+    for (int c = lane; c < H / 8; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+struct PeerCounters {
+  uint32_t* ctr[kMaxPeers];
+  int R;
+};
+
+// release: this stream's earlier writes (the pack / return kernels) become
+// visible system-wide before each peer's counter is bumped
+__global__ void p2p_signal_kernel(const PeerCounters m) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int d = 0; d < m.R; ++d) atomicAdd_system(m.ctr[d], 1u);
+  }
+}
+
+// acquire: spin until my counter reaches `target` (all peers have signalled)
+__global__ void p2p_wait_kernel(const uint32_t* ctr, uint32_t target) {
+  if (threadIdx.x == 0) {
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if ((int32_t)(v - target) >= 0) break;
+      __nanosleep(256);
+    }
+    __threadfence_system();
+  }
+}
+
+}  // namespace realb
+
+using namespace realb;
+
+extern "C" int realb_ipc_alloc(int64_t bytes, void** d_ptr, uint8_t* handle) {
+  if (bytes <= 0 || !d_ptr || !handle) {
+    set_error("realb_ipc_alloc: bad arguments");
+    return REALB_EINVAL;
+  }
+  int rc = cuda_status(cudaMalloc(d_ptr, (size_t)bytes), "realb_ipc_alloc (cudaMalloc)");
+  if (rc) return rc;
+  rc = cuda_status(cudaMemset(*d_ptr, 0, (size_t)bytes), "realb_ipc_alloc (memset)");
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  rc = cuda_status(cudaIpcGetMemHandle(&h, *d_ptr), "realb_ipc_alloc (cudaIpcGetMemHandle)");
+  if (rc) return rc;
+  memcpy(handle, &h, sizeof(h));
+  return REALB_OK;
+}
+
+extern "C" int realb_ipc_open(const uint8_t* handle, void** d_ptr) {
+  if (!handle || !d_ptr) {
+    set_error("realb_ipc_open: bad arguments");
+    return REALB_EINVAL;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                     "realb_ipc_open (cudaIpcOpenMemHandle)");
+}
+
+extern "C" int realb_ipc_close(void* d_ptr) {
+  return cuda_status(cudaIpcCloseMemHandle(d_ptr), "realb_ipc_close");
+}
+
+extern "C" int realb_ipc_free(void* d_ptr) { return cuda_status(cudaFree(d_ptr), "realb_ipc_free"); }
+
+extern "C" int realb_p2p_pack(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                              const int32_t* d_layout, int nchunks, int R, const uint8_t* h_rank_fmt,
+                              const int32_t* h_rank_row0, const uint64_t* h_rank_dst, int32_t* d_pair_pos,
+                              int32_t* d_flag, void* stream) {
+  if (T == 0 && nchunks == 0) return REALB_OK;
+  if (!d_x || !d_topk_idx || !d_layout || !d_pair_pos || !h_rank_fmt || !h_rank_row0 || !h_rank_dst ||
+      T < 0 || H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || R < 1 || R > kMaxPeers ||
+      E % R || nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
+    set_error("realb_p2p_pack: bad arguments (T=%d H=%d E=%d k=%d R=%d)", T, H, E, k, R);
+    return REALB_EINVAL;
+  }
+  PeerRows m{};
+  m.R = R;
+  m.El = E / R;
+  for (int d = 0; d < R; ++d) {
+    if (h_rank_fmt[d] > 1 || (h_rank_dst[d] & 15)) {
+      set_error("realb_p2p_pack: peer %d: format must be 0/1 and addresses 16-byte aligned", d);
+      return REALB_EINVAL;
+    }
+    m.base[d] = reinterpret_cast<uint8_t*>(h_rank_dst[d]);
+    m.row0[d] = h_rank_row0[d];
+    m.fmt[d] = h_rank_fmt[d];
+  }
+  int rc = ep_positions(d_topk_idx, T, E, k, d_layout, nchunks, d_pair_pos, stream);
+  if (rc) return rc;
+  const int64_t P = (int64_t)T * k;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  p2p_pack_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, m, d_flag);
+  return check_launch("realb_p2p_pack (rows)");
+}
+
+extern "C" int realb_p2p_return(const void* d_rows, const int32_t* d_row_pos, int64_t n, int H, int R,
+                                const int32_t* h_recv_prefix, const uint64_t* h_src_dst, void* stream) {
+  if (n < 0 || H <= 0 || H % 8 || R < 1 || R > kMaxPeers || !h_recv_prefix || !h_src_dst ||
+      (n > 0 && (!d_rows || !d_row_pos))) {
+    set_error("realb_p2p_return: bad arguments (n=%lld H=%d R=%d)", (long long)n, H, R);
+    return REALB_EINVAL;
+  }
+  if (n == 0) return REALB_OK;
+  PeerReturn m{};
+  m.R = R;
+  for (int s = 0; s < R; ++s) {
+    if (h_src_dst[s] & 15) {
+      set_error("realb_p2p_return: peer %d address not 16-byte aligned", s);
+      return REALB_EINVAL;
+    }
+    m.base[s] = reinterpret_cast<__nv_bfloat16*>(h_src_dst[s]);
+  }
+  for (int s = 0; s <= R; ++s) m.recv0[s] = h_recv_prefix[s];
+  int64_t grid = (n + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  p2p_return_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_rows), d_row_pos, n, H, m);
+  return check_launch("realb_p2p_return");
+}
+
+extern "C" int realb_p2p_signal(const uint64_t* h_peer_counters, int R, void* stream) {
+  if (!h_peer_counters || R < 1 || R > kMaxPeers) {
+    set_error("realb_p2p_signal: bad arguments (R=%d)", R);
+    return REALB_EINVAL;
+  }
+  PeerCounters m{};
+  m.R = R;
+  for (int d = 0; d < R; ++d) m.ctr[d] = reinterpret_cast<uint32_t*>(h_peer_counters[d]);
+  p2p_signal_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(m);
+  return check_launch("realb_p2p_signal");
+}
+
+extern "C" int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, void* stream) {
+  if (!d_counter) {
+    set_error("realb_p2p_wait: bad arguments");
+    return REALB_EINVAL;
+  }
+  p2p_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_counter, target);
+  return check_launch("realb_p2p_wait");
+}

@@ -44,11 +44,14 @@ class EPComm:
     """Collectives of the EP layer. ``staged`` copies device tensors through the
     host (gloo on a shared GPU / CPU tests); otherwise tensors go to NCCL as-is."""
 
-    def __init__(self, group=None, staged: bool = False):
+    def __init__(self, group=None, staged: bool = False, p2p: bool = False):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.staged = staged
+        # p2p: C2/C3 move rows through peer-memory windows (CudaEPOps.setup_p2p);
+        # the process group then only carries the C1 count exchange
+        self.p2p = p2p
 
     def all_gather_counts(self, vt_local: torch.Tensor) -> np.ndarray:
         """[E,2] int32 per rank -> host numpy [R,E,2] (the layer's one sync)."""
@@ -181,9 +184,13 @@ class CudaEPOps:
         return self.recv_buf
 
     # regroup received rows + local expert MLPs
-    def expert_compute(self, recv_buf, cnt: np.ndarray, w4a4: bool, packed_fp4: bool = False):
+    def expert_compute(self, recv_buf, cnt: np.ndarray, w4a4: bool, packed_fp4: bool = False,
+                       return_rows: bool = True):
+        """Regroup + gather the received rows (``recv_buf``: tensor or device address),
+        the local expert MLPs, and (return_rows) the copy back into receive order."""
         El, H, I = self.El, self.H, self.I
         n = int(cnt.sum())
+        recv_ptr = recv_buf if isinstance(recv_buf, int) else recv_buf.data_ptr()
         sp = _lib.stream_ptr()
         self.cnt_host.numpy()[:] = cnt
         self.cnt_dev.copy_(self.cnt_host, non_blocking=True)
@@ -193,10 +200,10 @@ class CudaEPOps:
                   self.row_pos.data_ptr(), sp)
         ws = self._fp4_ws() if w4a4 else None
         if packed_fp4:  # rows arrived as NVFP4 (sender-side K4): byte movement only
-            _lib.call("realb_gather_rows_nvfp4_packed", recv_buf.data_ptr(), self.row_pos.data_ptr(), n, H,
+            _lib.call("realb_gather_rows_nvfp4_packed", recv_ptr, self.row_pos.data_ptr(), n, H,
                       ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(), sp)
         else:
-            _lib.call("realb_gather_rows", recv_buf.data_ptr(), self.row_expert.data_ptr(), self.row_pos.data_ptr(),
+            _lib.call("realb_gather_rows", recv_ptr, self.row_expert.data_ptr(), self.row_pos.data_ptr(),
                       n, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(),
                       _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
                       self.flag.data_ptr(), sp)
@@ -216,9 +223,90 @@ class CudaEPOps:
             _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+        if not return_rows:
+            return None
         _lib.call("realb_index_rows", self.rows_out.data_ptr(), self.row_pos.data_ptr(), n, H,
                   self.back_buf.data_ptr(), sp)
         return self.back_buf
+
+    # ------------------------------------------------------------ peer-memory transport
+    def setup_p2p(self, comm: "EPComm"):
+        """Receive / return windows (CUDA IPC, realb_ipc_alloc) plus two uint32
+        counters (dispatch, return) per rank; handles exchanged once over the
+        process group; peers' windows mapped (NVLink peer memory across GPUs)."""
+        import ctypes as Cty
+
+        R, H, T, k = self.R, self.H, self.T, self.k
+        sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256}
+        self._p2p_own, handles = {}, {}
+        for name, nbytes in sizes.items():
+            ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
+            _lib.call("realb_ipc_alloc", nbytes, Cty.byref(ptr), h)
+            self._p2p_own[name] = ptr.value
+            handles[name] = bytes(h)
+        allh = [None] * R
+        dist.all_gather_object(allh, handles, group=comm.group)
+        self.p2p = {name: [0] * R for name in sizes}
+        self._p2p_opened = []
+        for r in range(R):
+            for name in sizes:
+                if r == comm.rank:
+                    self.p2p[name][r] = self._p2p_own[name]
+                else:
+                    ptr = Cty.c_void_p()
+                    _lib.call("realb_ipc_open", allh[r][name], Cty.byref(ptr))
+                    self.p2p[name][r] = ptr.value
+                    self._p2p_opened.append(ptr.value)
+        self.p2p_epoch = 0
+        dist.barrier(group=comm.group)
+
+    def p2p_dispatch(self, x, topk_idx, fp4_rows, pairs: np.ndarray, rank: int):
+        """C2 over peer memory: rows written straight into every destination's
+        receive window (source-major, at offsets derived from the [R][R] pair
+        counts), then a system-scope signal per destination and a wait for all
+        sources. pairs[s][d]: (token, expert) pairs rank s sends to rank d."""
+        T, H, R = x.shape[0], self.H, self.R
+        units = np.array([H // 2 + H // 16 if f else 2 * H for f in fp4_rows], np.int64)
+        row0 = np.concatenate([[0], np.cumsum(pairs[rank])[:-1]]).astype(np.int32)
+        recv_off = np.cumsum(pairs, axis=0) - pairs                     # [s][d] rows before source s at d
+        dst = np.array([self.p2p["recv"][d] + int(recv_off[rank, d]) * int(units[d]) for d in range(R)],
+                       np.uint64)
+        fmt = np.array(fp4_rows, np.uint8)
+        sp = _lib.stream_ptr()
+        _lib.call("realb_p2p_pack", x.data_ptr(), self.topk_idx.data_ptr(), T, H, self.E, self.k,
+                  self.send_layout.data_ptr(), (T + 63) // 64, R, fmt.ctypes.data, row0.ctypes.data,
+                  dst.ctypes.data, self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
+        self.p2p_epoch += 1
+        self._p2p_signal_wait(0)
+        return self.p2p["recv"][rank], self.send_pos[:T]
+
+    def p2p_return(self, cnt: np.ndarray, pairs: np.ndarray, rank: int):
+        """C3 over peer memory: every received row goes from my grouped output
+        straight into its source's return window, in the source's send order."""
+        R, H = self.R, self.H
+        n = int(cnt.sum())
+        recv_prefix = np.concatenate([[0], np.cumsum(cnt.sum(axis=1))]).astype(np.int32)
+        send_row0 = np.cumsum(pairs, axis=1) - pairs                    # [s][d] rows s sends before d
+        dst = np.array([self.p2p["ret"][s_] + int(send_row0[s_, rank]) * 2 * H for s_ in range(R)], np.uint64)
+        _lib.call("realb_p2p_return", self.rows_out.data_ptr(), self.row_pos.data_ptr(), n, H, R,
+                  recv_prefix.ctypes.data, dst.ctypes.data, _lib.stream_ptr())
+        self._p2p_signal_wait(4)
+        return self.p2p["ret"][rank]
+
+    def _p2p_signal_wait(self, ctr_off: int):
+        R = self.R
+        ctrs = np.array([self.p2p["ctr"][d] + ctr_off for d in range(R)], np.uint64)
+        sp = _lib.stream_ptr()
+        _lib.call("realb_p2p_signal", ctrs.ctypes.data, R, sp)
+        _lib.call("realb_p2p_wait", self._p2p_own["ctr"] + ctr_off, (self.p2p_epoch * R) & 0xFFFFFFFF, sp)
+
+    def close_p2p(self):
+        torch.cuda.synchronize()
+        for p in getattr(self, "_p2p_opened", []):
+            _lib.call("realb_ipc_close", p)
+        for p in getattr(self, "_p2p_own", {}).values():
+            _lib.call("realb_ipc_free", p)
+        self._p2p_opened, self._p2p_own = [], {}
 
     def ret_buffer(self):
         return self.ret_buf
@@ -251,7 +339,8 @@ class CudaEPOps:
     def combine(self, ret_buf, send_pos, topk_w):
         T = send_pos.shape[0]
         y = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.dev)
-        _lib.call("realb_combine", ret_buf.data_ptr(), self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+        ret_ptr = ret_buf if isinstance(ret_buf, int) else ret_buf.data_ptr()
+        _lib.call("realb_combine", ret_ptr, self.send_pos.data_ptr(), self.topk_w.data_ptr(),
                   T, self.H, self.k, None, y.data_ptr(), _lib.stream_ptr())
         return y
 
@@ -290,13 +379,21 @@ class EPMoELayer:
         mark("schedule")
         if w4a4:
             self.ops.quantize_local_weights_async(timer)                     # K3 under C2
-        send_buf, send_pos, units = self.ops.pack(x, topk_idx, fp4_rows, send_counts)
-        recv_buf = self.comm.all_to_all_rows(self.ops.recv_buffer(), send_buf, recv_counts * units[r],
-                                             send_counts * units)            # C2
-        mark("dispatch")
-        back = self.ops.expert_compute(recv_buf, cnt, w4a4, fp4_rows[r])
-        mark("compute")
-        ret = self.comm.all_to_all_rows(self.ops.ret_buffer(), back, send_counts, recv_counts)  # C3
+        if self.comm.p2p:  # C2 / C3 through peer-memory windows (no collective on the data path)
+            pairs = vt_all.sum(axis=2).reshape(R, R, El).sum(axis=2)         # [s][d] pairs s -> d
+            recv_buf, send_pos = self.ops.p2p_dispatch(x, topk_idx, fp4_rows, pairs, r)
+            mark("dispatch")
+            self.ops.expert_compute(recv_buf, cnt, w4a4, fp4_rows[r], return_rows=False)
+            mark("compute")
+            ret = self.ops.p2p_return(cnt, pairs, r)
+        else:
+            send_buf, send_pos, units = self.ops.pack(x, topk_idx, fp4_rows, send_counts)
+            recv_buf = self.comm.all_to_all_rows(self.ops.recv_buffer(), send_buf, recv_counts * units[r],
+                                                 send_counts * units)        # C2
+            mark("dispatch")
+            back = self.ops.expert_compute(recv_buf, cnt, w4a4, fp4_rows[r])
+            mark("compute")
+            ret = self.comm.all_to_all_rows(self.ops.ret_buffer(), back, send_counts, recv_counts)  # C3
         y = self.ops.combine(ret, send_pos, topk_w)
         mark("combine")
         return y, plan, vt_all
@@ -357,9 +454,13 @@ def run_bench(args):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
-    # REALB_EP_COMM=gloo: validation mode for a one-GPU box (all ranks share cuda:0,
-    # collectives staged through the host); the default is NCCL, one GPU per rank.
-    staged = os.environ.get("REALB_EP_COMM", "nccl") == "gloo"
+    # REALB_EP_COMM: "nccl" (default: NCCL all-to-alls, one GPU per rank); "p2p" (C2/C3
+    # through CUDA-IPC peer-memory windows, NCCL only for the C1 counts); "gloo" /
+    # "p2p-gloo": validation modes for a one-GPU box (all ranks share cuda:0, C1
+    # (and C2/C3 for "gloo") staged through the host).
+    mode = os.environ.get("REALB_EP_COMM", "nccl")
+    staged = mode in ("gloo", "p2p-gloo")
+    p2p = mode in ("p2p", "p2p-gloo")
     if staged:
         torch.cuda.set_device(0)
         dist.init_process_group("gloo")
@@ -374,8 +475,10 @@ def run_bench(args):
     bias = torch.zeros(shape.num_experts, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
     local = split_weights(shape, router, gu, dn, rank, world)
     del gu, dn
-    comm = EPComm(staged=staged)
+    comm = EPComm(staged=staged, p2p=p2p)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
+    if p2p:
+        ops.setup_p2p(comm)
     fp4_dispatch = not getattr(args, "bf16_dispatch", False)
     layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
     dev_t = "cpu" if staged else "cuda"
@@ -473,6 +576,11 @@ def run_bench(args):
                "rank_phases_ns": {s: [dict(zip(names, r)) for r in rows] for s, rows in phases.items()},
                "gpu_launches": int(launches),
                "clocks": clk.summary(),
-               "comm": "gloo-staged on one shared GPU (validation only)" if staged else "nccl"}
+               "comm": {"nccl": "nccl", "p2p": "peer-memory windows (CUDA IPC / NVLink), NCCL for C1",
+                        "gloo": "gloo-staged on one shared GPU (validation only)",
+                        "p2p-gloo": "peer-memory windows on one shared GPU, gloo for C1 (validation only)"}[mode]}
         print(json.dumps(out), flush=True)
+    if p2p:
+        dist.barrier()
+        ops.close_p2p()
     dist.destroy_process_group()

@@ -36,7 +36,7 @@ def _setup(shape_name, E, T, world, rank, device="cuda"):
     return shape, x, mod, router, gu, dn
 
 
-def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir):
+def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir, p2p=False):
     import sys
     from pathlib import Path
 
@@ -53,9 +53,17 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir)
     bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
     local = split_weights(shape, router, gu, dn, rank, world)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
-    layer = EPMoELayer(shape, EPComm(staged=True), ops, fp4_dispatch=fp4_dispatch)
+    comm = EPComm(staged=True, p2p=p2p)
+    if p2p:
+        ops.setup_p2p(comm)
+    layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
     y, plan, vt = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+    if p2p:  # a second layer call exercises window reuse and the epoch counters
+        y, plan, vt = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
     torch.cuda.synchronize()
+    if p2p:
+        dist.barrier()
+        ops.close_p2p()
     np.savez(os.path.join(outdir, f"r{rank}.npz"), y=y.float().cpu().numpy(),
              acc=np.array(sorted(plan.accelerated_ranks), dtype=np.int64))
     dist.destroy_process_group()
@@ -68,8 +76,21 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir)
     # the same codes it would compute itself, so the layer output is unchanged
     ("kimi", 16, 384, "realb", True), ("qwen", 16, 256, "fp4all", True), ("tiny", 8, 512, "realb", True)])
 def test_ep2_on_one_gpu_equals_single_gpu_layer(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
+    _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=False)
+
+
+@pytest.mark.parametrize("shape_name,E,T,strategy,fp4_dispatch", [
+    ("kimi", 16, 384, "realb", True), ("qwen", 16, 256, "fp4all", False), ("tiny", 8, 512, "baseline", False)])
+def test_ep2_peer_memory_transport_equals_single_gpu_layer(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
+    """C2/C3 through CUDA-IPC peer-memory windows (realb_p2p_*: rows written into
+    the peers' windows, system-scope counters, no collective on the data path);
+    the two processes share one GPU, as NVLink peers would share windows."""
+    _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=True)
+
+
+def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path)),
+    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path), p2p),
              nprocs=world)
     from paper_2604_19503_b200 import _lib
     from paper_2604_19503_b200.moe import MoELayer, MoEWeights
