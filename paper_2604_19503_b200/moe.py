@@ -371,7 +371,8 @@ class MoELayer:
                   lay.data_ptr(), _lib.PREC_W16A16, _lib.EPI_STORE, self.sh_y.data_ptr(), 0, sp)
 
     def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
-                params: RealbParams | None = None, out: torch.Tensor | None = None) -> LayerResult:
+                params: RealbParams | None = None, out: torch.Tensor | None = None,
+                timer=None) -> LayerResult:
         """One MoE layer over the local tokens; stream-ordered, no host sync.
 
         strategy "baseline" (and the EPLB tags) runs the all-BF16 comparator with
@@ -404,30 +405,37 @@ class MoELayer:
         code = _STRATEGY_CODE[strategy]
         mixed = code == 1 or (code == 2 and not (self.cluster.num_ranks == 1
                                                  and params.capacity_factor >= 1.0))
+        mark = timer.mark if timer is not None else (lambda *a, **kw: None)
         if mixed:
             ws = self._fp4_ws()
             self.side.wait_stream(main)
             with torch.cuda.stream(self.side):
                 ssp = _lib.stream_ptr(self.side)
+                mark("k3_start", self.side)
                 _lib.call("realb_quantize_experts_nvfp4", self.w.w_gu.data_ptr(), E, 2 * I, H,
                           self.prec_dev.data_ptr(), ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
                           self.flag.data_ptr(), self.quant_max_ctas, ssp)
                 _lib.call("realb_quantize_experts_nvfp4", self.w.w_d.data_ptr(), E, H, I,
                           self.prec_dev.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
                           self.flag.data_ptr(), self.quant_max_ctas, ssp)
+                mark("k3_end", self.side)
         else:
             ws = None
+        mark("dispatch_start", main)
         _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
                   self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
                   self.pair_pos.data_ptr(), self.a_bf16.data_ptr(),
                   _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
                   self.flag.data_ptr(), sp)
+        mark("dispatch_end", main)
         lay = self.layout.data_ptr()
         _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
                   self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
                   self.h_bf16.data_ptr(), 0, sp)
         if ws is not None:
+            mark("fp4_ready", main)  # main stream reaches the first W4A4 GEMM
             main.wait_stream(self.side)
+            mark("fp4_start", main)
             _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
                       ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, E,
                       lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)

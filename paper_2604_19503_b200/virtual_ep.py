@@ -128,6 +128,39 @@ def layer_timing(comp_ms, trans_ms, accelerated, mode: PipelineMode, disp_ms: fl
                        totals.index(lat), mode)
 
 
+class EventMarks:
+    """Named CUDA events recorded on given streams (MoELayer.forward(timer=...))."""
+
+    def __init__(self, torch):
+        self.torch, self.ev = torch, {}
+
+    def mark(self, name, stream=None):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        self.ev[name] = e
+
+    def ms(self, a, b):
+        return self.ev[a].elapsed_time(self.ev[b])
+
+
+def measure_k3_overlap(torch, layer, x, mod, params) -> dict:
+    """Timeline of one realb forward on this GPU: K3 on the side stream vs the main
+    stream's dispatch and BF16 GEMMs, up to the first W4A4 GEMM that needs K3's
+    output. stall_ms > 0 would mean the quantiser was NOT hidden."""
+    tm = EventMarks(torch)
+    layer.forward(x, mod, "realb", params, timer=tm)
+    torch.cuda.synchronize()
+    if "k3_start" not in tm.ev:
+        return {"skipped": "no W4A4 launches for this plan"}
+    return {"k3_ms": tm.ms("k3_start", "k3_end"),
+            "dispatch_ms": tm.ms("dispatch_start", "dispatch_end"),
+            "main_work_before_first_w4a4_gemm_ms": tm.ms("dispatch_start", "fp4_ready"),
+            "stall_ms": max(0.0, tm.ms("fp4_ready", "fp4_start")),
+            "k3_hidden": tm.ms("k3_end", "fp4_ready") >= 0.0,
+            "what": "one-GPU forward of the EP global batch: K3 (side stream) runs under the main "
+                    "stream's dispatch and W16A16 GEMMs; stall = wait of the first W4A4 GEMM on K3"}
+
+
 def measure_ep_kernels(torch, layer, x, mod, T_local: int, recv_rows, w4a4):
     """The EP layer's non-GEMM kernels of every virtual rank, timed on this GPU
     (ep.CudaEPOps runs exactly these around the two all-to-alls):
@@ -269,6 +302,7 @@ class VirtualEP:
         bf16_ms, realb_ms = measure_rank_compute(torch, layer, T, [np.zeros(E, np.int64), prec], R, epr)
         transform_ms = measure_transform(torch, layer, prec, R, epr)
         whole_realb = _median_ms(torch, lambda: layer.forward(x, mod, "realb", params), reps=5)
+        k3_timeline = measure_k3_overlap(torch, layer, x, mod, params)
         whole_bf16 = _median_ms(torch, lambda: layer.forward(x, mod, "baseline"), reps=5)
 
         # projected full path: engine.py:120-159 overlap rule, measured compute/transform
@@ -327,6 +361,7 @@ class VirtualEP:
             "projected_ep_layer_speedup_fp4_dispatch": ep_bf16.layer_latency_ns / ep_realb4.layer_latency_ns,
             "projected_full_path_speedup_fp4_dispatch": lt_bf16.layer_latency_ns / lt_realb4.layer_latency_ns,
             "transform_hidden": all(t <= disp_bf16 for t in transform_ms),
+            "k3_overlap_one_gpu": k3_timeline,
         }
 
 
