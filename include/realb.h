@@ -176,12 +176,16 @@ REALB_API int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx,
 REALB_API int realb_gather_rows(const void* d_x, const int32_t* d_expert, const int32_t* d_pos,
                                 int64_t P, int H, int k, const uint8_t* d_prec, void* d_a_bf16,
                                 uint8_t* d_a_codes, uint8_t* d_a_sf, int32_t* d_nonfinite_flag,
-                                void* stream);
+                                const int32_t* d_count, const int32_t* d_gate, void* stream);
+/* d_count (nullable): device row count; P is then an upper bound (capacity launch).
+ * d_gate (nullable): the kernel does nothing when *d_gate == 0 (a device-side
+ * choice between this gather and realb_gather_rows_nvfp4_packed). */
 
 /* EP receive side (C2): rows arrive source-major, per source ordered by local
  * expert (senders pack by global expert id). From the [R][El] count matrix
  * build the local grouped layout (as realb_moe_align, El experts) and, for
  * every received row, its local expert and grouped position.
+ *   n_recv : received rows, or an upper bound (the true count comes from d_cnt)
  *   d_base : int32 workspace [2*R*El + 2] */
 REALB_API int realb_ep_regroup(const int32_t* d_cnt, int R, int El, const uint8_t* d_prec_local,
                                int64_t n_recv, int32_t* d_layout, int32_t* d_base,
@@ -211,6 +215,7 @@ REALB_API int realb_ep_pack(const void* d_x, const int32_t* d_topk_idx, int T, i
  * scales into the REALB_SF_MMA128x4 layout of d_a_sf. H % 256 == 0. */
 REALB_API int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_t* d_pos, int64_t n,
                                              int H, uint8_t* d_a_codes, uint8_t* d_a_sf,
+                                             const int32_t* d_count, const int32_t* d_gate,
                                              void* stream);
 
 /* ------------------------------------------------------------------------ *
@@ -245,6 +250,37 @@ REALB_API int realb_p2p_return(const void* d_rows, const int32_t* d_row_pos, int
                                const int32_t* h_recv_prefix, const uint64_t* h_src_dst, void* stream);
 REALB_API int realb_p2p_signal(const uint64_t* h_peer_counters, int R, void* stream);
 REALB_API int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, void* stream);
+
+/* Host-sync-free form (the EP layer becomes CUDA-graph capturable):
+ * realb_p2p_publish      : copy n_words int32 (my [E][2] counts) into every peer
+ *                          window h_peer_windows[d] at word offset offset_words (C1).
+ * realb_p2p_plan_offsets : from the gathered counts [R][E][2] and the device plan's
+ *                          expert precisions, write the P2P plan record (d_plan,
+ *                          realb_p2p_plan_bytes() bytes: per-peer send offsets and
+ *                          row formats, receive prefix, return offsets, my received
+ *                          row count and gather gates), my [R][El] receive counts
+ *                          and my experts' precisions.
+ * realb_p2p_pack_dev / realb_p2p_return_dev : realb_p2p_pack / realb_p2p_return
+ *                          with every offset, format and count read from d_plan;
+ *                          h_peer_recv / h_peer_ret are the peers' window bases. */
+REALB_API int64_t realb_p2p_plan_bytes(void);
+/* [size, offsetof(n_recv), offsetof(w4a4), offsetof(gate_bf16), offsetof(gate_packed)] of the
+ * plan record, so callers can point realb_gather_rows' d_count / d_gate into it. */
+REALB_API int realb_p2p_plan_layout(int64_t* out5);
+/* graph-safe wait: *d_expected += inc, then wait until *d_counter reaches it */
+REALB_API int realb_p2p_wait_next(uint32_t* d_expected, uint32_t inc, const uint32_t* d_counter,
+                                  void* stream);
+REALB_API int realb_p2p_publish(const int32_t* d_src, int n_words, int R, const uint64_t* h_peer_windows,
+                                int64_t offset_words, void* stream);
+REALB_API int realb_p2p_plan_offsets(const int32_t* d_counts, int R, int E, int rank, int H,
+                                     int fp4_dispatch, const uint8_t* d_prec, void* d_plan,
+                                     int32_t* d_cnt_local, uint8_t* d_prec_local, void* stream);
+REALB_API int realb_p2p_pack_dev(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                                 const int32_t* d_layout, int nchunks, int R,
+                                 const uint64_t* h_peer_recv, const void* d_plan, int32_t* d_pair_pos,
+                                 int32_t* d_nonfinite_flag, void* stream);
+REALB_API int realb_p2p_return_dev(const void* d_rows, const int32_t* d_row_pos, int64_t n_cap, int H,
+                                   int R, const uint64_t* h_peer_ret, const void* d_plan, void* stream);
 
 /* dst[i] = src[idx[i]] for bf16 rows of H (EP return path before C3). */
 REALB_API int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t n, int H,

@@ -50,7 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "realb_moe_align_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _f64, _f64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_quantize_experts_nvfp4": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
     "realb_moe_align": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
-    "realb_gather_rows": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "realb_gather_rows": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "realb_ep_regroup": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "realb_index_rows": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "realb_dispatch_permute": (
@@ -62,7 +62,14 @@ SIGNATURES: dict[str, tuple] = {
     "realb_plan": (_i32, [_vp, _i32, _f64, _f64, _i64, _i32, _vp, _vp]),
     "realb_ep_pack": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp]),
-    "realb_gather_rows_nvfp4_packed": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),
+    "realb_gather_rows_nvfp4_packed": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "realb_p2p_plan_bytes": (_i64, []),
+    "realb_p2p_plan_layout": (_i32, [_vp]),
+    "realb_p2p_wait_next": (_i32, [_vp, _u32, _vp, _vp]),
+    "realb_p2p_publish": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp]),
+    "realb_p2p_plan_offsets": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "realb_p2p_pack_dev": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "realb_p2p_return_dev": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "realb_ipc_alloc": (_i32, [_i64, _vp, _vp]),
     "realb_ipc_open": (_i32, [_vp, _vp]),
     "realb_ipc_close": (_i32, [_vp]),
@@ -85,6 +92,8 @@ LAUNCHES_KERNEL = {
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
     "realb_p2p_pack": 2, "realb_p2p_return": 1, "realb_p2p_signal": 1, "realb_p2p_wait": 1,
+    "realb_p2p_publish": 1, "realb_p2p_plan_offsets": 1, "realb_p2p_pack_dev": 2, "realb_p2p_return_dev": 1,
+    "realb_p2p_wait_next": 1,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 

@@ -232,7 +232,10 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
     const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ topk_idx,
     const int32_t* __restrict__ pair_pos, int64_t P, int H, int k,
     const uint8_t* __restrict__ prec, __nv_bfloat16* __restrict__ a_bf16,
-    uint8_t* __restrict__ a_codes, uint8_t* __restrict__ a_sf, int32_t* flag) {
+    uint8_t* __restrict__ a_codes, uint8_t* __restrict__ a_sf, int32_t* flag,
+    const int32_t* __restrict__ d_count, const int32_t* __restrict__ d_gate) {
+  if (d_gate && *d_gate == 0) return;
+  if (d_count && (int64_t)*d_count < P) P = *d_count;  // device-side row count (capacity launch)
   const int lane = threadIdx.x & 31;
   const int nkb = H / 16;
   for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(256) ep_rows_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ row_pos) {
   const int F = R * El;
   const int32_t* pre = base + F + 1;  // [F+1] source-major prefix
+  if ((int64_t)pre[F] < n) n = pre[F];  // n may be an upper bound (device-count mode)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = F - 1;  // largest f with pre[f] <= i
@@ -472,7 +476,11 @@ __global__ void __launch_bounds__(256) gather_packed_fp4_kernel(const uint8_t* _
                                                                 const int32_t* __restrict__ row_pos,
                                                                 int64_t n, int H,
                                                                 uint8_t* __restrict__ a_codes,
-                                                                uint8_t* __restrict__ a_sf) {
+                                                                uint8_t* __restrict__ a_sf,
+                                                                const int32_t* __restrict__ d_count,
+                                                                const int32_t* __restrict__ d_gate) {
+  if (d_gate && *d_gate == 0) return;
+  if (d_count && (int64_t)*d_count < n) n = *d_count;
   const int lane = threadIdx.x & 31;
   const int nkb = H / 16;
   const int64_t rb = H / 2 + H / 16;
@@ -571,7 +579,7 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
   if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
   gather_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, d_prec,
-      reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag);
+      reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag, nullptr, nullptr);
   return check_launch("realb_dispatch_permute (rows)");
 }
 
@@ -604,7 +612,7 @@ extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const flo
 extern "C" int realb_gather_rows(const void* d_x, const int32_t* d_expert, const int32_t* d_pos,
                                  int64_t P, int H, int k, const uint8_t* d_prec, void* d_a_bf16,
                                  uint8_t* d_a_codes, uint8_t* d_a_sf, int32_t* d_flag,
-                                 void* stream) {
+                                 const int32_t* d_count, const int32_t* d_gate, void* stream) {
   if (!d_x || !d_expert || !d_pos || !d_prec || !d_a_bf16 || P < 0 || H <= 0 || H % 64 || k < 1) {
     set_error("realb_gather_rows: bad arguments");
     return REALB_EINVAL;
@@ -614,7 +622,7 @@ extern "C" int realb_gather_rows(const void* d_x, const int32_t* d_expert, const
   if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
   gather_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(d_x), d_expert, d_pos, P, H, k, d_prec,
-      reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag);
+      reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag, d_count, d_gate);
   return check_launch("realb_gather_rows");
 }
 
@@ -690,6 +698,7 @@ extern "C" int realb_ep_pack(const void* d_x, const int32_t* d_topk_idx, int T, 
 
 extern "C" int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_t* d_pos, int64_t n,
                                               int H, uint8_t* d_a_codes, uint8_t* d_a_sf,
+                                              const int32_t* d_count, const int32_t* d_gate,
                                               void* stream) {
   if (!d_src || !d_pos || !d_a_codes || !d_a_sf || n < 0 || H <= 0 || H % 256) {
     set_error("realb_gather_rows_nvfp4_packed: bad arguments (H=%d; H %% 256 == 0)", H);
@@ -699,6 +708,7 @@ extern "C" int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_
   int64_t grid = (n + 7) / 8;
   if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
   gather_packed_fp4_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(d_src, d_pos, n, H,
-                                                                             d_a_codes, d_a_sf);
+                                                                             d_a_codes, d_a_sf, d_count,
+                                                                             d_gate);
   return check_launch("realb_gather_rows_nvfp4_packed");
 }

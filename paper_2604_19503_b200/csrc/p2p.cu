@@ -10,6 +10,7 @@
 // Window offsets are a pure function of the [R][R] pair-count matrix every
 // rank holds after C1 (source-major receive order, expert-sorted send order),
 // so senders and receivers agree on every row's address without a handshake.
+#include <cstddef>
 #include <cstring>
 
 #include "common.cuh"
@@ -113,6 +114,155 @@ __global__ void p2p_wait_kernel(const uint32_t* ctr, uint32_t target) {
       __nanosleep(256);
     }
     __threadfence_system();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-sync-free form: the C1 counts travel through peer memory too, and every
+// rank derives the plan and all window offsets ON THE DEVICE from the gathered
+// [R][E][2] counts, so the whole EP layer is stream-ordered and CUDA-graph
+// capturable (realb_p2p_publish, realb_p2p_plan_offsets and the *_dev kernels).
+struct P2PPlan {
+  int32_t row0[kMaxPeers];       // my send-order position of the first row bound for peer d
+  int64_t dst_off[kMaxPeers];    // byte offset of my block inside peer d's receive window
+  int32_t fmt[kMaxPeers];        // row format towards peer d (0 bf16, 1 packed NVFP4)
+  int32_t recv0[kMaxPeers + 1];  // source-major prefix of the rows I receive
+  int32_t ret_row0[kMaxPeers];   // row offset of my block inside source s's return window
+  int32_t n_recv;                // rows I receive (= recv0[R])
+  int32_t w4a4;                  // my precision (W4A4 = 1)
+  int32_t gate_bf16, gate_packed;  // which receive-side gather runs
+};
+
+__global__ void p2p_publish_kernel(const int32_t* __restrict__ src, int n, const PeerRows dst,
+                                   int64_t off_words) {
+  for (int d = 0; d < dst.R; ++d) {
+    int32_t* o = reinterpret_cast<int32_t*>(dst.base[d]) + off_words;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) o[i] = src[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) p2p_plan_kernel(const int32_t* __restrict__ counts, int R, int E,
+                                                        int rank, int H, int fp4_dispatch,
+                                                        const uint8_t* __restrict__ prec, P2PPlan* plan,
+                                                        int32_t* __restrict__ cnt_local,
+                                                        uint8_t* __restrict__ prec_local) {
+  __shared__ int32_t pairs[kMaxPeers * kMaxPeers];  // [s][d]
+  const int El = E / R;
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+    const int s = i / R, d = i - s * R;
+    int acc = 0;
+    for (int e = d * El; e < (d + 1) * El; ++e) acc += counts[(s * E + e) * 2] + counts[(s * E + e) * 2 + 1];
+    pairs[i] = acc;
+  }
+  for (int i = threadIdx.x; i < R * El; i += blockDim.x) {
+    const int s = i / El, le = i - s * El, e = rank * El + le;
+    cnt_local[i] = counts[(s * E + e) * 2] + counts[(s * E + e) * 2 + 1];
+  }
+  for (int i = threadIdx.x; i < El; i += blockDim.x) prec_local[i] = prec[rank * El + i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int d = 0; d < R; ++d) {
+      const int f = fp4_dispatch && prec[d * El] == REALB_PREC_W4A4;
+      const int64_t units = f ? (H / 2 + H / 16) : 2 * (int64_t)H;
+      int64_t before = 0;
+      for (int s2 = 0; s2 < rank; ++s2) before += pairs[s2 * R + d];
+      plan->row0[d] = run;
+      plan->dst_off[d] = before * units;
+      plan->fmt[d] = f;
+      run += pairs[rank * R + d];
+    }
+    int32_t pr = 0;
+    for (int s2 = 0; s2 < R; ++s2) {
+      plan->recv0[s2] = pr;
+      pr += pairs[s2 * R + rank];
+      int32_t before = 0;
+      for (int d = 0; d < rank; ++d) before += pairs[s2 * R + d];
+      plan->ret_row0[s2] = before;
+    }
+    plan->recv0[R] = pr;
+    plan->n_recv = pr;
+    const int w4 = prec[rank * El] == REALB_PREC_W4A4;
+    plan->w4a4 = w4;
+    plan->gate_packed = w4 && fp4_dispatch;
+    plan->gate_bf16 = !(w4 && fp4_dispatch);
+  }
+}
+
+// graph-safe wait: the expected value lives in device memory and advances by
+// `inc` (= R signals per layer) on every call, so a captured graph can replay it
+__global__ void p2p_wait_next_kernel(uint32_t* expected, uint32_t inc, const uint32_t* ctr) {
+  if (threadIdx.x == 0) {
+    const uint32_t target = *expected + inc;
+    *expected = target;
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if ((int32_t)(v - target) >= 0) break;
+      __nanosleep(256);
+    }
+    __threadfence_system();
+  }
+}
+
+// pack with the per-peer row offsets / formats read from the device plan
+__global__ void __launch_bounds__(256) p2p_pack_dev_kernel(const __nv_bfloat16* __restrict__ x,
+                                                           const int32_t* __restrict__ topk_idx,
+                                                           const int32_t* __restrict__ pair_pos, int64_t P,
+                                                           int H, int k, const PeerRows win,
+                                                           const P2PPlan* __restrict__ plan, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int nkb = H / 16;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = p / k;
+    const int d = topk_idx[p] / win.El;
+    const int64_t rel = (int64_t)pair_pos[p] - plan->row0[d];
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+    uint8_t* base = win.base[d] + plan->dst_off[d];
+    if (plan->fmt[d] == 0) {
+      uint4* o = reinterpret_cast<uint4*>(base + rel * (2 * (int64_t)H));
+      for (int i = lane; i < H / 8; i += 32) o[i] = __ldg(src + i);
+    } else {
+      uint8_t* row = base + rel * (int64_t)(H / 2 + H / 16);
+      for (int g = lane; g < nkb / 4; g += 32) {
+        uint32_t sfw = 0;
+        uint2 cw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint4 u0 = __ldg(src + (g * 4 + b) * 2), u1 = __ldg(src + (g * 4 + b) * 2 + 1);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          uint32_t sb;
+          bool nf;
+          cw[b] = quant_block16_bf16(w, sb, nf);
+          if (nf && flag) atomicOr(flag, 1);
+          sfw |= sb << (8 * b);
+        }
+        uint4* cdst = reinterpret_cast<uint4*>(row + g * 32);
+        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
+        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
+        reinterpret_cast<uint32_t*>(row + H / 2)[g] = sfw;
+      }
+    }
+  }
+}
+
+// return with the sources' offsets and my received-row count from the device plan
+__global__ void __launch_bounds__(256) p2p_return_dev_kernel(const __nv_bfloat16* __restrict__ rows,
+                                                             const int32_t* __restrict__ row_pos, int64_t n_cap,
+                                                             int H, const PeerRows win,
+                                                             const P2PPlan* __restrict__ plan) {
+  const int lane = threadIdx.x & 31;
+  const int R = win.R;
+  const int64_t n = min(n_cap, (int64_t)plan->n_recv);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int s = 0;
+    while (s + 1 < R && plan->recv0[s + 1] <= i) ++s;
+    const uint4* src = reinterpret_cast<const uint4*>(rows + (int64_t)row_pos[i] * H);
+    uint4* dst = reinterpret_cast<uint4*>(win.base[s] + ((int64_t)plan->ret_row0[s] + (i - plan->recv0[s])) *
+                                                            (2 * (int64_t)H));
+    for (int c = lane; c < H / 8; c += 32) dst[c] = __ldg(src + c);
   }
 }
 
@@ -230,4 +380,111 @@ extern "C" int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, void* 
   }
   p2p_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_counter, target);
   return check_launch("realb_p2p_wait");
+}
+
+static int fill_bases(PeerRows& w, const uint64_t* h, int R, const char* fn) {
+  if (!h || R < 1 || R > kMaxPeers) {
+    set_error("%s: bad peer list (R=%d)", fn, R);
+    return REALB_EINVAL;
+  }
+  for (int d = 0; d < R; ++d) {
+    if (h[d] & 15) {
+      set_error("%s: peer %d address not 16-byte aligned", fn, d);
+      return REALB_EINVAL;
+    }
+    w.base[d] = reinterpret_cast<uint8_t*>(h[d]);
+  }
+  w.R = R;
+  return REALB_OK;
+}
+
+extern "C" int64_t realb_p2p_plan_bytes(void) { return (int64_t)sizeof(P2PPlan); }
+
+extern "C" int realb_p2p_publish(const int32_t* d_src, int n_words, int R, const uint64_t* h_peer_windows,
+                                 int64_t offset_words, void* stream) {
+  if (!d_src || n_words <= 0 || offset_words < 0) {
+    set_error("realb_p2p_publish: bad arguments");
+    return REALB_EINVAL;
+  }
+  PeerRows w{};
+  int rc = fill_bases(w, h_peer_windows, R, "realb_p2p_publish");
+  if (rc) return rc;
+  p2p_publish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_src, n_words, w, offset_words);
+  return check_launch("realb_p2p_publish");
+}
+
+extern "C" int realb_p2p_plan_offsets(const int32_t* d_counts, int R, int E, int rank, int H, int fp4_dispatch,
+                                      const uint8_t* d_prec, void* d_plan, int32_t* d_cnt_local,
+                                      uint8_t* d_prec_local, void* stream) {
+  if (!d_counts || !d_prec || !d_plan || !d_cnt_local || !d_prec_local || R < 1 || R > kMaxPeers ||
+      E < 1 || E % R || rank < 0 || rank >= R || H <= 0) {
+    set_error("realb_p2p_plan_offsets: bad arguments (R=%d E=%d rank=%d)", R, E, rank);
+    return REALB_EINVAL;
+  }
+  p2p_plan_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_counts, R, E, rank, H, fp4_dispatch, d_prec,
+                                                       reinterpret_cast<P2PPlan*>(d_plan), d_cnt_local,
+                                                       d_prec_local);
+  return check_launch("realb_p2p_plan_offsets");
+}
+
+extern "C" int realb_p2p_pack_dev(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                                  const int32_t* d_layout, int nchunks, int R, const uint64_t* h_peer_recv,
+                                  const void* d_plan, int32_t* d_pair_pos, int32_t* d_flag, void* stream) {
+  if (T == 0 && nchunks == 0) return REALB_OK;
+  if (!d_x || !d_topk_idx || !d_layout || !d_plan || !d_pair_pos || T < 0 || H <= 0 || H % 64 || E < 1 ||
+      E > 256 || k < 1 || k > 8 || E % R || nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
+    set_error("realb_p2p_pack_dev: bad arguments (T=%d H=%d E=%d k=%d R=%d)", T, H, E, k, R);
+    return REALB_EINVAL;
+  }
+  PeerRows w{};
+  int rc = fill_bases(w, h_peer_recv, R, "realb_p2p_pack_dev");
+  if (rc) return rc;
+  w.El = E / R;
+  rc = ep_positions(d_topk_idx, T, E, k, d_layout, nchunks, d_pair_pos, stream);
+  if (rc) return rc;
+  const int64_t P = (int64_t)T * k;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  p2p_pack_dev_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, w,
+      reinterpret_cast<const P2PPlan*>(d_plan), d_flag);
+  return check_launch("realb_p2p_pack_dev");
+}
+
+extern "C" int realb_p2p_return_dev(const void* d_rows, const int32_t* d_row_pos, int64_t n_cap, int H, int R,
+                                    const uint64_t* h_peer_ret, const void* d_plan, void* stream) {
+  if (!d_rows || !d_row_pos || !d_plan || n_cap < 0 || H <= 0 || H % 8) {
+    set_error("realb_p2p_return_dev: bad arguments");
+    return REALB_EINVAL;
+  }
+  PeerRows w{};
+  int rc = fill_bases(w, h_peer_ret, R, "realb_p2p_return_dev");
+  if (rc || n_cap == 0) return rc;
+  int64_t grid = (n_cap + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  p2p_return_dev_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_rows), d_row_pos, n_cap, H, w,
+      reinterpret_cast<const P2PPlan*>(d_plan));
+  return check_launch("realb_p2p_return_dev");
+}
+
+extern "C" int realb_p2p_wait_next(uint32_t* d_expected, uint32_t inc, const uint32_t* d_counter,
+                                   void* stream) {
+  if (!d_expected || !d_counter) {
+    set_error("realb_p2p_wait_next: bad arguments");
+    return REALB_EINVAL;
+  }
+  p2p_wait_next_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_expected, inc, d_counter);
+  return check_launch("realb_p2p_wait_next");
+}
+
+// [sizeof(P2PPlan), offsetof n_recv, w4a4, gate_bf16, gate_packed]
+extern "C" int realb_p2p_plan_layout(int64_t* out5) {
+  if (!out5) return REALB_EINVAL;
+  out5[0] = (int64_t)sizeof(P2PPlan);
+  out5[1] = (int64_t)offsetof(P2PPlan, n_recv);
+  out5[2] = (int64_t)offsetof(P2PPlan, w4a4);
+  out5[3] = (int64_t)offsetof(P2PPlan, gate_bf16);
+  out5[4] = (int64_t)offsetof(P2PPlan, gate_packed);
+  return REALB_OK;
 }

@@ -27,6 +27,7 @@ and in the one-GPU, two-process test (gloo staged through the host).
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 
 import numpy as np
@@ -35,7 +36,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .moe import MoEShape, MoEWeights
-from .policy import ClusterConfig, Precision, PrecisionPlan, RealbParams, plan_for, \
+from .policy import STRATEGIES, ClusterConfig, Precision, PrecisionPlan, RealbParams, plan_for, \
     rank_loads_from_counts
 
 
@@ -201,12 +202,12 @@ class CudaEPOps:
         ws = self._fp4_ws() if w4a4 else None
         if packed_fp4:  # rows arrived as NVFP4 (sender-side K4): byte movement only
             _lib.call("realb_gather_rows_nvfp4_packed", recv_ptr, self.row_pos.data_ptr(), n, H,
-                      ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(), sp)
+                      ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(), None, None, sp)
         else:
             _lib.call("realb_gather_rows", recv_ptr, self.row_expert.data_ptr(), self.row_pos.data_ptr(),
                       n, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(),
                       _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
-                      self.flag.data_ptr(), sp)
+                      self.flag.data_ptr(), None, None, sp)
         lay = self.local_layout.data_ptr()
         if not w4a4:
             _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.local.w_gu.data_ptr(),
@@ -236,8 +237,8 @@ class CudaEPOps:
         process group; peers' windows mapped (NVLink peer memory across GPUs)."""
         import ctypes as Cty
 
-        R, H, T, k = self.R, self.H, self.T, self.k
-        sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256}
+        R, H, T, k, E = self.R, self.H, self.T, self.k, self.E
+        sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256, "cnt": R * E * 2 * 4}
         self._p2p_own, handles = {}, {}
         for name, nbytes in sizes.items():
             ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
@@ -258,6 +259,21 @@ class CudaEPOps:
                     self.p2p[name][r] = ptr.value
                     self._p2p_opened.append(ptr.value)
         self.p2p_epoch = 0
+        self.p2p_rank = comm.rank
+        # host-sync-free (device-plan) form: plan record, expected-counter words,
+        # global expert precisions and the plan kernel's scratch
+        dev = self.dev
+        lay = (C.c_int64 * 5)()
+        _lib.call("realb_p2p_plan_layout", lay)
+        self.plan_layout = list(lay)
+        self.d_plan = torch.zeros(int(lay[0]) + 64, dtype=torch.uint8, device=dev)
+        self.d_expected = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.prec_global = torch.zeros(E, dtype=torch.uint8, device=dev)
+        self.plan_out = torch.zeros(3 + R, dtype=torch.int32, device=dev)
+        self.plan_host = torch.zeros(3 + R, dtype=torch.int32, pin_memory=True)
+        self.vt_all_host = torch.zeros(R, E, 2, dtype=torch.int32, pin_memory=True)
+        self.gl_layout = torch.zeros(int(_lib.load().realb_layout_words(E, R)), dtype=torch.int32, device=dev)
+        self.gl_vt = torch.zeros(E, 2, dtype=torch.int32, device=dev)
         dist.barrier(group=comm.group)
 
     def p2p_dispatch(self, x, topk_idx, fp4_rows, pairs: np.ndarray, rank: int):
@@ -300,6 +316,110 @@ class CudaEPOps:
         _lib.call("realb_p2p_signal", ctrs.ctypes.data, R, sp)
         _lib.call("realb_p2p_wait", self._p2p_own["ctr"] + ctr_off, (self.p2p_epoch * R) & 0xFFFFFFFF, sp)
 
+    def forward_device(self, x, mod, strategy: str, params: RealbParams, fp4_dispatch: bool,
+                       timer=None):
+        """The whole EP layer with no host synchronisation (CUDA-graph capturable):
+        C1 through peer memory, the plan and every window offset derived on the
+        device (realb_moe_align_plan over the gathered [R][E][2] counts,
+        realb_p2p_plan_offsets), K3 / gathers / both GEMM precisions launched
+        unconditionally and selected by device-side group lists and gates.
+        -> y; the plan and counts are read back lazily (DevicePlanResult)."""
+        from .moe import _STRATEGY_CODE
+
+        R, r, E, El, H, I, k = self.R, self.p2p_rank, self.E, self.El, self.H, self.I, self.k
+        T = x.shape[0]
+        mark = timer.mark if timer is not None else (lambda *a, **kw: None)
+        main = torch.cuda.current_stream()
+        sp = _lib.stream_ptr(main)
+        mark("start")
+        self.route(x, mod)
+        # C1: my [E][2] counts into every rank's counts window, slot r
+        cnt_bases = np.array(self.p2p["cnt"], np.uint64)
+        _lib.call("realb_p2p_publish", self.vt_local.data_ptr(), E * 2, R, cnt_bases.ctypes.data, r * E * 2, sp)
+        self._signal_wait_dev(8, 2)
+        # P1 on the device over the global counts (R "chunks" of [E][2]), then the window plan
+        _lib.call("realb_moe_align_plan", self.p2p["cnt"][r], R, E, R, _STRATEGY_CODE[strategy],
+                  float(params.capacity_factor), float(params.modality_threshold),
+                  int(params.global_batch_threshold), int(bool(self.s.modality_isolated)),
+                  self.prec_global.data_ptr(), self.plan_out.data_ptr(), self.gl_layout.data_ptr(),
+                  self.gl_vt.data_ptr(), sp)
+        _lib.call("realb_p2p_plan_offsets", self.p2p["cnt"][r], R, E, r, H, int(bool(fp4_dispatch)),
+                  self.prec_global.data_ptr(), self.d_plan.data_ptr(), self.cnt_dev.data_ptr(),
+                  self.prec_local.data_ptr(), sp)
+        mark("schedule")
+        # K3 for my experts if the device plan made them W4A4 (no-op otherwise), under C2
+        ws = self._fp4_ws()
+        self.side.wait_stream(main)
+        with torch.cuda.stream(self.side):
+            ssp = _lib.stream_ptr(self.side)
+            _lib.call("realb_quantize_experts_nvfp4", self.local.w_gu.data_ptr(), El, 2 * I, H,
+                      self.prec_local.data_ptr(), ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
+                      self.flag.data_ptr(), self.quant_max_ctas, ssp)
+            _lib.call("realb_quantize_experts_nvfp4", self.local.w_d.data_ptr(), El, H, I,
+                      self.prec_local.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
+                      self.flag.data_ptr(), self.quant_max_ctas, ssp)
+        # C2
+        recv_bases = np.array(self.p2p["recv"], np.uint64)
+        _lib.call("realb_p2p_pack_dev", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
+                  self.send_layout.data_ptr(), (T + 63) // 64, R, recv_bases.ctypes.data, self.d_plan.data_ptr(),
+                  self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
+        self._signal_wait_dev(0, 0)
+        mark("dispatch")
+        # receive side: regroup, then exactly one of the two gathers runs (device gates)
+        cap = self.recv_cap
+        _lib.call("realb_ep_regroup", self.cnt_dev.data_ptr(), R, El, self.prec_local.data_ptr(), cap,
+                  self.local_layout.data_ptr(), self.base.data_ptr(), self.row_expert.data_ptr(),
+                  self.row_pos.data_ptr(), sp)
+        pl = self.d_plan.data_ptr()
+        n_ptr, g16, gpk = pl + self.plan_layout[1], pl + self.plan_layout[3], pl + self.plan_layout[4]
+        _lib.call("realb_gather_rows", self.p2p["recv"][r], self.row_expert.data_ptr(), self.row_pos.data_ptr(),
+                  cap, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(), ws["a_codes"].data_ptr(),
+                  ws["a_sf"].data_ptr(), self.flag.data_ptr(), n_ptr, g16, sp)
+        _lib.call("realb_gather_rows_nvfp4_packed", self.p2p["recv"][r], self.row_pos.data_ptr(), cap, H,
+                  ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(), n_ptr, gpk, sp)
+        # both precisions' GEMMs; each runs only the groups the device plan gave it
+        lay = self.local_layout.data_ptr()
+        _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.local.w_gu.data_ptr(), self.rows_cap,
+                  2 * I, H, El, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.h_bf16.data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.local.w_d.data_ptr(), self.rows_cap,
+                  H, I, El, lay, _lib.PREC_W16A16, _lib.EPI_STORE, self.rows_out.data_ptr(), 0, sp)
+        main.wait_stream(self.side)
+        _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
+                  ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, El, lay,
+                  _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+                  ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
+                  _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+        mark("compute")
+        # C3: every output row straight into its source's return window
+        ret_bases = np.array(self.p2p["ret"], np.uint64)
+        _lib.call("realb_p2p_return_dev", self.rows_out.data_ptr(), self.row_pos.data_ptr(), cap, H, R,
+                  ret_bases.ctypes.data, pl, sp)
+        self._signal_wait_dev(4, 1)
+        y = torch.empty(T, H, dtype=torch.bfloat16, device=self.dev)
+        _lib.call("realb_combine", self.p2p["ret"][r], self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+                  T, H, k, None, y.data_ptr(), sp)
+        mark("combine")
+        if torch.cuda.is_current_stream_capturing():
+            return y, None
+        self.plan_host.copy_(self.plan_out, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        return y, DevicePlanResult(self, ev)
+
+    def read_counts(self) -> np.ndarray:
+        """[R, E, 2] global counts of the last device-plan layer call (own counts window)."""
+        view = _device_view(self.p2p["cnt"][self.p2p_rank], self.R * self.E * 2, torch.int32)
+        return view.reshape(self.R, self.E, 2).cpu().numpy().astype(np.int64)
+
+    def _signal_wait_dev(self, ctr_off: int, slot: int):
+        R = self.R
+        ctrs = np.array([self.p2p["ctr"][d] + ctr_off for d in range(R)], np.uint64)
+        sp = _lib.stream_ptr()
+        _lib.call("realb_p2p_signal", ctrs.ctypes.data, R, sp)
+        _lib.call("realb_p2p_wait_next", self.d_expected.data_ptr() + 4 * slot, R,
+                  self._p2p_own["ctr"] + ctr_off, sp)
+
     def close_p2p(self):
         torch.cuda.synchronize()
         for p in getattr(self, "_p2p_opened", []):
@@ -315,7 +435,7 @@ class CudaEPOps:
         """(median ms, algorithmic flops, is_fp4) of the local gate_up grouped GEMM
         over the rows of the last forward (valid rows only, padding excluded)."""
         El, H, I = self.El, self.H, self.I
-        n = int(self.cnt_host.numpy().sum())
+        n = int(self.cnt_dev.sum().item())  # filled by the host (C1 path) or the device plan
         w4a4 = bool(self.prec_local[0].item() == _lib.PREC_W4A4)
         lay, sp = self.local_layout.data_ptr(), _lib.stream_ptr()
         ts = []
@@ -363,6 +483,15 @@ class EPMoELayer:
         self.cluster = ClusterConfig(self.R, 1, self.El, 1, shape.modality_isolated)
         self.fp4_dispatch = fp4_dispatch
 
+    def forward_device(self, x, mod, strategy: str = "realb", params: RealbParams | None = None, timer=None):
+        """Host-sync-free EP layer (peer-memory transport only): -> (y, DevicePlanResult
+        or None under graph capture)."""
+        if not (self.comm.p2p and hasattr(self.ops, "forward_device")):
+            raise ValueError("the device-plan EP layer needs the peer-memory transport")
+        if strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {strategy!r}")
+        return self.ops.forward_device(x, mod, strategy, params or RealbParams(), self.fp4_dispatch, timer)
+
     def forward(self, x, mod, strategy: str = "realb", params: RealbParams | None = None, timer=None):
         R, r, El, E = self.R, self.rank, self.El, self.shape.num_experts
         mark = timer.mark if timer is not None else (lambda *a, **k: None)
@@ -397,6 +526,36 @@ class EPMoELayer:
         y = self.ops.combine(ret, send_pos, topk_w)
         mark("combine")
         return y, plan, vt_all
+
+
+def _device_view(ptr: int, numel: int, dtype) -> torch.Tensor:
+    """Zero-copy torch view of raw device memory (a peer-memory window)."""
+    typestr = {torch.int32: "<i4", torch.uint8: "|u1", torch.bfloat16: "<f2"}[dtype]
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False),
+                                    "version": 3}
+    return torch.as_tensor(_Arr(), device="cuda")
+
+
+class DevicePlanResult:
+    """The device plan of a host-sync-free EP layer call, read back on first use."""
+
+    def __init__(self, ops, event):
+        self.ops, self.event, self._plan = ops, event, None
+
+    @property
+    def plan(self) -> PrecisionPlan:
+        if self._plan is None:
+            self.event.synchronize()
+            po = self.ops.plan_host.numpy()
+            R = self.ops.R
+            flags = po[3:3 + R]
+            self._plan = PrecisionPlan(
+                tuple(Precision.W4A4 if f & 4 else Precision.W16A16 for f in flags),
+                frozenset(int(i) for i in np.flatnonzero(flags & 1)),
+                frozenset(int(i) for i in np.flatnonzero(flags & 2)), bool(po[0]))
+        return self._plan
 
 
 class CudaPhaseTimer:
@@ -458,9 +617,12 @@ def run_bench(args):
     # through CUDA-IPC peer-memory windows, NCCL only for the C1 counts); "gloo" /
     # "p2p-gloo": validation modes for a one-GPU box (all ranks share cuda:0, C1
     # (and C2/C3 for "gloo") staged through the host).
+    # "p2p-graph" / "p2p-graph-gloo": the host-sync-free layer (device plan) replayed as
+    # one CUDA graph per step
     mode = os.environ.get("REALB_EP_COMM", "nccl")
-    staged = mode in ("gloo", "p2p-gloo")
-    p2p = mode in ("p2p", "p2p-gloo")
+    staged = mode in ("gloo", "p2p-gloo", "p2p-graph-gloo")
+    p2p = mode in ("p2p", "p2p-gloo", "p2p-graph", "p2p-graph-gloo")
+    graph = mode in ("p2p-graph", "p2p-graph-gloo")
     if staged:
         torch.cuda.set_device(0)
         dist.init_process_group("gloo")
@@ -495,12 +657,29 @@ def run_bench(args):
         yh = torch.empty(T, shape.hidden, dtype=torch.bfloat16).pin_memory()
         xd, md = torch.empty_like(x), torch.empty_like(mod)
 
+        if graph:
+            xin, min_ = (xd, md) if e2e else (x, mod)
+            xd.copy_(x)
+            md.copy_(mod)
+            layer.forward_device(xin, min_, strategy)  # eager first: lazy workspaces
+            torch.cuda.synchronize()
+            dist.barrier()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                yg, _ = layer.forward_device(xin, min_, strategy)
+
         def step():
             if e2e:
                 xd.copy_(xh, non_blocking=True)
                 md.copy_(mh, non_blocking=True)
-                y, _, _ = layer.forward(xd, md, strategy)
+                if graph:
+                    g.replay()
+                    y = yg
+                else:
+                    y, _, _ = layer.forward(xd, md, strategy)
                 yh.copy_(y, non_blocking=True)
+            elif graph:
+                g.replay()
             else:
                 layer.forward(x, mod, strategy)
 
@@ -517,10 +696,15 @@ def run_bench(args):
         dist.barrier()
         return max_over_ranks(s.elapsed_time(e)) / steps
 
+    # kernels per layer call, counted on one eager call, x timed steps
     _lib.launch_count = 0
+    if graph:
+        layer.forward_device(x, mod, "realb")
+    else:
+        layer.forward(x, mod, "realb")
+    launches = _lib.launch_count * args.steps
     with ClockSampler(local_rank) as clk:
         ms = timed("realb", args.steps, args.warmup)
-    launches = _lib.launch_count * args.steps // (args.steps + args.warmup)
     ms_bf16 = timed("baseline", args.steps, args.warmup)
     ms_e2e = timed("realb", args.steps, max(1, args.warmup // 2), e2e=True)
 
@@ -528,7 +712,11 @@ def run_bench(args):
     phases = {}
     for strategy in ("realb", "baseline"):
         tm = CudaPhaseTimer()
-        _, plan_s, vt_all = layer.forward(x, mod, strategy, timer=tm)
+        if graph:
+            _, res = layer.forward_device(x, mod, strategy, timer=tm)
+            plan_s, vt_all = res.plan, ops.read_counts()
+        else:
+            _, plan_s, vt_all = layer.forward(x, mod, strategy, timer=tm)
         ph = tm.phases()
         row = [ph.schedule_ns, ph.transform_ns, ph.dispatch_ns, ph.compute_ns, ph.combine_ns, tm.total_ns()]
         allrows = [None] * world
@@ -537,7 +725,10 @@ def run_bench(args):
         if strategy == "realb":
             plan = plan_s
     # critical rank's gate_up GEMM (the dominant kernel) against its precision's peak
-    layer.forward(x, mod, "realb")
+    if graph:
+        layer.forward_device(x, mod, "realb")
+    else:
+        layer.forward(x, mod, "realb")
     torch.cuda.synchronize()
     g_ms, g_flops, g_fp4 = ops.time_gate_up()
     allg = [None] * world
@@ -563,7 +754,9 @@ def run_bench(args):
                "e2e": {"value": world * T / (ms_e2e / 1e3), "unit": "tokens/s",
                        "h2d_bytes_per_step": int(world * (x.numel() * 2 + mod.numel())),
                        "d2h_bytes_per_step": int(world * T * shape.hidden * 2),
-                       "pipeline": "serial per step (the C1 count exchange syncs the host)"},
+                       "pipeline": "serial per step: H2D, one CUDA-graph replay of the host-sync-free "
+                                   "layer, D2H" if graph else
+                                   "serial per step (the C1 count exchange syncs the host)"},
                "roofline": {"kernel": f"grouped GEMM gate_up on the critical rank {crit} "
                                       f"({'NVFP4 K6' if g4 else 'BF16 K5'})",
                             "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -577,6 +770,8 @@ def run_bench(args):
                "gpu_launches": int(launches),
                "clocks": clk.summary(),
                "comm": {"nccl": "nccl", "p2p": "peer-memory windows (CUDA IPC / NVLink), NCCL for C1",
+                        "p2p-graph": "peer-memory windows incl. C1, device plan, one CUDA graph per layer",
+                        "p2p-graph-gloo": "p2p-graph with ranks sharing one GPU (validation only)",
                         "gloo": "gloo-staged on one shared GPU (validation only)",
                         "p2p-gloo": "peer-memory windows on one shared GPU, gloo for C1 (validation only)"}[mode]}
         print(json.dumps(out), flush=True)

@@ -207,10 +207,10 @@ def measure_ep_kernels(torch, layer, x, mod, T_local: int, recv_rows, w4a4):
         sp = _lib.stream_ptr()
         if packed_fp4:
             return lambda: _lib.call("realb_gather_rows_nvfp4_packed", packed.data_ptr(), row_p.data_ptr(), n,
-                                     H, ac.data_ptr(), asf.data_ptr(), sp)
+                                     H, ac.data_ptr(), asf.data_ptr(), None, None, sp)
         return lambda: _lib.call("realb_gather_rows", recv.data_ptr(), row_e.data_ptr(), row_p.data_ptr(), n,
                                  H, 1, precs[int(w4)].data_ptr(), a.data_ptr(), ac.data_ptr(), asf.data_ptr(),
-                                 flag.data_ptr(), sp)
+                                 flag.data_ptr(), None, None, sp)
 
     out = {"send": _median_ms(torch, sender, reps=5)}
     out["recv_bf16"] = [_median_ms(torch, gather(int(n), False, False), reps=5) for n in recv_rows]

@@ -36,7 +36,7 @@ def _setup(shape_name, E, T, world, rank, device="cuda"):
     return shape, x, mod, router, gu, dn
 
 
-def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir, p2p=False):
+def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir, p2p=False, device_plan=False):
     import sys
     from pathlib import Path
 
@@ -57,9 +57,25 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir,
     if p2p:
         ops.setup_p2p(comm)
     layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
-    y, plan, vt = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
-    if p2p:  # a second layer call exercises window reuse and the epoch counters
-        y, plan, vt = layer.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
+    params = RealbParams(global_batch_threshold=0)
+    if device_plan:
+        # host-sync-free layer: eager twice, then captured as a CUDA graph and replayed
+        y0, res = layer.forward_device(x, mod, strategy, params)
+        plan = res.plan
+        y1, _ = layer.forward_device(x, mod, strategy, params)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            yg, _ = layer.forward_device(x, mod, strategy, params)
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y0, y1) and torch.equal(yg, y0)
+        y = yg
+    else:
+        y, plan, vt = layer.forward(x, mod, strategy, params)
+        if p2p:  # a second layer call exercises window reuse and the epoch counters
+            y, plan, vt = layer.forward(x, mod, strategy, params)
     torch.cuda.synchronize()
     if p2p:
         dist.barrier()
@@ -88,10 +104,20 @@ def test_ep2_peer_memory_transport_equals_single_gpu_layer(tmp_path, shape_name,
     _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=True)
 
 
-def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p):
+@pytest.mark.parametrize("shape_name,E,T,strategy,fp4_dispatch", [
+    ("kimi", 16, 384, "realb", True), ("kimi", 16, 384, "realb", False), ("qwen", 16, 256, "fp4all", True),
+    ("tiny", 8, 512, "baseline", False)])
+def test_ep2_host_sync_free_layer_and_graph(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
+    """The host-sync-free EP layer: C1 through peer memory, plan and window offsets
+    derived on the device, both precisions launched and selected by device-side
+    group lists; eager == CUDA-graph replay == the single-GPU layer, exactly."""
+    _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=True, device_plan=True)
+
+
+def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path), p2p),
-             nprocs=world)
+    mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path), p2p,
+                            device_plan), nprocs=world)
     from paper_2604_19503_b200 import _lib
     from paper_2604_19503_b200.moe import MoELayer, MoEWeights
     from paper_2604_19503_b200.policy import ClusterConfig, RealbParams
