@@ -406,19 +406,23 @@ class MoELayer:
         mixed = code == 1 or (code == 2 and not (self.cluster.num_ranks == 1
                                                  and params.capacity_factor >= 1.0))
         mark = timer.mark if timer is not None else (lambda *a, **kw: None)
+        # realb-seq: the reference's sequential ablation (engine.py:162-167): K3 on the
+        # main stream, so the transform is NOT hidden behind dispatch
+        k3_stream = main if strategy == "realb-seq" else self.side
         if mixed:
             ws = self._fp4_ws()
-            self.side.wait_stream(main)
-            with torch.cuda.stream(self.side):
-                ssp = _lib.stream_ptr(self.side)
-                mark("k3_start", self.side)
+            if k3_stream is not main:
+                self.side.wait_stream(main)
+            with torch.cuda.stream(k3_stream):
+                ssp = _lib.stream_ptr(k3_stream)
+                mark("k3_start", k3_stream)
                 _lib.call("realb_quantize_experts_nvfp4", self.w.w_gu.data_ptr(), E, 2 * I, H,
                           self.prec_dev.data_ptr(), ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
                           self.flag.data_ptr(), self.quant_max_ctas, ssp)
                 _lib.call("realb_quantize_experts_nvfp4", self.w.w_d.data_ptr(), E, H, I,
                           self.prec_dev.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
                           self.flag.data_ptr(), self.quant_max_ctas, ssp)
-                mark("k3_end", self.side)
+                mark("k3_end", k3_stream)
         else:
             ws = None
         mark("dispatch_start", main)
@@ -434,7 +438,8 @@ class MoELayer:
                   self.h_bf16.data_ptr(), 0, sp)
         if ws is not None:
             mark("fp4_ready", main)  # main stream reaches the first W4A4 GEMM
-            main.wait_stream(self.side)
+            if k3_stream is not main:
+                main.wait_stream(self.side)
             mark("fp4_start", main)
             _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
                       ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, E,

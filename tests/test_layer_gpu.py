@@ -392,3 +392,16 @@ def test_layer_with_shared_expert_vs_oracle(strategy, R):
     eager = res.y.clone()
     cap = layer.capture(x, mod, strategy, params)
     assert torch.equal(cap.replay(), eager)
+
+
+def test_realb_seq_equals_realb():
+    """realb-seq (K3 serialised on the main stream, the reference's sequential
+    ablation) computes exactly what realb (K3 overlapped on the side stream) does."""
+    shape = small(SHAPES["kimi"], 64)
+    T = 2048
+    layer, x, mod, *_ = build_layer(shape, T, R=8)
+    params = RealbParams(global_batch_threshold=0)
+    a = layer.forward(x, mod, "realb", params).y.clone()
+    b = layer.forward(x, mod, "realb-seq", params).y.clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
