@@ -119,6 +119,11 @@ class CudaEPOps:
         self.quant_max_ctas = quant_max_ctas
         self.side = torch.cuda.Stream(device=dev)
         self._fp4 = None
+        self.shared = None
+        if shape.shared_intermediate:
+            from .moe import SharedExpertMLP
+
+            self.shared = SharedExpertMLP(local.shared_gu, local.shared_d, T, dev)
 
     def _fp4_ws(self):
         if self._fp4 is None:
@@ -333,6 +338,7 @@ class CudaEPOps:
         sp = _lib.stream_ptr(main)
         mark("start")
         self.route(x, mod)
+        self.start_shared(x)
         # C1: my [E][2] counts into every rank's counts window, slot r
         cnt_bases = np.array(self.p2p["cnt"], np.uint64)
         _lib.call("realb_p2p_publish", self.vt_local.data_ptr(), E * 2, R, cnt_bases.ctypes.data, r * E * 2, sp)
@@ -397,8 +403,9 @@ class CudaEPOps:
                   ret_bases.ctypes.data, pl, sp)
         self._signal_wait_dev(4, 1)
         y = torch.empty(T, H, dtype=torch.bfloat16, device=self.dev)
+        addend = self.shared.join() if self.shared is not None and T > 0 else None
         _lib.call("realb_combine", self.p2p["ret"][r], self.send_pos.data_ptr(), self.topk_w.data_ptr(),
-                  T, H, k, None, y.data_ptr(), sp)
+                  T, H, k, addend, y.data_ptr(), sp)
         mark("combine")
         if torch.cuda.is_current_stream_capturing():
             return y, None
@@ -456,12 +463,19 @@ class CudaEPOps:
             ts.append(s.elapsed_time(e))
         return float(sorted(ts)[len(ts) // 2]), 2.0 * n * (2 * I) * H, w4a4
 
+    def start_shared(self, x):
+        """Shared-expert MLP of this rank's tokens on its own stream, overlapping
+        C1 / plan / dispatch / expert compute / return (§8f-2)."""
+        if self.shared is not None and x.shape[0] > 0:
+            self.shared.start(x)
+
     def combine(self, ret_buf, send_pos, topk_w):
         T = send_pos.shape[0]
         y = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.dev)
         ret_ptr = ret_buf if isinstance(ret_buf, int) else ret_buf.data_ptr()
+        addend = self.shared.join() if self.shared is not None and T > 0 else None
         _lib.call("realb_combine", ret_ptr, self.send_pos.data_ptr(), self.topk_w.data_ptr(),
-                  T, self.H, self.k, None, y.data_ptr(), _lib.stream_ptr())
+                  T, self.H, self.k, addend, y.data_ptr(), _lib.stream_ptr())
         return y
 
 
@@ -497,6 +511,8 @@ class EPMoELayer:
         mark = timer.mark if timer is not None else (lambda *a, **k: None)
         mark("start")
         topk_idx, topk_w, vt_local = self.ops.route(x, mod)
+        if hasattr(self.ops, "start_shared"):
+            self.ops.start_shared(x)
         vt_all = self.comm.all_gather_counts(vt_local)                      # C1 (host sync)
         plan = plan_for(strategy, rank_loads_from_counts(vt_all.sum(0), self.cluster), self.cluster,
                         params or RealbParams())                             # P1
@@ -587,14 +603,16 @@ class CudaPhaseTimer:
 
 
 def split_weights(shape: MoEShape, router, gate_up_hf, down_hf, rank: int, world: int, bias=None,
-                  device="cuda") -> MoEWeights:
-    """The local experts' weights of an EP rank (contiguous placement)."""
+                  device="cuda", shared=None) -> MoEWeights:
+    """The local experts' weights of an EP rank (contiguous placement); the shared
+    expert (if any) is replicated on every rank."""
     from dataclasses import replace
 
     El = shape.num_experts // world
     sl = slice(rank * El, (rank + 1) * El)
     local_shape = replace(shape, num_experts=El)
-    return MoEWeights.from_hf(local_shape, router[:El], gate_up_hf[sl], down_hf[sl], device=device)
+    return MoEWeights.from_hf(local_shape, router[:El], gate_up_hf[sl], down_hf[sl], device=device,
+                              shared=shared)
 
 
 # ----------------------------------------------------------------------------- bench (N > 1)
@@ -635,7 +653,9 @@ def run_bench(args):
     x, mod, router, _ = make_batch(shape, spec)
     gu, dn = make_experts(shape)  # same seed on every rank: identical global weights
     bias = torch.zeros(shape.num_experts, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
-    local = split_weights(shape, router, gu, dn, rank, world)
+    from .workload import make_shared_expert
+
+    local = split_weights(shape, router, gu, dn, rank, world, shared=make_shared_expert(shape))
     del gu, dn
     comm = EPComm(staged=staged, p2p=p2p)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)

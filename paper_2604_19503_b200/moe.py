@@ -229,6 +229,47 @@ class CapturedLayer:
         return self.y
 
 
+class SharedExpertMLP:
+    """The shared-expert MLP (every token; BF16 K5: SwiGLU gate_up, then down) on
+    its own stream: start() forks it off the current stream, join() makes the
+    current stream wait and returns the bf16 [T, H] output for the combine's
+    addend. Used by the single-GPU layer and by every EP rank (the shared expert
+    is replicated, not expert-parallel)."""
+
+    def __init__(self, gate_up: torch.Tensor, down: torch.Tensor, max_tokens: int, device):
+        self.gu, self.d = gate_up, down
+        self.Is, self.H = down.shape[1], down.shape[0]
+        self.h = torch.empty(max_tokens, self.Is, dtype=torch.bfloat16, device=device)
+        self.y = torch.empty(max_tokens, self.H, dtype=torch.bfloat16, device=device)
+        self.stream = torch.cuda.Stream(device=device)
+        self.device = device
+        self._layouts = {}
+
+    def layout(self, T: int) -> torch.Tensor:
+        """One dense group of T rows (cached per T; built before any graph capture,
+        the layers run an eager call first)."""
+        lay = self._layouts.get(T)
+        if lay is None:
+            lay = torch.from_numpy(host_layout([T], [0])[0]).to(self.device)
+            self._layouts[T] = lay
+        return lay
+
+    def start(self, x: torch.Tensor) -> None:
+        T = x.shape[0]
+        lay = self.layout(T).data_ptr()
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            sp = _lib.stream_ptr(self.stream)
+            _lib.call("realb_grouped_gemm_bf16", x.data_ptr(), self.gu.data_ptr(), T, 2 * self.Is, self.H, 1,
+                      lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.h.data_ptr(), 0, sp)
+            _lib.call("realb_grouped_gemm_bf16", self.h.data_ptr(), self.d.data_ptr(), T, self.H, self.Is, 1,
+                      lay, _lib.PREC_W16A16, _lib.EPI_STORE, self.y.data_ptr(), 0, sp)
+
+    def join(self) -> int:
+        torch.cuda.current_stream().wait_stream(self.stream)
+        return self.y.data_ptr()
+
+
 class MoELayer:
     """Executes one MoE layer for ``T`` local tokens with preallocated workspaces.
 
@@ -278,14 +319,11 @@ class MoELayer:
         self.y_buf = torch.empty(T, H, dtype=bf, device=dev)
         self._fp4 = None  # lazily allocated W4A4 workspaces
         self.side = torch.cuda.Stream(device=dev, priority=0)
+        self.shared = None
         if s.shared_intermediate:
-            Is = s.shared_intermediate
-            if Is % 128:
+            if s.shared_intermediate % 128:
                 raise ValueError("shared_intermediate must be a multiple of 128")
-            self.sh_h = torch.empty(T, Is, dtype=bf, device=dev)
-            self.sh_y = torch.empty(T, H, dtype=bf, device=dev)
-            self.sh_stream = torch.cuda.Stream(device=dev)
-            self._sh_layouts = {}
+            self.shared = SharedExpertMLP(weights.shared_gu, weights.shared_d, T, dev)
 
     # -- W4A4 workspaces (activations + quantised weights of every expert)
     def _fp4_ws(self):
@@ -350,26 +388,6 @@ class MoELayer:
                   int(bool(c.modality_isolated)), self.prec_dev.data_ptr(), self.plan_dev.data_ptr(),
                   self.layout.data_ptr(), self.expert_vt.data_ptr(), _lib.stream_ptr())
 
-    def _shared_layout(self, T: int) -> torch.Tensor:
-        """One dense group of T rows (cached per T; built before any graph capture,
-        capture() runs an eager forward first)."""
-        lay = self._sh_layouts.get(T)
-        if lay is None:
-            lay = torch.from_numpy(host_layout([T], [0])[0]).to(self.device)
-            self._sh_layouts[T] = lay
-        return lay
-
-    def shared_mlp(self, x: torch.Tensor, stream) -> None:
-        """The shared-expert MLP on every token (BF16 K5: SwiGLU gate_up, then down)
-        into self.sh_y, on `stream`."""
-        T, H, Is = x.shape[0], self.H, self.shape.shared_intermediate
-        lay = self._shared_layout(T)
-        sp = _lib.stream_ptr(stream)
-        _lib.call("realb_grouped_gemm_bf16", x.data_ptr(), self.w.shared_gu.data_ptr(), T, 2 * Is, H, 1,
-                  lay.data_ptr(), _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.sh_h.data_ptr(), 0, sp)
-        _lib.call("realb_grouped_gemm_bf16", self.sh_h.data_ptr(), self.w.shared_d.data_ptr(), T, H, Is, 1,
-                  lay.data_ptr(), _lib.PREC_W16A16, _lib.EPI_STORE, self.sh_y.data_ptr(), 0, sp)
-
     def forward(self, x: torch.Tensor, modality: torch.Tensor, strategy: str = "realb",
                 params: RealbParams | None = None, out: torch.Tensor | None = None,
                 timer=None) -> LayerResult:
@@ -390,12 +408,9 @@ class MoELayer:
         nch = (T + 63) // 64
         main = torch.cuda.current_stream()
         sp = _lib.stream_ptr(main)
-        shared = bool(self.shape.shared_intermediate) and T > 0
+        shared = self.shared is not None and T > 0
         if shared:  # overlapped with the whole routed path, joined before the combine
-            self._shared_layout(T)
-            self.sh_stream.wait_stream(main)
-            with torch.cuda.stream(self.sh_stream):
-                self.shared_mlp(x, self.sh_stream)
+            self.shared.start(x)
         self.route(x, modality)
         self.align_plan(T, strategy, params)
         # NVFP4 launches are needed unless the plan provably stays all-W16A16: the
@@ -452,11 +467,9 @@ class MoELayer:
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
         y = self.y_buf[:T] if out is None else out
-        if shared:
-            main.wait_stream(self.sh_stream)
+        addend = self.shared.join() if shared else None
         _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
-                  self.topk_w.data_ptr(), T, H, k, self.sh_y.data_ptr() if shared else None,
-                  y.data_ptr(), sp)
+                  self.topk_w.data_ptr(), T, H, k, addend, y.data_ptr(), sp)
         if torch.cuda.is_current_stream_capturing():
             return LayerResult(y, self, self.plan_host, self.expert_vt_host, None, self.placement,
                                self.cluster)

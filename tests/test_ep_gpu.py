@@ -30,10 +30,13 @@ def _setup(shape_name, E, T, world, rank, device="cuda"):
     from paper_2604_19503_b200.moe import SHAPES
     from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts
 
+    from paper_2604_19503_b200.workload import make_shared_expert
+
     shape = replace(SHAPES[shape_name], num_experts=E)
     x, mod, router, _ = make_batch(shape, WorkloadSpec(tokens=T, num_ranks=world, rank=rank), device=device)
     gu, dn = make_experts(shape, device=device)
-    return shape, x, mod, router, gu, dn
+    sh = make_shared_expert(shape, device=device)
+    return shape, x, mod, router, gu, dn, sh
 
 
 def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir, p2p=False, device_plan=False):
@@ -49,9 +52,9 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir,
     from paper_2604_19503_b200.ep import CudaEPOps, EPComm, EPMoELayer, split_weights
     from paper_2604_19503_b200.policy import RealbParams
 
-    shape, x, mod, router, gu, dn = _setup(shape_name, E, T, world, rank)
+    shape, x, mod, router, gu, dn, sh = _setup(shape_name, E, T, world, rank)
     bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
-    local = split_weights(shape, router, gu, dn, rank, world)
+    local = split_weights(shape, router, gu, dn, rank, world, shared=sh)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
     comm = EPComm(staged=True, p2p=p2p)
     if p2p:
@@ -90,7 +93,9 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir,
     ("kimi", 16, 384, "baseline", False),
     # NVFP4 rows on the wire to W4A4 ranks (§8f-1): sender-side K4 gives the receiver
     # the same codes it would compute itself, so the layer output is unchanged
-    ("kimi", 16, 384, "realb", True), ("qwen", 16, 256, "fp4all", True), ("tiny", 8, 512, "realb", True)])
+    ("kimi", 16, 384, "realb", True), ("qwen", 16, 256, "fp4all", True), ("tiny", 8, 512, "realb", True),
+    # the replicated shared expert of Kimi-VL, overlapped with the EP path
+    ("kimi_shared", 16, 384, "realb", True)])
 def test_ep2_on_one_gpu_equals_single_gpu_layer(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
     _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=False)
 
@@ -106,7 +111,7 @@ def test_ep2_peer_memory_transport_equals_single_gpu_layer(tmp_path, shape_name,
 
 @pytest.mark.parametrize("shape_name,E,T,strategy,fp4_dispatch", [
     ("kimi", 16, 384, "realb", True), ("kimi", 16, 384, "realb", False), ("qwen", 16, 256, "fp4all", True),
-    ("tiny", 8, 512, "baseline", False)])
+    ("tiny", 8, 512, "baseline", False), ("kimi_shared", 16, 384, "realb", True)])
 def test_ep2_host_sync_free_layer_and_graph(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
     """The host-sync-free EP layer: C1 through peer memory, plan and window offsets
     derived on the device, both precisions launched and selected by device-side
@@ -123,11 +128,11 @@ def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, de
     from paper_2604_19503_b200.policy import ClusterConfig, RealbParams
 
     parts = [_setup(shape_name, E, T, world, r) for r in range(world)]
-    shape, _, _, router, gu, dn = parts[0]
+    shape, _, _, router, gu, dn, sh = parts[0]
     x = torch.cat([p[1] for p in parts])
     mod = torch.cat([p[2] for p in parts])
     bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
-    single = MoELayer(MoEWeights.from_hf(shape, router, gu, dn, bias=bias), max_tokens=world * T,
+    single = MoELayer(MoEWeights.from_hf(shape, router, gu, dn, bias=bias, shared=sh), max_tokens=world * T,
                       cluster=ClusterConfig(world, 1, E // world, 1, shape.modality_isolated))
     res = single.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
     ref = res.y.float().cpu().numpy()
