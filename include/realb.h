@@ -235,7 +235,8 @@ REALB_API int realb_gather_rows_nvfp4_packed(const uint8_t* d_src, const int32_t
  * realb_p2p_signal : after this stream's earlier writes are visible system-wide,
  *                    atomically add 1 to each of the R peer counters.
  * realb_p2p_wait   : stream waits until *d_counter (acquire, system scope)
- *                    reaches target (modular uint32 compare).
+ *                    reaches target (modular uint32 compare); after 10 s without
+ *                    it, sets *d_err (if non-NULL) and gives up instead of hanging.
  * h_* are host arrays (read during the call); addresses 16-byte aligned.
  * ------------------------------------------------------------------------ */
 REALB_API int realb_ipc_alloc(int64_t bytes, void** d_ptr, uint8_t* handle64);
@@ -249,7 +250,7 @@ REALB_API int realb_p2p_pack(const void* d_x, const int32_t* d_topk_idx, int T, 
 REALB_API int realb_p2p_return(const void* d_rows, const int32_t* d_row_pos, int64_t n, int H, int R,
                                const int32_t* h_recv_prefix, const uint64_t* h_src_dst, void* stream);
 REALB_API int realb_p2p_signal(const uint64_t* h_peer_counters, int R, void* stream);
-REALB_API int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, void* stream);
+REALB_API int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, int32_t* d_err, void* stream);
 
 /* Host-sync-free form (the EP layer becomes CUDA-graph capturable):
  * realb_p2p_publish      : copy n_words int32 (my [E][2] counts) into every peer
@@ -269,7 +270,7 @@ REALB_API int64_t realb_p2p_plan_bytes(void);
 REALB_API int realb_p2p_plan_layout(int64_t* out5);
 /* graph-safe wait: *d_expected += inc, then wait until *d_counter reaches it */
 REALB_API int realb_p2p_wait_next(uint32_t* d_expected, uint32_t inc, const uint32_t* d_counter,
-                                  void* stream);
+                                  int32_t* d_err, void* stream);
 REALB_API int realb_p2p_publish(const int32_t* d_src, int n_words, int R, const uint64_t* h_peer_windows,
                                 int64_t offset_words, void* stream);
 REALB_API int realb_p2p_plan_offsets(const int32_t* d_counts, int R, int E, int rank, int H,

@@ -65,7 +65,7 @@ SIGNATURES: dict[str, tuple] = {
     "realb_gather_rows_nvfp4_packed": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_p2p_plan_bytes": (_i64, []),
     "realb_p2p_plan_layout": (_i32, [_vp]),
-    "realb_p2p_wait_next": (_i32, [_vp, _u32, _vp, _vp]),
+    "realb_p2p_wait_next": (_i32, [_vp, _u32, _vp, _vp, _vp]),
     "realb_p2p_publish": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp]),
     "realb_p2p_plan_offsets": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_p2p_pack_dev": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
@@ -78,7 +78,7 @@ SIGNATURES: dict[str, tuple] = {
                               _vp]),
     "realb_p2p_return": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "realb_p2p_signal": (_i32, [_vp, _i32, _vp]),
-    "realb_p2p_wait": (_i32, [_vp, _u32, _vp]),
+    "realb_p2p_wait": (_i32, [_vp, _u32, _vp, _vp]),
 }
 
 _lib: C.CDLL | None = None

@@ -104,17 +104,33 @@ __global__ void p2p_signal_kernel(const PeerCounters m) {
   }
 }
 
-// acquire: spin until my counter reaches `target` (all peers have signalled)
-__global__ void p2p_wait_kernel(const uint32_t* ctr, uint32_t target) {
-  if (threadIdx.x == 0) {
-    uint32_t v;
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-      if ((int32_t)(v - target) >= 0) break;
-      __nanosleep(256);
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr uint64_t kWaitTimeoutNs = 10ull * 1000 * 1000 * 1000;  // a dead peer must not hang the GPU
+
+// acquire spin until *ctr reaches target; after kWaitTimeoutNs without it, raise
+// *err (if given) and give up, so a broken transport fails loudly instead of hanging
+__device__ __forceinline__ void spin_until(const uint32_t* ctr, uint32_t target, int32_t* err) {
+  const uint64_t t0 = global_ns();
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if ((int32_t)(v - target) >= 0) break;
+    if (err && global_ns() - t0 > kWaitTimeoutNs) {
+      atomicOr(err, 1);
+      break;
     }
-    __threadfence_system();
+    __nanosleep(256);
   }
+  __threadfence_system();
+}
+
+// acquire: spin until my counter reaches `target` (all peers have signalled)
+__global__ void p2p_wait_kernel(const uint32_t* ctr, uint32_t target, int32_t* err) {
+  if (threadIdx.x == 0) spin_until(ctr, target, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -191,17 +207,11 @@ __global__ void __launch_bounds__(256) p2p_plan_kernel(const int32_t* __restrict
 
 // graph-safe wait: the expected value lives in device memory and advances by
 // `inc` (= R signals per layer) on every call, so a captured graph can replay it
-__global__ void p2p_wait_next_kernel(uint32_t* expected, uint32_t inc, const uint32_t* ctr) {
+__global__ void p2p_wait_next_kernel(uint32_t* expected, uint32_t inc, const uint32_t* ctr, int32_t* err) {
   if (threadIdx.x == 0) {
     const uint32_t target = *expected + inc;
     *expected = target;
-    uint32_t v;
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-      if ((int32_t)(v - target) >= 0) break;
-      __nanosleep(256);
-    }
-    __threadfence_system();
+    spin_until(ctr, target, err);
   }
 }
 
@@ -373,12 +383,12 @@ extern "C" int realb_p2p_signal(const uint64_t* h_peer_counters, int R, void* st
   return check_launch("realb_p2p_signal");
 }
 
-extern "C" int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, void* stream) {
+extern "C" int realb_p2p_wait(const uint32_t* d_counter, uint32_t target, int32_t* d_err, void* stream) {
   if (!d_counter) {
     set_error("realb_p2p_wait: bad arguments");
     return REALB_EINVAL;
   }
-  p2p_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_counter, target);
+  p2p_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_counter, target, d_err);
   return check_launch("realb_p2p_wait");
 }
 
@@ -469,12 +479,12 @@ extern "C" int realb_p2p_return_dev(const void* d_rows, const int32_t* d_row_pos
 }
 
 extern "C" int realb_p2p_wait_next(uint32_t* d_expected, uint32_t inc, const uint32_t* d_counter,
-                                   void* stream) {
+                                   int32_t* d_err, void* stream) {
   if (!d_expected || !d_counter) {
     set_error("realb_p2p_wait_next: bad arguments");
     return REALB_EINVAL;
   }
-  p2p_wait_next_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_expected, inc, d_counter);
+  p2p_wait_next_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_expected, inc, d_counter, d_err);
   return check_launch("realb_p2p_wait_next");
 }
 

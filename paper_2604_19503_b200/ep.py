@@ -273,6 +273,7 @@ class CudaEPOps:
         self.plan_layout = list(lay)
         self.d_plan = torch.zeros(int(lay[0]) + 64, dtype=torch.uint8, device=dev)
         self.d_expected = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.p2p_err = torch.zeros(1, dtype=torch.int32, device=dev)  # set by a timed-out wait
         self.prec_global = torch.zeros(E, dtype=torch.uint8, device=dev)
         self.plan_out = torch.zeros(3 + R, dtype=torch.int32, device=dev)
         self.plan_host = torch.zeros(3 + R, dtype=torch.int32, pin_memory=True)
@@ -319,7 +320,8 @@ class CudaEPOps:
         ctrs = np.array([self.p2p["ctr"][d] + ctr_off for d in range(R)], np.uint64)
         sp = _lib.stream_ptr()
         _lib.call("realb_p2p_signal", ctrs.ctypes.data, R, sp)
-        _lib.call("realb_p2p_wait", self._p2p_own["ctr"] + ctr_off, (self.p2p_epoch * R) & 0xFFFFFFFF, sp)
+        _lib.call("realb_p2p_wait", self._p2p_own["ctr"] + ctr_off, (self.p2p_epoch * R) & 0xFFFFFFFF,
+                  self.p2p_err.data_ptr(), sp)
 
     def forward_device(self, x, mod, strategy: str, params: RealbParams, fp4_dispatch: bool,
                        timer=None):
@@ -425,7 +427,7 @@ class CudaEPOps:
         sp = _lib.stream_ptr()
         _lib.call("realb_p2p_signal", ctrs.ctypes.data, R, sp)
         _lib.call("realb_p2p_wait_next", self.d_expected.data_ptr() + 4 * slot, R,
-                  self._p2p_own["ctr"] + ctr_off, sp)
+                  self._p2p_own["ctr"] + ctr_off, self.p2p_err.data_ptr(), sp)
 
     def close_p2p(self):
         torch.cuda.synchronize()
@@ -636,11 +638,15 @@ def run_bench(args):
     # "p2p-gloo": validation modes for a one-GPU box (all ranks share cuda:0, C1
     # (and C2/C3 for "gloo") staged through the host).
     # "p2p-graph" / "p2p-graph-gloo": the host-sync-free layer (device plan) replayed as
-    # one CUDA graph per step
-    mode = os.environ.get("REALB_EP_COMM", "nccl")
-    staged = mode in ("gloo", "p2p-gloo", "p2p-graph-gloo")
-    p2p = mode in ("p2p", "p2p-gloo", "p2p-graph", "p2p-graph-gloo")
-    graph = mode in ("p2p-graph", "p2p-graph-gloo")
+    # one CUDA graph per step. "auto" (default) / "auto-gloo": set up the peer-memory
+    # transport, check on this very box that one host-sync-free layer call equals the
+    # NCCL path bit for bit (and that no wait timed out) on every rank, and use it if
+    # so; otherwise fall back to the NCCL path. The line reports which one ran.
+    mode = os.environ.get("REALB_EP_COMM", "auto")
+    staged = mode in ("gloo", "p2p-gloo", "p2p-graph-gloo", "auto-gloo")
+    auto = mode in ("auto", "auto-gloo")
+    p2p = mode in ("p2p", "p2p-gloo", "p2p-graph", "p2p-graph-gloo") or auto
+    graph = mode in ("p2p-graph", "p2p-graph-gloo") or auto
     if staged:
         torch.cuda.set_device(0)
         dist.init_process_group("gloo")
@@ -659,11 +665,34 @@ def run_bench(args):
     del gu, dn
     comm = EPComm(staged=staged, p2p=p2p)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
-    if p2p:
-        ops.setup_p2p(comm)
     fp4_dispatch = not getattr(args, "bf16_dispatch", False)
-    layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
     dev_t = "cpu" if staged else "cuda"
+    transport_check = None
+    if p2p:
+        try:
+            ops.setup_p2p(comm)
+        except Exception as e:  # no peer mapping on this box: the collective path
+            if not auto:
+                raise
+            p2p = graph = False
+            comm = EPComm(staged=staged, p2p=False)
+            transport_check = f"peer-memory setup failed ({type(e).__name__}): NCCL path"
+    layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
+    if auto and p2p:
+        ref_layer = EPMoELayer(shape, EPComm(staged=staged, p2p=False), ops, fp4_dispatch=fp4_dispatch)
+        y_ref, _, _ = ref_layer.forward(x, mod, "realb")
+        y_ref = y_ref.clone()
+        y_dev, _ = layer.forward_device(x, mod, "realb")
+        torch.cuda.synchronize()
+        ok = torch.tensor([int(torch.equal(y_ref, y_dev) and int(ops.p2p_err.item()) == 0)], device=dev_t)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()):
+            transport_check = "host-sync-free peer-memory layer == NCCL layer bit for bit on every rank"
+        else:
+            transport_check = "peer-memory layer differed from the NCCL layer (or a wait timed out): NCCL path"
+            p2p = graph = False
+            layer = ref_layer
+            comm = layer.comm
 
     def max_over_ranks(v: float) -> float:
         t = torch.tensor([v], dtype=torch.float64, device=dev_t)
@@ -789,13 +818,13 @@ def run_bench(args):
                "rank_phases_ns": {s: [dict(zip(names, r)) for r in rows] for s, rows in phases.items()},
                "gpu_launches": int(launches),
                "clocks": clk.summary(),
-               "comm": {"nccl": "nccl", "p2p": "peer-memory windows (CUDA IPC / NVLink), NCCL for C1",
-                        "p2p-graph": "peer-memory windows incl. C1, device plan, one CUDA graph per layer",
-                        "p2p-graph-gloo": "p2p-graph with ranks sharing one GPU (validation only)",
-                        "gloo": "gloo-staged on one shared GPU (validation only)",
-                        "p2p-gloo": "peer-memory windows on one shared GPU, gloo for C1 (validation only)"}[mode]}
+               "comm": ("peer-memory windows incl. C1, device plan, one CUDA graph per layer" if graph else
+                        "peer-memory windows (CUDA IPC / NVLink), host plan" if p2p else
+                        "gloo-staged all-to-alls" if staged else "nccl all-to-alls")
+                       + (" — ranks share one GPU (validation only)" if staged else ""),
+               "transport_check": transport_check}
         print(json.dumps(out), flush=True)
-    if p2p:
+    if getattr(ops, "_p2p_own", None):
         dist.barrier()
         ops.close_p2p()
     dist.destroy_process_group()
