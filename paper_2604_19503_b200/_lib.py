@@ -70,6 +70,8 @@ SIGNATURES: dict[str, tuple] = {
     "realb_p2p_plan_offsets": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_p2p_pack_dev": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_p2p_return_dev": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "realb_p2p_pack_direct": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp]),
     "realb_ipc_alloc": (_i32, [_i64, _vp, _vp]),
     "realb_ipc_open": (_i32, [_vp, _vp]),
     "realb_ipc_close": (_i32, [_vp]),
@@ -93,7 +95,7 @@ LAUNCHES_KERNEL = {
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
     "realb_p2p_pack": 2, "realb_p2p_return": 1, "realb_p2p_signal": 1, "realb_p2p_wait": 1,
     "realb_p2p_publish": 1, "realb_p2p_plan_offsets": 1, "realb_p2p_pack_dev": 2, "realb_p2p_return_dev": 1,
-    "realb_p2p_wait_next": 1,
+    "realb_p2p_wait_next": 1, "realb_p2p_pack_direct": 2,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 

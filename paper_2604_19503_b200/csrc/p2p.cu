@@ -147,6 +147,9 @@ struct P2PPlan {
   int32_t n_recv;                // rows I receive (= recv0[R])
   int32_t w4a4;                  // my precision (W4A4 = 1)
   int32_t gate_bf16, gate_packed;  // which receive-side gather runs
+  // direct dispatch: grouped row (the owner's GEMM operand row space, 128-padded
+  // per expert, source-major inside an expert) of MY first row of each global expert
+  int32_t gpos0[256];
 };
 
 __global__ void p2p_publish_kernel(const int32_t* __restrict__ src, int n, const PeerRows dst,
@@ -198,6 +201,22 @@ __global__ void __launch_bounds__(256) p2p_plan_kernel(const int32_t* __restrict
     }
     plan->recv0[R] = pr;
     plan->n_recv = pr;
+    // the owner's grouped layout (ep_layout_kernel's rule: experts in order, each
+    // padded to 128 rows, sources in rank order inside an expert)
+    for (int d = 0; d < R; ++d) {
+      int32_t start = 0;
+      for (int le = 0; le < El; ++le) {
+        const int e = d * El + le;
+        int32_t tot = 0, before = 0;
+        for (int s2 = 0; s2 < R; ++s2) {
+          const int32_t c = counts[(s2 * E + e) * 2] + counts[(s2 * E + e) * 2 + 1];
+          tot += c;
+          if (s2 < rank) before += c;
+        }
+        plan->gpos0[e] = start + before;
+        start += (tot + 127) / 128 * 128;
+      }
+    }
     const int w4 = prec[rank * El] == REALB_PREC_W4A4;
     plan->w4a4 = w4;
     plan->gate_packed = w4 && fp4_dispatch;
@@ -252,6 +271,58 @@ __global__ void __launch_bounds__(256) p2p_pack_dev_kernel(const __nv_bfloat16* 
         cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
         cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
         reinterpret_cast<uint32_t*>(row + H / 2)[g] = sfw;
+      }
+    }
+  }
+}
+
+struct PeerOperands {
+  __nv_bfloat16* a[kMaxPeers];  // peer d's bf16 GEMM operand rows [rows_cap][H]
+  uint8_t* codes[kMaxPeers];    // peer d's NVFP4 operand codes [rows_cap][H/2]
+  uint8_t* sf[kMaxPeers];       // peer d's NVFP4 operand scales (MMA 128x4 layout)
+  int R, El;
+};
+
+// Direct dispatch: every (token, slot) row is written straight into its
+// destination's GEMM operand at its final grouped row — bf16 for a W16A16
+// destination, NVFP4 codes + MMA-layout scales (the K4 rule) for a W4A4 one —
+// so the receiver runs no gather at all.
+__global__ void __launch_bounds__(256) p2p_pack_direct_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const int32_t* __restrict__ topk_idx,
+                                                              const int32_t* __restrict__ pair_pos,
+                                                              const int32_t* __restrict__ send_start,
+                                                              int64_t P, int H, int k, const PeerOperands ops,
+                                                              const P2PPlan* __restrict__ plan, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int nkb = H / 16;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = p / k;
+    const int e = topk_idx[p];
+    const int d = e / ops.El;
+    const int64_t g = (int64_t)plan->gpos0[e] + (pair_pos[p] - send_start[e]);
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+    if (plan->fmt[d] == 0) {
+      uint4* o = reinterpret_cast<uint4*>(ops.a[d] + g * H);
+      for (int i = lane; i < H / 8; i += 32) o[i] = __ldg(src + i);
+    } else {
+      for (int gi = lane; gi < nkb / 4; gi += 32) {
+        uint32_t sfw = 0;
+        uint2 cw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint4 u0 = __ldg(src + (gi * 4 + b) * 2), u1 = __ldg(src + (gi * 4 + b) * 2 + 1);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          uint32_t sb;
+          bool nf;
+          cw[b] = quant_block16_bf16(w, sb, nf);
+          if (nf && flag) atomicOr(flag, 1);
+          sfw |= sb << (8 * b);
+        }
+        uint4* cdst = reinterpret_cast<uint4*>(ops.codes[d] + g * (H / 2) + gi * 32);
+        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
+        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
+        *reinterpret_cast<uint32_t*>(ops.sf[d] + sf_mma_offset(g, (int64_t)gi * 4, nkb)) = sfw;
       }
     }
   }
@@ -497,4 +568,38 @@ extern "C" int realb_p2p_plan_layout(int64_t* out5) {
   out5[3] = (int64_t)offsetof(P2PPlan, gate_bf16);
   out5[4] = (int64_t)offsetof(P2PPlan, gate_packed);
   return REALB_OK;
+}
+
+extern "C" int realb_p2p_pack_direct(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                                     const int32_t* d_layout, int nchunks, int R, const uint64_t* h_peer_a,
+                                     const uint64_t* h_peer_codes, const uint64_t* h_peer_sf,
+                                     const void* d_plan, int32_t* d_pair_pos, int32_t* d_flag, void* stream) {
+  if (T == 0 && nchunks == 0) return REALB_OK;
+  if (!d_x || !d_topk_idx || !d_layout || !d_plan || !d_pair_pos || !h_peer_a || !h_peer_codes || !h_peer_sf ||
+      T < 0 || H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || R < 1 || R > kMaxPeers || E % R ||
+      nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
+    set_error("realb_p2p_pack_direct: bad arguments (T=%d H=%d E=%d k=%d R=%d)", T, H, E, k, R);
+    return REALB_EINVAL;
+  }
+  PeerOperands o{};
+  o.R = R;
+  o.El = E / R;
+  for (int d = 0; d < R; ++d) {
+    if ((h_peer_a[d] | h_peer_codes[d]) & 15 || h_peer_sf[d] & 3) {
+      set_error("realb_p2p_pack_direct: peer %d operand addresses misaligned", d);
+      return REALB_EINVAL;
+    }
+    o.a[d] = reinterpret_cast<__nv_bfloat16*>(h_peer_a[d]);
+    o.codes[d] = reinterpret_cast<uint8_t*>(h_peer_codes[d]);
+    o.sf[d] = reinterpret_cast<uint8_t*>(h_peer_sf[d]);
+  }
+  int rc = ep_positions(d_topk_idx, T, E, k, d_layout, nchunks, d_pair_pos, stream);
+  if (rc) return rc;
+  const int64_t P = (int64_t)T * k;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  p2p_pack_direct_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, d_layout + 8, P, H, k, o,
+      reinterpret_cast<const P2PPlan*>(d_plan), d_flag);
+  return check_launch("realb_p2p_pack_direct");
 }

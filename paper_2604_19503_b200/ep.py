@@ -243,7 +243,10 @@ class CudaEPOps:
         import ctypes as Cty
 
         R, H, T, k, E = self.R, self.H, self.T, self.k, self.E
-        sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256, "cnt": R * E * 2 * 4}
+        rc = self.rows_cap
+        sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256, "cnt": R * E * 2 * 4,
+                 # the GEMM operands themselves, written directly by the senders (device-plan path)
+                 "opa": rc * H * 2, "opc": rc * (H // 2), "ops": rc * (H // 16)}
         self._p2p_own, handles = {}, {}
         for name, nbytes in sizes.items():
             ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
@@ -265,6 +268,8 @@ class CudaEPOps:
                     self._p2p_opened.append(ptr.value)
         self.p2p_epoch = 0
         self.p2p_rank = comm.rank
+        # peers' operand bases (kept alive: the ABI reads them through a host pointer)
+        self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "ops")]
         # host-sync-free (device-plan) form: plan record, expected-counter words,
         # global expert precisions and the plan kernel's scratch
         dev = self.dev
@@ -328,8 +333,10 @@ class CudaEPOps:
         """The whole EP layer with no host synchronisation (CUDA-graph capturable):
         C1 through peer memory, the plan and every window offset derived on the
         device (realb_moe_align_plan over the gathered [R][E][2] counts,
-        realb_p2p_plan_offsets), K3 / gathers / both GEMM precisions launched
-        unconditionally and selected by device-side group lists and gates.
+        realb_p2p_plan_offsets), rows dispatched straight into the destinations'
+        GEMM operands (NVFP4 towards W4A4 ranks, so the receivers run no gather),
+        K3 and both GEMM precisions launched unconditionally and selected by the
+        device-side group lists.
         -> y; the plan and counts are read back lazily (DevicePlanResult)."""
         from .moe import _STRATEGY_CODE
 
@@ -351,7 +358,8 @@ class CudaEPOps:
                   int(params.global_batch_threshold), int(bool(self.s.modality_isolated)),
                   self.prec_global.data_ptr(), self.plan_out.data_ptr(), self.gl_layout.data_ptr(),
                   self.gl_vt.data_ptr(), sp)
-        _lib.call("realb_p2p_plan_offsets", self.p2p["cnt"][r], R, E, r, H, int(bool(fp4_dispatch)),
+        # fp4_dispatch=1: direct dispatch always hands a W4A4 rank its NVFP4 operand
+        _lib.call("realb_p2p_plan_offsets", self.p2p["cnt"][r], R, E, r, H, 1,
                   self.prec_global.data_ptr(), self.d_plan.data_ptr(), self.cnt_dev.data_ptr(),
                   self.prec_local.data_ptr(), sp)
         mark("schedule")
@@ -366,33 +374,30 @@ class CudaEPOps:
             _lib.call("realb_quantize_experts_nvfp4", self.local.w_d.data_ptr(), El, H, I,
                       self.prec_local.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
                       self.flag.data_ptr(), self.quant_max_ctas, ssp)
-        # C2
-        recv_bases = np.array(self.p2p["recv"], np.uint64)
-        _lib.call("realb_p2p_pack_dev", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
-                  self.send_layout.data_ptr(), (T + 63) // 64, R, recv_bases.ctypes.data, self.d_plan.data_ptr(),
+        # C2, direct: every row lands in its destination's GEMM operand at its final
+        # grouped row (bf16, or NVFP4 + MMA-layout scales for a W4A4 destination)
+        _lib.call("realb_p2p_pack_direct", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
+                  self.send_layout.data_ptr(), (T + 63) // 64, R,
+                  self.op_bases[0].ctypes.data, self.op_bases[1].ctypes.data, self.op_bases[2].ctypes.data,
+                  self.d_plan.data_ptr(),
                   self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
         self._signal_wait_dev(0, 0)
         mark("dispatch")
-        # receive side: regroup, then exactly one of the two gathers runs (device gates)
+        # receive side: only the grouped layout and the row map for the return (no row copies)
         cap = self.recv_cap
         _lib.call("realb_ep_regroup", self.cnt_dev.data_ptr(), R, El, self.prec_local.data_ptr(), cap,
                   self.local_layout.data_ptr(), self.base.data_ptr(), self.row_expert.data_ptr(),
                   self.row_pos.data_ptr(), sp)
         pl = self.d_plan.data_ptr()
-        n_ptr, g16, gpk = pl + self.plan_layout[1], pl + self.plan_layout[3], pl + self.plan_layout[4]
-        _lib.call("realb_gather_rows", self.p2p["recv"][r], self.row_expert.data_ptr(), self.row_pos.data_ptr(),
-                  cap, H, 1, self.prec_local.data_ptr(), self.a_bf16.data_ptr(), ws["a_codes"].data_ptr(),
-                  ws["a_sf"].data_ptr(), self.flag.data_ptr(), n_ptr, g16, sp)
-        _lib.call("realb_gather_rows_nvfp4_packed", self.p2p["recv"][r], self.row_pos.data_ptr(), cap, H,
-                  ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(), n_ptr, gpk, sp)
+        a_bf16, a_codes, a_sf = self.p2p["opa"][r], self.p2p["opc"][r], self.p2p["ops"][r]
         # both precisions' GEMMs; each runs only the groups the device plan gave it
         lay = self.local_layout.data_ptr()
-        _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.local.w_gu.data_ptr(), self.rows_cap,
+        _lib.call("realb_grouped_gemm_bf16", a_bf16, self.local.w_gu.data_ptr(), self.rows_cap,
                   2 * I, H, El, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.h_bf16.data_ptr(), 0, sp)
         _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.local.w_d.data_ptr(), self.rows_cap,
                   H, I, El, lay, _lib.PREC_W16A16, _lib.EPI_STORE, self.rows_out.data_ptr(), 0, sp)
         main.wait_stream(self.side)
-        _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
+        _lib.call("realb_grouped_gemm_nvfp4", a_codes, a_sf,
                   ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, El, lay,
                   _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
         _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
