@@ -227,9 +227,7 @@ def roofline_gate_up(torch, layer, x, mod, shape, args):
     for _ in range(max(5, args.steps)):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        _lib.call("realb_grouped_gemm_bf16", layer.a_bf16.data_ptr(), layer.w.w_gu.data_ptr(), layer.rows_cap,
-                  2 * I, H, E, layer.layout.data_ptr(), _lib.PREC_W16A16, _lib.EPI_SWIGLU,
-                  layer.h_bf16.data_ptr(), 0, sp)
+        layer._gate_up_bf16(layer.layout.data_ptr(), sp)  # the layer's own launch (gather form)
         e.record()
         e.synchronize()
         durs.append(s.elapsed_time(e))
@@ -244,7 +242,9 @@ def roofline_gate_up(torch, layer, x, mod, shape, args):
             traffic = json.loads(tf.read_text()).get(f"gate_up_{args.config}_{T}")
         except Exception:
             traffic = None
-    return {"kernel": "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)", "bound": "tensor",
+    kname = ("realb_grouped_gemm_bf16_gather (K5 gate_up, TMA gather4 rows of x, SwiGLU epilogue)"
+             if layer.gather_dispatch else "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)")
+    return {"kernel": kname, "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": f"{src} bf16_tflops (burst)",
             "algorithmic_flops_per_launch": flops, "launch_ms": t * 1e3}

@@ -170,6 +170,16 @@ REALB_API int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx,
                            int32_t* d_pair_pos, void* d_a_bf16, uint8_t* d_a_codes,
                            uint8_t* d_a_sf, int32_t* d_nonfinite_flag, void* stream);
 
+/* realb_dispatch_permute without the W16A16 row copy: positions, plus the
+ * inverse map d_row_src [rows_cap] (grouped row -> token; entries of padding
+ * rows are not written) for realb_grouped_gemm_bf16_gather. Rows of W4A4 experts
+ * are still quantised into d_a_codes / d_a_sf (both NULL: none is W4A4). */
+REALB_API int realb_dispatch_index(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                                   const uint8_t* d_expert_prec, const int32_t* d_layout, int nchunks,
+                                   int64_t rows_cap, int32_t* d_pair_pos, int32_t* d_row_src,
+                                   uint8_t* d_a_codes, uint8_t* d_a_sf, int32_t* d_nonfinite_flag,
+                                   void* stream);
+
 /* The row-movement half of realb_dispatch_permute, exposed for the EP
  * receive side: row p of x (token p / k) goes to position d_pos[p] of the
  * grouped space as bf16 or, when d_prec[d_expert[p]] is W4A4, as NVFP4 (K4). */
@@ -314,6 +324,16 @@ REALB_API int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t 
 REALB_API int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t rows_cap,
                             int N, int K, int E, const int32_t* d_layout, int prec,
                             int epilogue, void* d_out, int max_ctas, void* stream);
+
+/* K5, gather form: the A operand is the token matrix itself. Grouped row g of
+ * the layout reads x[d_row_src[g]] (bf16 [n_src][K]) through TMA tile::gather4;
+ * rows past a group's count are zero. With realb_dispatch_index this replaces
+ * realb_dispatch_permute's row copy for W16A16 experts (the dispatch half of
+ * moesim's dispatch term, costmodel.py:71-76, done inside the GEMM's loads). */
+REALB_API int realb_grouped_gemm_bf16_gather(const void* d_x, int64_t n_src, const int32_t* d_row_src,
+                                             const void* d_w, int64_t rows_cap, int N, int K, int E,
+                                             const int32_t* d_layout, int prec, int epilogue, void* d_out,
+                                             int max_ctas, void* stream);
 
 /* K6 — grouped NVFP4 x NVFP4 GEMM (tcgen05 kind::mxf4nvf4.block_scale,
  * scale_vec::4X, UE4M3 scales in REALB_SF_MMA128x4 layout) over the W4A4

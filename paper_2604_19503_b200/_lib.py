@@ -56,6 +56,10 @@ SIGNATURES: dict[str, tuple] = {
     "realb_dispatch_permute": (
         _i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "realb_grouped_gemm_bf16": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]),
+    "realb_grouped_gemm_bf16_gather": (
+        _i32, [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]),
+    "realb_dispatch_index": (
+        _i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "realb_grouped_gemm_nvfp4": (
         _i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _vp]),
     "realb_combine": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
@@ -90,7 +94,8 @@ LAUNCHES_KERNEL = {
     "realb_dispatch_permute": 2,
     "realb_quantize_nvfp4": 1, "realb_router_topk_stats": 1, "realb_moe_align": 1,
     "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
-    "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_nvfp4": 1, "realb_combine": 1,
+    "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_bf16_gather": 1, "realb_grouped_gemm_nvfp4": 1,
+    "realb_dispatch_index": 1,  # + 1 when NVFP4 rows are quantised (call() adds it) "realb_combine": 1,
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
     "realb_p2p_pack": 2, "realb_p2p_return": 1, "realb_p2p_signal": 1, "realb_p2p_wait": 1,
@@ -128,6 +133,8 @@ def call(name: str, *args) -> int:
     if st < 0:
         raise RealbError(name, st, lib.realb_last_error().decode(errors="replace"))
     launch_count += LAUNCHES_KERNEL.get(name, 0)
+    if name == "realb_dispatch_index" and args[12] is not None and args[2] > 0:
+        launch_count += 1
     return st
 
 

@@ -13,6 +13,16 @@
 //   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> (SwiGLU) -> bf16
 //               -> global; each warp owns TMEM lane quadrant (warp % 4)
 // Roofline: tensor-bound, 2*M*N*K flop per tile.
+//
+// Gather form (realb_grouped_gemm_bf16_gather): A is not a grouped operand but
+// the token matrix x itself; grouped row g reads x[row_src[g]]. Warps 2-3 load
+// the A tile with 16-B cp.async.cg (each warp 64 rows; lane -> 16-B piece of a
+// row, stored at its SWIZZLE_128B position) and signal the stage's full barrier
+// with cp.async.mbarrier.arrive.noinc; warp 0 keeps the W tile on TMA. Rows past
+// the m-block's valid count are zero-filled (src-size 0). This removes the
+// dispatch row copy (2H B written + re-read per pair) and keeps the x rows, read
+// up to k times, L2-resident. (TMA tile::gather4 gives the same smem image but
+// was measured 2.4x slower here: 32 gather4 per 16 KB stage, ~77 cycles each.)
 #include <cstdlib>
 
 #include "common.cuh"
@@ -61,12 +71,23 @@ __device__ __forceinline__ void stage_row64(uint32_t buf, int r, const uint32_t 
 //   operand bytes in flight (TMA-only time 0.38 of 0.49 ms on the 1-GPU gate_up).
 //   Both CTAs' loads complete on the leader's full barrier; the leader's
 //   multicast commits release both CTAs' stages and publish both accumulators.
-template <int BN, int STAGES, int EPI, int CL>
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+constexpr int kGatherWarps = 2;  // warps 2..3 load A in the gather form
+
+template <int BN, int STAGES, int EPI, int CL, bool GATHER>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut, const int32_t* layout,
-                             int E, int prec, int N, int K, uint32_t dbg) {
+                             int E, int prec, int N, int K, uint32_t dbg,
+                             const __nv_bfloat16* __restrict__ xsrc, const int32_t* __restrict__ row_src) {
+  static_assert(!GATHER || CL == 1, "the gather form is 1-CTA only");
   using S = SmemBf16<BN, STAGES, CL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -88,14 +109,15 @@ __global__ void __launch_bounds__(256, 1)
   constexpr uint16_t kBoth = 0x3;
   // consumers of a tile-id slot: 1-CTA: MMA + 4 epilogue warps; pair: leader MMA +
   // 4 leader epilogue warps + peer producer + 4 peer epilogue warps
-  constexpr uint32_t kSlotConsumers = CL == 2 ? 10 : 5;
+  // gather form: + the two A-loader warps
+  constexpr uint32_t kSlotConsumers = CL == 2 ? 10 : (GATHER ? 5 + kGatherWarps : 5);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmOut);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], GATHER ? 1 + 32 * kGatherWarps : 1);  // gather: + one noinc arrive per loader lane
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -172,7 +194,12 @@ __global__ void __launch_bounds__(256, 1)
       dummy1 = __shfl_sync(0xffffffffu, (int)dummy1, 0) != 0;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        if (leader) {
+        if constexpr (GATHER) {  // W only; A comes from the loader warps
+          if (leader) {
+            mbar_arrive_expect_tx(&full[stage], S::B_BYTES);
+            tma_load_2d(smem + stage * S::STAGE_BYTES + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
+          }
+        } else if (leader) {
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
           if constexpr (CL == 2) {
             const uint32_t fb = full0 + (uint32_t)stage * 8u;
@@ -213,6 +240,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t dtmem = tbase + acc * BN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
+        if constexpr (GATHER) fence_proxy_async_smem();  // cp.async (generic proxy) -> MMA reads
         tc_fence_after();
         const uint64_t soff = (uint64_t)((uint32_t)(stage * S::STAGE_BYTES) >> 4);
         if (leader) {
@@ -236,6 +264,45 @@ __global__ void __launch_bounds__(256, 1)
         else tc_commit(&tfull[acc]);
       }
       __syncwarp();
+    }
+  } else if (GATHER && (warp == 2 || warp == 3)) {  // ---------------- A loaders (gather form)
+    // warp w loads rows 64(w-2) .. +63 of the m-block: instruction i covers rows
+    // 4i + lane/8 (16-B piece lane%8 of each), 16 instructions per k-block
+    const int rsub = lane >> 3, piece = lane & 7;
+    const int rbase = (warp - 2) * 64;
+    const uint32_t s0 = smem_u32(smem);
+    const int64_t ldx = K;  // x row stride (elements)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0;; ++i) {
+      const int slot = i % kTileRing;
+      mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
+      const int t = slot_tile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[slot]);
+      if (t < 0) break;
+      bool dummy;
+      const TileCoord c = tile_of(t, 0, dummy);
+      const __nv_bfloat16* src[16];
+      uint32_t nbytes = 0;  // bit j: row of instruction j is real
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int r = rbase + 4 * j + rsub;
+        const bool ok = r < c.valid;
+        src[j] = xsrc + (ok ? (int64_t)__ldg(row_src + c.a_row + r) * ldx : 0) + piece * 8;
+        nbytes |= (ok ? 1u : 0u) << j;
+      }
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t sa = s0 + stage * S::STAGE_BYTES;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int r = rbase + 4 * j + rsub;
+          cp_async_16(sa + r * 128 + ((piece ^ (r & 7)) << 4), src[j] + kb * kBK, ((nbytes >> j) & 1u) * 16u);
+        }
+        cp_async_arrive_noinc(&full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
     }
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> smem -> TMA store
     const int q = warp & 3;  // TMEM lane quadrant = 32-row slice of this CTA's 128 rows
@@ -313,13 +380,14 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) GroupedSched::finish(layout, prec);
 }
 
-template <int BN, int STAGES, int EPI, int CL>
+template <int BN, int STAGES, int EPI, int CL, bool GATHER = false>
 static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, int N, int K, int E,
                                const int32_t* layout, int prec, void* out, int max_ctas,
-                               cudaStream_t st) {
+                               cudaStream_t st, const int32_t* row_src = nullptr) {
   CUtensorMap ta, tb, to;
-  int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a, K, rows_cap, (uint64_t)K * 2, kBK,
-                        kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  // gather form: A is read by the loader warps (the A map is unused, built over x)
+  int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a, K, GATHER ? 1 : rows_cap, (uint64_t)K * 2,
+                        kBK, GATHER ? 1 : kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, K, (uint64_t)E * N, (uint64_t)K * 2,
                     kBK, BN / CL, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -328,7 +396,7 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, NO, rows_cap, (uint64_t)NO * 2, 32,
                     32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
-  auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL>;
+  auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL, GATHER>;
   const int smem = SmemBf16<BN, STAGES, CL>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_bf16: smem attribute");
   if (rc) return rc;
@@ -350,7 +418,8 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  rc = cuda_status(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, layout, E, prec, N, K, dbg),
+  rc = cuda_status(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, layout, E, prec, N, K, dbg,
+                                      reinterpret_cast<const __nv_bfloat16*>(a), row_src),
                    "realb_grouped_gemm_bf16 launch");
   if (rc) return rc;
   return check_launch("realb_grouped_gemm_bf16");
@@ -393,5 +462,29 @@ extern "C" int realb_grouped_gemm_bf16(const void* d_a, const void* d_w, int64_t
                 : launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 1>(d_a, d_w, rows_cap, N, K, E,
                                                                     d_layout, prec, d_out, max_ctas, st);
   set_error("realb_grouped_gemm_bf16: unknown epilogue %d", epilogue);
+  return REALB_EINVAL;
+}
+
+extern "C" int realb_grouped_gemm_bf16_gather(const void* d_x, int64_t n_src, const int32_t* d_row_src,
+                                              const void* d_w, int64_t rows_cap, int N, int K, int E,
+                                              const int32_t* d_layout, int prec, int epilogue, void* d_out,
+                                              int max_ctas, void* stream) {
+  if (!d_x || !d_row_src || !d_w || !d_layout || !d_out || n_src <= 0 || n_src >= (1LL << 31) - 1 ||
+      rows_cap <= 0 || E <= 0 || (prec != REALB_PREC_W16A16 && prec != REALB_PREC_W4A4)) {
+    set_error("realb_grouped_gemm_bf16_gather: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (K % kBK || N % 256) {
+    set_error("realb_grouped_gemm_bf16_gather: needs K %% 64 == 0 and N %% 256 == 0 (N=%d K=%d)", N, K);
+    return REALB_EUNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (epilogue == REALB_EPI_STORE)
+    return launch_grouped_bf16<256, 4, REALB_EPI_STORE, 1, true>(d_x, d_w, rows_cap, N, K, E, d_layout, prec,
+                                                                 d_out, max_ctas, st, d_row_src);
+  if (epilogue == REALB_EPI_SWIGLU)
+    return launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 1, true>(d_x, d_w, rows_cap, N, K, E, d_layout, prec,
+                                                                  d_out, max_ctas, st, d_row_src);
+  set_error("realb_grouped_gemm_bf16_gather: unknown epilogue %d", epilogue);
   return REALB_EINVAL;
 }

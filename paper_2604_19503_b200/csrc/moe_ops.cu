@@ -173,7 +173,8 @@ constexpr int kPermWarps = 8;
 
 __global__ void __launch_bounds__(256) permute_kernel(
     const int32_t* __restrict__ topk_idx, int T, int E, int k,
-    const int32_t* __restrict__ layout, int32_t* __restrict__ pair_pos) {
+    const int32_t* __restrict__ layout, int32_t* __restrict__ pair_pos,
+    int32_t* __restrict__ row_src = nullptr) {
   extern __shared__ int32_t sm[];
   int32_t* s_base = sm;                       // [E]
   int32_t* s_cnt = s_base + E;                // [kPermWarps][E]
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(256) permute_kernel(
     const int pos = s_cnt[(p / seg) * E + e] + s_pos[p];
     s_pos[p] = pos;
     pair_pos[(int64_t)t0 * k + p] = pos;
+    if (row_src) row_src[pos] = t0 + p / k;  // inverse map for the gather-form GEMM
   }
   __syncthreads();
 }
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
     const int64_t pos = pair_pos[p];
     const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
     if (prec[e] == REALB_PREC_W16A16) {
+      if (!a_bf16) continue;  // the gather-form GEMM reads these rows from x itself
       uint4* dst = reinterpret_cast<uint4*>(a_bf16 + pos * H);
       for (int i = lane; i < H / 8; i += 32) dst[i] = __ldg(src + i);
     } else {
@@ -581,6 +584,33 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
       reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, d_prec,
       reinterpret_cast<__nv_bfloat16*>(d_a_bf16), d_a_codes, d_a_sf, d_flag, nullptr, nullptr);
   return check_launch("realb_dispatch_permute (rows)");
+}
+
+extern "C" int realb_dispatch_index(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                                    const uint8_t* d_prec, const int32_t* d_layout, int nchunks,
+                                    int64_t rows_cap, int32_t* d_pair_pos, int32_t* d_row_src,
+                                    uint8_t* d_a_codes, uint8_t* d_a_sf, int32_t* d_flag, void* stream) {
+  if (T == 0 && nchunks == 0) return REALB_OK;
+  if (!d_x || !d_topk_idx || !d_prec || !d_layout || !d_pair_pos || !d_row_src || (!d_a_codes != !d_a_sf) ||
+      T < 0 || H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || rows_cap < (int64_t)T * k ||
+      nchunks != (T + REALB_CHUNK_TOKENS - 1) / REALB_CHUNK_TOKENS) {
+    set_error("realb_dispatch_index: bad arguments (T=%d H=%d E=%d k=%d nchunks=%d)", T, H, E, k, nchunks);
+    return REALB_EINVAL;
+  }
+  if (T == 0) return REALB_OK;
+  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout, d_pair_pos,
+                                                                d_row_src);
+  int rc = check_launch("realb_dispatch_index (positions)");
+  if (rc || !d_a_codes) return rc;
+  // only the rows of W4A4 experts move (K4 quantisation into the NVFP4 operand)
+  const int64_t P = (int64_t)T * k;
+  int64_t grid = (P + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  gather_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_x), d_topk_idx, d_pair_pos, P, H, k, d_prec, nullptr, d_a_codes,
+      d_a_sf, d_flag, nullptr, nullptr);
+  return check_launch("realb_dispatch_index (nvfp4 rows)");
 }
 
 extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const float* d_w, int T,

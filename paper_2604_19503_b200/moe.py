@@ -313,6 +313,14 @@ class MoELayer:
         self.plan_host = torch.zeros(3 + self.cluster.num_ranks, dtype=i32, pin_memory=True)
         R = self.rows_cap
         self.a_bf16 = torch.empty(R, H, dtype=bf, device=dev)
+        # gather dispatch: the gate_up GEMM reads token rows straight from x through
+        # row_src (grouped row -> token, realb_dispatch_index) instead of a copy into
+        # a_bf16 (realb_dispatch_permute). Off by default: measured interleaved on the
+        # Kimi 8192-token layer the two are equal (0.977 ms both; the gather GEMM's
+        # cp.async loaders cost what the 39 us row copy saves; scripts/bench_dispatch.py)
+        self.gather_dispatch = False
+        self.row_src = torch.zeros(R, dtype=i32, device=dev)
+        self._x_src = None  # (x, T) of the last forward: the gather GEMM's A
         self.h_bf16 = torch.empty(R, I, dtype=bf, device=dev)
         self.rows_out = torch.empty(R, H, dtype=bf, device=dev)
         self.flag = torch.zeros(1, dtype=i32, device=dev)
@@ -441,16 +449,22 @@ class MoELayer:
         else:
             ws = None
         mark("dispatch_start", main)
-        _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
-                  self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
-                  self.pair_pos.data_ptr(), self.a_bf16.data_ptr(),
-                  _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
-                  self.flag.data_ptr(), sp)
+        self._x_src = (x, T)
+        if self.gather_dispatch:
+            _lib.call("realb_dispatch_index", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
+                      self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
+                      self.pair_pos.data_ptr(), self.row_src.data_ptr(),
+                      _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
+                      self.flag.data_ptr(), sp)
+        else:
+            _lib.call("realb_dispatch_permute", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
+                      self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
+                      self.pair_pos.data_ptr(), self.a_bf16.data_ptr(),
+                      _lib.ptr(ws["a_codes"]) if ws else None, _lib.ptr(ws["a_sf"]) if ws else None,
+                      self.flag.data_ptr(), sp)
         mark("dispatch_end", main)
         lay = self.layout.data_ptr()
-        _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
-                  self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
-                  self.h_bf16.data_ptr(), 0, sp)
+        self._gate_up_bf16(lay, sp)
         if ws is not None:
             mark("fp4_ready", main)  # main stream reaches the first W4A4 GEMM
             if k3_stream is not main:
@@ -505,9 +519,7 @@ class MoELayer:
         self.align(T)
         sp, lay = _lib.stream_ptr(), self.layout.data_ptr()
         if (prec == 0).any():
-            _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
-                      self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
-                      self.h_bf16.data_ptr(), 0, sp)
+            self._gate_up_bf16(lay, sp)
             _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
                       self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
                       self.rows_out.data_ptr(), 0, sp)
@@ -527,12 +539,26 @@ class MoELayer:
         activation buffers hold."""
         E, H, I = self.E, self.H, self.I
         sp, lay = _lib.stream_ptr(), layout_dev.data_ptr()
-        _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
-                  self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
-                  self.h_bf16.data_ptr(), 0, sp)
+        self._gate_up_bf16(lay, sp)
         _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
                   self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
                   self.rows_out.data_ptr(), 0, sp)
+
+    def _gate_up_bf16(self, lay: int, sp: int) -> None:
+        """K5 gate_up (+ SwiGLU) of the W16A16 experts: the gather form reads the
+        rows of the last forward's x through row_src; the copy form reads a_bf16."""
+        H, I, E = self.H, self.I, self.E
+        if self.gather_dispatch and self._x_src is not None:
+            x, T = self._x_src
+            if T == 0:
+                return
+            _lib.call("realb_grouped_gemm_bf16_gather", x.data_ptr(), T, self.row_src.data_ptr(),
+                      self.w.w_gu.data_ptr(), self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16,
+                      _lib.EPI_SWIGLU, self.h_bf16.data_ptr(), 0, sp)
+        else:
+            _lib.call("realb_grouped_gemm_bf16", self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(),
+                      self.rows_cap, 2 * I, H, E, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU,
+                      self.h_bf16.data_ptr(), 0, sp)
 
     def check_flag(self):
         from .quant import QuantizationDomainError

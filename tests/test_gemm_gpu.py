@@ -84,3 +84,39 @@ def test_grouped_bf16_precision_subset():
             assert ((blk.float() - y).norm() / y.norm()) < 1e-2
         else:
             assert torch.isnan(blk.float()).all()
+
+
+@pytest.mark.parametrize("E,N,K,counts,T", [
+    (1, 256, 64, [77], 50),
+    (4, 512, 2048, [300, 0, 17, 1000], 700),
+    (8, 2816, 2048, [513, 129, 1, 0, 777, 256, 2048, 90], 1500),   # Kimi gate_up shape
+    (8, 2048, 1408, [513, 129, 1, 0, 777, 256, 2048, 90], 3000),   # Kimi down shape
+])
+@pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_SWIGLU])
+def test_grouped_bf16_gather_equals_copy(E, N, K, counts, T, epi):
+    """The gather form (A rows read from x through row_src by TMA tile::gather4)
+    gives bit-for-bit the rows the grouped-operand form gives on the copied rows
+    (same MMAs in the same order); padding rows of each group are never stored
+    from garbage (they read as zero)."""
+    torch.manual_seed(E + N + K + T)
+    prec_sel = np.zeros(E, np.int64)
+    lay, rows = host_layout(counts, prec_sel)
+    rows_cap = max(rows, 128)
+    x = torch.randn(T, K, device="cuda").to(torch.bfloat16)
+    src = torch.randint(0, T, (rows_cap,), dtype=torch.int32, device="cuda")
+    W = (torch.randn(E * N, K, device="cuda") / K**0.5).to(torch.bfloat16)
+    A = x[src.long()].contiguous()
+    ref = run_bf16(A, W, lay, N, K, E, 0, epi, rows_cap)
+    lay_t = torch.from_numpy(lay).cuda()
+    NO = N if epi == _lib.EPI_STORE else N // 2
+    out = torch.full((rows_cap, NO), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.call("realb_grouped_gemm_bf16_gather", x.data_ptr(), T, src.data_ptr(), W.data_ptr(), rows_cap, N, K,
+              E, lay_t.data_ptr(), 0, epi, out.data_ptr(), 0, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for e in range(E):
+        rs = int(lay[8 + e])
+        c = counts[e]
+        assert torch.equal(out[rs:rs + c], ref[rs:rs + c]), e
+        pad = (c + 127) // 128 * 128
+        if pad > c:  # padding rows: computed on zero rows -> zero (SwiGLU(0,0) = 0)
+            assert (out[rs + c:rs + pad].float() == 0).all(), e

@@ -122,6 +122,50 @@ def test_dispatch_layout_and_positions(name, E, T):
         assert torch.equal(a[pos[t, j]], xs[t])
 
 
+@pytest.mark.parametrize("name,E,T", [("tiny", None, 1024), ("kimi", 16, 700), ("qwen", 32, 300)])
+def test_dispatch_index_inverse_map(name, E, T):
+    """realb_dispatch_index: the same positions as realb_dispatch_permute, and
+    row_src[pair_pos[t, j]] == t for every pair (the gather GEMM's row map)."""
+    shape = small(SHAPES[name], E)
+    layer, x, mod, *_ = build_layer(shape, T)
+    layer.route(x, mod)
+    layer.prec_dev.zero_()
+    layer.align(T)
+    nch = (T + 63) // 64
+    args = (x.data_ptr(), layer.topk_idx.data_ptr(), T, shape.hidden, shape.num_experts, shape.top_k,
+            layer.prec_dev.data_ptr(), layer.layout.data_ptr(), nch, layer.rows_cap)
+    _lib.call("realb_dispatch_permute", *args, layer.pair_pos.data_ptr(), layer.a_bf16.data_ptr(), None, None,
+              layer.flag.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    pos_ref = layer.pair_pos[:T].cpu().clone()
+    layer.row_src.fill_(-1)
+    _lib.call("realb_dispatch_index", *args, layer.pair_pos.data_ptr(), layer.row_src.data_ptr(), None, None,
+              layer.flag.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    pos = layer.pair_pos[:T].cpu()
+    assert torch.equal(pos, pos_ref)
+    src = layer.row_src.cpu().numpy()
+    tok = np.repeat(np.arange(T), shape.top_k)
+    assert (src[pos.numpy().reshape(-1)] == tok).all()
+    assert (src >= 0).sum() == T * shape.top_k  # padding rows untouched
+
+
+@pytest.mark.parametrize("name,E,T,strategy", [("kimi", 16, 700, "baseline"), ("qwen", 32, 300, "fp4all"),
+                                               ("tiny", None, 1024, "realb")])
+def test_gather_dispatch_equals_copy_dispatch(name, E, T, strategy):
+    """The layer with gather dispatch equals the copy-dispatch layer
+    bit for bit, W4A4 experts included."""
+    shape = small(SHAPES[name], E)
+    layer, x, mod, *_ = build_layer(shape, T, R=2)
+    params = RealbParams(global_batch_threshold=0)
+    layer.gather_dispatch = False
+    y0 = layer.forward(x, mod, strategy, params).y.clone()
+    layer.gather_dispatch = True
+    y1 = layer.forward(x, mod, strategy, params).y.clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+
+
 def test_combine_weighted_sum():
     T, H, k, R = 333, 512, 6, 4096
     g = torch.Generator(device="cuda").manual_seed(1)
