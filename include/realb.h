@@ -292,6 +292,12 @@ REALB_API int realb_p2p_pack_dev(const void* d_x, const int32_t* d_topk_idx, int
                                  int32_t* d_nonfinite_flag, void* stream);
 REALB_API int realb_p2p_return_dev(const void* d_rows, const int32_t* d_row_pos, int64_t n_cap, int H,
                                    int R, const uint64_t* h_peer_ret, const void* d_plan, void* stream);
+
+/* The return map of the fused down-GEMM + return: for every received row i
+ * (n_cap bounds the device-plan count), d_row_map[d_row_pos[i]] = (s << 25) | j,
+ * j = the row of source s's return window realb_p2p_return_dev would write. */
+REALB_API int realb_p2p_return_map(const int32_t* d_row_pos, int64_t n_cap, int R, const void* d_plan,
+                                   int32_t* d_row_map, void* stream);
 /* Direct dispatch: each (token, slot) row goes straight to its destination's GEMM
  * operand at its final grouped row (realb_ep_regroup's layout, derived from the
  * gathered counts in d_plan): bf16 into h_peer_a[d] for a W16A16 destination,
@@ -335,6 +341,15 @@ REALB_API int realb_grouped_gemm_bf16_gather(const void* d_x, int64_t n_src, con
                                              const int32_t* d_layout, int prec, int epilogue, void* d_out,
                                              int max_ctas, void* stream);
 
+/* K5 fused with the EP return (C3 over peer memory): the STORE epilogue, but
+ * output row g goes to h_dst_bases[m >> 25] + (m & (2^25 - 1)) * N * 2 with
+ * m = d_row_map[g] (int32 [rows_cap]; realb_p2p_return_map builds it), i.e.
+ * straight into the token's source rank's return window; no local output
+ * buffer and no separate return copy. n_dst <= 64; bases 16-B aligned. */
+REALB_API int realb_grouped_gemm_bf16_scatter(const void* d_a, const void* d_w, int64_t rows_cap, int N, int K,
+                                              int E, const int32_t* d_layout, int prec, const int32_t* d_row_map,
+                                              int n_dst, const uint64_t* h_dst_bases, int max_ctas, void* stream);
+
 /* K6 — grouped NVFP4 x NVFP4 GEMM (tcgen05 kind::mxf4nvf4.block_scale,
  * scale_vec::4X, UE4M3 scales in REALB_SF_MMA128x4 layout) over the W4A4
  * groups of d_layout. Weight rows are indexed by global expert id
@@ -347,6 +362,14 @@ REALB_API int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t* 
                              const int32_t* d_layout, int epilogue,
                              void* d_out, uint8_t* d_out_codes, uint8_t* d_out_sf,
                              int max_ctas, void* stream);
+
+/* K6 fused with the EP return: the STORE epilogue with per-row destinations,
+ * as realb_grouped_gemm_bf16_scatter. */
+REALB_API int realb_grouped_gemm_nvfp4_scatter(const uint8_t* d_a_codes, const uint8_t* d_a_sf,
+                                               const uint8_t* d_w_codes, const uint8_t* d_w_sf, int64_t rows_cap,
+                                               int N, int K, int E, const int32_t* d_layout,
+                                               const int32_t* d_row_map, int n_dst, const uint64_t* h_dst_bases,
+                                               int max_ctas, void* stream);
 
 /* C3 (local part) — weighted top-k combine:
  *   y[t][h] = addend[t][h] + sum_j topk_w[t][j] * rows[pair_pos[t][j]][h]

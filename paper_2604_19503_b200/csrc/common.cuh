@@ -157,6 +157,42 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
 }
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// ---- scatter epilogue (down GEMM fused with the EP return, C3): output row g of
+// the grouped row space goes to base[m >> 25] + (m & (2^25 - 1)) * ld, m = row_map[g]
+// (peer memory of the token's source rank); m < 0 rows are skipped.
+constexpr int kEpiScatter = 2;  // internal epilogue id: STORE math, per-row destinations
+constexpr int kScatterPeers = 64;
+constexpr int kScatterRowBits = 25;
+struct RowScatter {
+  uint8_t* base[kScatterPeers];
+  const int32_t* row_map;
+  int64_t ld;  // destination row stride (bytes)
+};
+__device__ __forceinline__ uint8_t* scatter_row(const RowScatter& s, int32_t m) {
+  return s.base[m >> kScatterRowBits] + (int64_t)(m & ((1 << kScatterRowBits) - 1)) * s.ld;
+}
+// 32 rows x 64 B staged in the SWIZZLE_64B layout (piece c of row r at c ^ ((r >> 1) & 3))
+// -> 8 rows x 64 B per warp instruction to each row's destination; m = this lane's row map
+__device__ __forceinline__ void scatter_chunk64(uint32_t buf, const RowScatter& s, int32_t m, int64_t col_bytes) {
+  const int lane = threadIdx.x & 31, pc = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int rr = 8 * j + (lane >> 2);
+    const int32_t mr = __shfl_sync(0xffffffffu, m, rr);
+    if (mr >= 0) {
+      const uint4 v = ld_shared_v4(buf + rr * 64 + ((pc ^ ((rr >> 1) & 3)) << 4));
+      *reinterpret_cast<uint4*>(scatter_row(s, mr) + col_bytes + pc * 16) = v;
+    }
+  }
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

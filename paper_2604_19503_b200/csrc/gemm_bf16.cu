@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(256, 1)
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut, const int32_t* layout,
                              int E, int prec, int N, int K, uint32_t dbg,
-                             const __nv_bfloat16* __restrict__ xsrc, const int32_t* __restrict__ row_src) {
+                             const __nv_bfloat16* __restrict__ xsrc, const int32_t* __restrict__ row_src,
+                             const __grid_constant__ RowScatter scat) {
   static_assert(!GATHER || CL == 1, "the gather form is 1-CTA only");
   using S = SmemBf16<BN, STAGES, CL>;
   extern __shared__ uint8_t smem_raw[];
@@ -322,17 +323,20 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       const int row0 = c.a_row + q * 32;
+      int32_t smap = -1;  // scatter: this lane's row -> destination (C3 fused)
+      if constexpr (EPI == kEpiScatter)
+        if (!dummy && q * 32 + lane < c.valid) smap = __ldg(scat.row_map + row0 + lane);
       if ((dbg & 1u) || dummy) {  // nothing to store: release the accumulator at once
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_leader(&tempty[acc]);
         continue;
       }
-      constexpr int NCH = EPI == REALB_EPI_STORE ? BN / 32 : BN / 64;
+      constexpr int NCH = EPI == REALB_EPI_SWIGLU ? BN / 64 : BN / 32;
 #pragma unroll 1
       for (int ch = 0; ch < NCH; ++ch) {
         uint32_t p[16];
-        if constexpr (EPI == REALB_EPI_STORE) {
+        if constexpr (EPI != REALB_EPI_SWIGLU) {
           uint32_t v[32];
           tmem_ld32(tbase + ch * 32, v);
           tmem_wait_ld();
@@ -349,6 +353,13 @@ __global__ void __launch_bounds__(256, 1)
             p[j] = pack_bf16x2(silu_mul(__uint_as_float(g[2 * j]), __uint_as_float(u[2 * j])),
                                silu_mul(__uint_as_float(g[2 * j + 1]), __uint_as_float(u[2 * j + 1])));
         }
+        if constexpr (EPI == kEpiScatter) {  // stage, then 8 rows x 64 B per store instruction
+          stage_row64(ebuf, lane, p);
+          __syncwarp();
+          scatter_chunk64(ebuf, scat, smap, (int64_t)(c.n0 + ch * 32) * 2);
+          __syncwarp();
+          continue;
+        }
         // the buffer about to be reused must have been read out by its TMA store
         if (lane == 0) bulk_wait_group_read<kEpiBufs - 1>();
         __syncwarp();
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(256, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          const int col = EPI == REALB_EPI_STORE ? c.n0 + ch * 32 : c.n0 / 2 + ch * 32;
+          const int col = EPI == REALB_EPI_SWIGLU ? c.n0 / 2 + ch * 32 : c.n0 + ch * 32;
           tma_store_2d(&tmOut, smem + S::EPI_OFF + q * (kEpiBufs * 2048) + nbuf * 2048, col, row0);
           bulk_commit_group();
         }
@@ -383,7 +394,8 @@ __global__ void __launch_bounds__(256, 1)
 template <int BN, int STAGES, int EPI, int CL, bool GATHER = false>
 static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, int N, int K, int E,
                                const int32_t* layout, int prec, void* out, int max_ctas,
-                               cudaStream_t st, const int32_t* row_src = nullptr) {
+                               cudaStream_t st, const int32_t* row_src = nullptr,
+                               const RowScatter* scat = nullptr) {
   CUtensorMap ta, tb, to;
   // gather form: A is read by the loader warps (the A map is unused, built over x)
   int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a, K, GATHER ? 1 : rows_cap, (uint64_t)K * 2,
@@ -392,9 +404,11 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   rc = make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, K, (uint64_t)E * N, (uint64_t)K * 2,
                     kBK, BN / CL, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  const int NO = EPI == REALB_EPI_STORE ? N : N / 2;
-  rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, NO, rows_cap, (uint64_t)NO * 2, 32,
-                    32, CU_TENSOR_MAP_SWIZZLE_64B);
+  const int NO = EPI == REALB_EPI_SWIGLU ? N / 2 : N;
+  // scatter: no output tensor (the map is built over the A operand, never used)
+  rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, EPI == kEpiScatter ? a : out, NO,
+                    EPI == kEpiScatter ? 1 : rows_cap, (uint64_t)NO * 2, 32, EPI == kEpiScatter ? 1 : 32,
+                    CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
   auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL, GATHER>;
   const int smem = SmemBf16<BN, STAGES, CL>::TOTAL;
@@ -418,8 +432,10 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  RowScatter sc{};
+  if (scat) sc = *scat;
   rc = cuda_status(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, layout, E, prec, N, K, dbg,
-                                      reinterpret_cast<const __nv_bfloat16*>(a), row_src),
+                                      reinterpret_cast<const __nv_bfloat16*>(a), row_src, sc),
                    "realb_grouped_gemm_bf16 launch");
   if (rc) return rc;
   return check_launch("realb_grouped_gemm_bf16");
@@ -487,4 +503,31 @@ extern "C" int realb_grouped_gemm_bf16_gather(const void* d_x, int64_t n_src, co
                                                                   d_out, max_ctas, st, d_row_src);
   set_error("realb_grouped_gemm_bf16_gather: unknown epilogue %d", epilogue);
   return REALB_EINVAL;
+}
+
+extern "C" int realb_grouped_gemm_bf16_scatter(const void* d_a, const void* d_w, int64_t rows_cap, int N, int K,
+                                               int E, const int32_t* d_layout, int prec, const int32_t* d_row_map,
+                                               int n_dst, const uint64_t* h_dst_bases, int max_ctas,
+                                               void* stream) {
+  if (!d_a || !d_w || !d_layout || !d_row_map || !h_dst_bases || rows_cap <= 0 || E <= 0 || n_dst < 1 ||
+      n_dst > kScatterPeers || (prec != REALB_PREC_W16A16 && prec != REALB_PREC_W4A4)) {
+    set_error("realb_grouped_gemm_bf16_scatter: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (K % kBK || N % 256) {
+    set_error("realb_grouped_gemm_bf16_scatter: needs K %% 64 == 0 and N %% 256 == 0 (N=%d K=%d)", N, K);
+    return REALB_EUNSUPPORTED;
+  }
+  RowScatter sc{};
+  for (int d = 0; d < n_dst; ++d) {
+    if (h_dst_bases[d] & 15) {
+      set_error("realb_grouped_gemm_bf16_scatter: destination %d not 16-B aligned", d);
+      return REALB_EINVAL;
+    }
+    sc.base[d] = reinterpret_cast<uint8_t*>(h_dst_bases[d]);
+  }
+  sc.row_map = d_row_map;
+  sc.ld = (int64_t)N * 2;
+  return launch_grouped_bf16<256, 4, kEpiScatter, 1>(d_a, d_w, rows_cap, N, K, E, d_layout, prec, nullptr,
+                                                     max_ctas, (cudaStream_t)stream, nullptr, &sc);
 }

@@ -46,14 +46,14 @@ constexpr int kF4EpiBufs = 3;             // TMA-store staging buffers per epilo
 template <int EPI, int CL>
 struct SmemFp4 {
   // STORE (bf16 out) needs 32 KB of TMA-store staging
-  static constexpr int STAGES = CL == 1 ? (EPI == REALB_EPI_STORE ? 3 : 4) : (EPI == REALB_EPI_STORE ? 4 : 5);
+  static constexpr int STAGES = CL == 1 ? (EPI != REALB_EPI_SWIGLU ? 3 : 4) : (EPI != REALB_EPI_SWIGLU ? 4 : 5);
   static constexpr int A_BYTES = kF4BM * kF4BKB;              // 16 KB
   static constexpr int B_BYTES = (kF4BN / CL) * kF4BKB;       // 32 KB (16 KB per CTA of a pair)
   static constexpr int SFA_BYTES = 4 * 512;                   // 128 rows x 16 scales
   static constexpr int SFB_BYTES = 2 * 4 * 512;               // 256 rows x 16 scales (full W tile)
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
   static constexpr int EPI_OFF = STAGES * STAGE;    // 8 warps x kF4EpiBufs x 2 KB (STORE only)
-  static constexpr int EPI_BYTES = EPI == REALB_EPI_STORE ? 8 * kF4EpiBufs * 2048 : 0;
+  static constexpr int EPI_BYTES = EPI != REALB_EPI_SWIGLU ? 8 * kF4EpiBufs * 2048 : 0;
   static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -71,6 +71,7 @@ struct Fp4Args {
   uint8_t* out_sf;      // SWIGLU: MMA-layout scales of the [rows][N/2] result
   uint32_t sf_lbo, sf_sbo;
   uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies, 4 skip MMAs
+  RowScatter scat;  // kEpiScatter: per-row destinations (down GEMM fused with the EP return)
 };
 
 __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -360,6 +361,25 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       if (lane == 0) arrive_leader(tempty);  // accumulator free: next mainloop may start
       if ((args.dbg & 1u) || dummy) continue;
       const int64_t r = (int64_t)c.a_row + row_in_tile;
+      if constexpr (EPI == kEpiScatter) {  // bf16 rows straight to their sources' return windows
+        const int32_t smap = row_in_tile < c.valid ? __ldg(args.scat.row_map + r) : -1;
+        const uint32_t ebuf = smem_u32(smem + S::EPI_OFF + (warp - 4) * (kF4EpiBufs * 2048));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            p[j] = pack_bf16x2(__uint_as_float(v[i][2 * j]), __uint_as_float(v[i][2 * j + 1]));
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            st_shared_v4(ebuf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), p[4 * cc], p[4 * cc + 1],
+                         p[4 * cc + 2], p[4 * cc + 3]);
+          __syncwarp();
+          scatter_chunk64(ebuf, args.scat, smap, (int64_t)(c.n0 + half * 128 + 32 * i) * 2);
+          __syncwarp();
+        }
+        continue;
+      }
       if constexpr (EPI == REALB_EPI_SWIGLU) {
         // outputs [n0/2 + half*64, +64): h = bf16(silu(g) * u), then NVFP4
         const int I = N / 2;
@@ -442,7 +462,8 @@ static int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int K) {
 template <int EPI, int CL>
 static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, const uint8_t* w_sf,
                       int64_t rows_cap, int N, int K, int E, const int32_t* layout, void* out,
-                      uint8_t* out_codes, uint8_t* out_sf, int max_ctas, cudaStream_t st) {
+                      uint8_t* out_codes, uint8_t* out_sf, int max_ctas, cudaStream_t st,
+                      const RowScatter* scat = nullptr) {
   CUtensorMap ta, tb, tsa, tsb, to;
   int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, a, (uint64_t)K / 2, rows_cap,
                         (uint64_t)K / 2, kF4BKB, kF4BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -454,7 +475,7 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   if (rc) return rc;
   rc = make_sf_map(&tsb, w_sf, (int64_t)E * N, K);
   if (rc) return rc;
-  if (EPI == REALB_EPI_STORE) {
+  if (EPI != REALB_EPI_SWIGLU && out) {
     rc = make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, rows_cap, (uint64_t)N * 2, 32, 32,
                       CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
@@ -474,6 +495,7 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   args.sf_lbo = env_u32("REALB_DBG_SF_LBO", 128);
   args.sf_sbo = env_u32("REALB_DBG_SF_SBO", 128);
   args.dbg = env_u32("REALB_DBG_FP4", 0);
+  args.scat = scat ? *scat : RowScatter{};
   auto kern = grouped_gemm_fp4_kernel<EPI, CL>;
   const int smem = SmemFp4<EPI, CL>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_nvfp4: smem attribute");
@@ -546,4 +568,33 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
   }
   set_error("realb_grouped_gemm_nvfp4: unknown epilogue %d", epilogue);
   return REALB_EINVAL;
+}
+
+extern "C" int realb_grouped_gemm_nvfp4_scatter(const uint8_t* d_a_codes, const uint8_t* d_a_sf,
+                                                const uint8_t* d_w_codes, const uint8_t* d_w_sf, int64_t rows_cap,
+                                                int N, int K, int E, const int32_t* d_layout,
+                                                const int32_t* d_row_map, int n_dst, const uint64_t* h_dst_bases,
+                                                int max_ctas, void* stream) {
+  if (!d_a_codes || !d_a_sf || !d_w_codes || !d_w_sf || !d_layout || !d_row_map || !h_dst_bases ||
+      rows_cap <= 0 || rows_cap % 128 || E <= 0 || n_dst < 1 || n_dst > kScatterPeers) {
+    set_error("realb_grouped_gemm_nvfp4_scatter: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (N % kF4BN || K % 64 || K > 3072) {
+    set_error("realb_grouped_gemm_nvfp4_scatter: needs N %% 256 == 0, K %% 64 == 0 and K <= 3072 (N=%d K=%d)",
+              N, K);
+    return REALB_EUNSUPPORTED;
+  }
+  RowScatter sc{};
+  for (int d = 0; d < n_dst; ++d) {
+    if (h_dst_bases[d] & 15) {
+      set_error("realb_grouped_gemm_nvfp4_scatter: destination %d not 16-B aligned", d);
+      return REALB_EINVAL;
+    }
+    sc.base[d] = reinterpret_cast<uint8_t*>(h_dst_bases[d]);
+  }
+  sc.row_map = d_row_map;
+  sc.ld = (int64_t)N * 2;
+  return launch_fp4<kEpiScatter, 1>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E, d_layout, nullptr,
+                                    nullptr, nullptr, max_ctas, (cudaStream_t)stream, &sc);
 }

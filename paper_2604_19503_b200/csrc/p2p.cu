@@ -347,9 +347,39 @@ __global__ void __launch_bounds__(256) p2p_return_dev_kernel(const __nv_bfloat16
   }
 }
 
+// the return map of the fused down-GEMM + return (realb_grouped_gemm_*_scatter):
+// grouped row row_pos[i] of received row i (source s, its j-th) -> (s << 25) | row
+// of s's return window, the address p2p_return_dev_kernel would copy it to
+__global__ void __launch_bounds__(256) p2p_return_map_kernel(const int32_t* __restrict__ row_pos, int64_t n_cap,
+                                                             int R, const P2PPlan* __restrict__ plan,
+                                                             int32_t* __restrict__ row_map) {
+  const int64_t n = min(n_cap, (int64_t)plan->n_recv);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int s = 0;
+    while (s + 1 < R && plan->recv0[s + 1] <= i) ++s;
+    const int64_t row = (int64_t)plan->ret_row0[s] + (i - plan->recv0[s]);
+    row_map[row_pos[i]] = (int32_t)(((int64_t)s << kScatterRowBits) | row);
+  }
+}
+
 }  // namespace realb
 
 using namespace realb;
+
+extern "C" int realb_p2p_return_map(const int32_t* d_row_pos, int64_t n_cap, int R, const void* d_plan,
+                                    int32_t* d_row_map, void* stream) {
+  if (!d_row_pos || !d_plan || !d_row_map || n_cap < 0 || n_cap >= (1LL << kScatterRowBits) || R < 1 ||
+      R > kMaxPeers || R > kScatterPeers) {
+    set_error("realb_p2p_return_map: bad arguments (n_cap=%lld R=%d)", (long long)n_cap, R);
+    return REALB_EINVAL;
+  }
+  if (n_cap == 0) return REALB_OK;
+  int64_t grid = (n_cap + 255) / 256;
+  if (grid > (int64_t)num_sms() * 8) grid = (int64_t)num_sms() * 8;
+  p2p_return_map_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      d_row_pos, n_cap, R, reinterpret_cast<const P2PPlan*>(d_plan), d_row_map);
+  return check_launch("realb_p2p_return_map");
+}
 
 extern "C" int realb_ipc_alloc(int64_t bytes, void** d_ptr, uint8_t* handle) {
   if (bytes <= 0 || !d_ptr || !handle) {

@@ -270,6 +270,9 @@ class CudaEPOps:
         self.p2p_rank = comm.rank
         # peers' operand bases (kept alive: the ABI reads them through a host pointer)
         self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "ops")]
+        self.ret_bases = np.array(self.p2p["ret"], np.uint64)
+        # fused down-GEMM + return: grouped row -> (source, row of its return window)
+        self.row_map = torch.empty(self.rows_cap, dtype=torch.int32, device=self.dev)
         # host-sync-free (device-plan) form: plan record, expected-counter words,
         # global expert precisions and the plan kernel's scratch
         dev = self.dev
@@ -389,25 +392,25 @@ class CudaEPOps:
                   self.local_layout.data_ptr(), self.base.data_ptr(), self.row_expert.data_ptr(),
                   self.row_pos.data_ptr(), sp)
         pl = self.d_plan.data_ptr()
+        # C3 is fused into the down GEMMs: each output row is stored straight into its
+        # source's return window (row_map: grouped row -> source, row), over NVLink
+        _lib.call("realb_p2p_return_map", self.row_pos.data_ptr(), cap, R, pl, self.row_map.data_ptr(), sp)
         a_bf16, a_codes, a_sf = self.p2p["opa"][r], self.p2p["opc"][r], self.p2p["ops"][r]
+        rb = self.ret_bases.ctypes.data
         # both precisions' GEMMs; each runs only the groups the device plan gave it
         lay = self.local_layout.data_ptr()
         _lib.call("realb_grouped_gemm_bf16", a_bf16, self.local.w_gu.data_ptr(), self.rows_cap,
                   2 * I, H, El, lay, _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.h_bf16.data_ptr(), 0, sp)
-        _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.local.w_d.data_ptr(), self.rows_cap,
-                  H, I, El, lay, _lib.PREC_W16A16, _lib.EPI_STORE, self.rows_out.data_ptr(), 0, sp)
+        _lib.call("realb_grouped_gemm_bf16_scatter", self.h_bf16.data_ptr(), self.local.w_d.data_ptr(),
+                  self.rows_cap, H, I, El, lay, _lib.PREC_W16A16, self.row_map.data_ptr(), R, rb, 0, sp)
         main.wait_stream(self.side)
         _lib.call("realb_grouped_gemm_nvfp4", a_codes, a_sf,
                   ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, El, lay,
                   _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
-        _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+        _lib.call("realb_grouped_gemm_nvfp4_scatter", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                   ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
-                  _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+                  self.row_map.data_ptr(), R, rb, 0, sp)
         mark("compute")
-        # C3: every output row straight into its source's return window
-        ret_bases = np.array(self.p2p["ret"], np.uint64)
-        _lib.call("realb_p2p_return_dev", self.rows_out.data_ptr(), self.row_pos.data_ptr(), cap, H, R,
-                  ret_bases.ctypes.data, pl, sp)
         self._signal_wait_dev(4, 1)
         y = torch.empty(T, H, dtype=torch.bfloat16, device=self.dev)
         addend = self.shared.join() if self.shared is not None and T > 0 else None

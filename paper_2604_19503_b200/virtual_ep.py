@@ -243,6 +243,26 @@ def ep_layer_timing(comp_ms, trans_ms, accelerated, mode, disp_a2a, comb_a2a, ek
                        totals.index(lat), mode)
 
 
+def p2p_layer_timing(comp_ms, trans_ms, accelerated, mode, disp_a2a, comb_a2a, ek):
+    """LayerTiming of the host-sync-free peer-memory EP layer (EPMoELayer.forward_device):
+    dispatch writes every row straight into its owner's GEMM operand (no receive
+    gather), and the down GEMMs store their rows straight into the sources' return
+    windows, so the return transfer overlaps the down GEMM (one third of the expert
+    flops: 2HI of 6HI per pair). schedule = router/align/pack + C1; dispatch = a2a
+    model; compute = GEMMs; combine = the return's excess over the down GEMM +
+    combine."""
+    phases, totals = [], []
+    for r in range(len(comp_ms)):
+        ret_exposed = max(0.0, comb_a2a - comp_ms[r] / 3.0)
+        ph = RankPhases(int((ek["send"] + ALPHA_US / 1e3) * 1e6), int(trans_ms[r] * 1e6), int(disp_a2a * 1e6),
+                        int(comp_ms[r] * 1e6), int((ret_exposed + ek["combine"]) * 1e6))
+        phases.append(ph)
+        totals.append(ph.total(mode, accelerated[r]))
+    lat = max(totals)
+    return LayerTiming(tuple(phases), tuple(totals), lat, max(p.compute_ns for p in phases),
+                       totals.index(lat), mode)
+
+
 class VirtualEP:
     """One model shape at EP degree R emulated on cuda:0; weights built once,
     batches (vision fraction, routing skew) regenerated per report."""
@@ -323,6 +343,8 @@ class VirtualEP:
                                    lambda r: ek["recv_w4a4"][r] if acc[r] else ek["recv_bf16"][r])
         ep_realb4 = ep_layer_timing(realb_ms, transform_ms, acc, mode, disp_fp4, comb, ek,
                                     lambda r: ek["recv_fp4_packed"][r] if acc[r] else ek["recv_bf16"][r])
+        p2p_bf16 = p2p_layer_timing(bf16_ms, [0.0] * R, [False] * R, PipelineMode.SEQUENTIAL, disp_bf16, comb, ek)
+        p2p_realb = p2p_layer_timing(realb_ms, transform_ms, acc, mode, disp_fp4, comb, ek)
         text_total = int(rank_vt[:, 1].sum())
         text_fp4 = int(sum(rank_vt[r, 1] for r in range(R) if acc[r]))
         return {
@@ -360,6 +382,13 @@ class VirtualEP:
             "projected_ep_layer_speedup": ep_bf16.layer_latency_ns / ep_realb.layer_latency_ns,
             "projected_ep_layer_speedup_fp4_dispatch": ep_bf16.layer_latency_ns / ep_realb4.layer_latency_ns,
             "projected_full_path_speedup_fp4_dispatch": lt_bf16.layer_latency_ns / lt_realb4.layer_latency_ns,
+            "projected_p2p_layer_ms": {"bf16": p2p_bf16.layer_latency_ns / 1e6,
+                                       "realb": p2p_realb.layer_latency_ns / 1e6,
+                                       "model": "host-sync-free peer-memory layer: direct dispatch into the "
+                                                "owners' GEMM operands (NVFP4 to W4A4 ranks, no receive "
+                                                "gather); down GEMM stores into the sources' return windows "
+                                                "(return overlaps the down GEMM = compute/3); then combine"},
+            "projected_p2p_layer_speedup": p2p_bf16.layer_latency_ns / p2p_realb.layer_latency_ns,
             "transform_hidden": all(t <= disp_bf16 for t in transform_ms),
             "k3_overlap_one_gpu": k3_timeline,
         }

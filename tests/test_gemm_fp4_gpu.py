@@ -101,3 +101,51 @@ def test_fp4_swiglu_requant_epilogue(counts, cluster):
         err = np.linalg.norm(got - href) / np.linalg.norm(href)
         assert err < 2e-2, err
         assert (got == href).mean() > 0.97
+
+
+def _scatter_map(lay, counts, n_dst, seed):
+    """A random row map over the valid rows: row g -> (destination d, row j), each
+    destination's rows a permutation of 0..n_d-1."""
+    rng = np.random.default_rng(seed)
+    valid = np.concatenate([int(lay[8 + e]) + np.arange(c) for e, c in enumerate(counts)]).astype(np.int64)
+    d = rng.integers(0, n_dst, len(valid))
+    rowmap = {}
+    sizes = []
+    for dd in range(n_dst):
+        sel = valid[d == dd]
+        perm = rng.permutation(len(sel))
+        for g, j in zip(sel, perm):
+            rowmap[int(g)] = (dd, int(j))
+        sizes.append(len(sel))
+    return rowmap, sizes
+
+
+@pytest.mark.parametrize("E,N,K,counts,n_dst", [
+    (3, 512, 1408, [300, 0, 700], 2),
+    (4, 2048, 1408, [513, 129, 1, 260], 5),     # Kimi down
+])
+def test_fp4_scatter_equals_store(E, N, K, counts, n_dst):
+    """realb_grouped_gemm_nvfp4_scatter: every valid row lands, bit-identical to
+    the STORE epilogue's row, at its mapped (destination, row); nothing else is
+    written."""
+    lay, rows, A, W, ac, asf, wc, wsf = make_problem(E, N, K, counts, seed=7 + E)
+    lay_t = torch.from_numpy(lay).cuda()
+    ref = torch.zeros((rows, N), dtype=torch.bfloat16, device="cuda")
+    _lib.call("realb_grouped_gemm_nvfp4", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(), rows, N, K,
+              E, lay_t.data_ptr(), _lib.EPI_STORE, ref.data_ptr(), None, None, 0, _lib.stream_ptr())
+    rowmap, sizes = _scatter_map(lay, counts, n_dst, seed=E)
+    m = np.full(rows, -1, np.int32)
+    for g, (d, j) in rowmap.items():
+        m[g] = (d << 25) | j
+    m_t = torch.from_numpy(m).cuda()
+    dsts = [torch.full((max(s, 1) + 1, N), 7.0, dtype=torch.bfloat16, device="cuda") for s in sizes]
+    bases = np.array([t.data_ptr() for t in dsts], np.uint64)
+    _lib.call("realb_grouped_gemm_nvfp4_scatter", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(),
+              rows, N, K, E, lay_t.data_ptr(), m_t.data_ptr(), n_dst, bases.ctypes.data, 0, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    got = [t.cpu() for t in dsts]
+    refc = ref.cpu()
+    for g, (d, j) in rowmap.items():
+        assert torch.equal(got[d][j], refc[g]), (g, d, j)
+    for d, s in enumerate(sizes):
+        assert (got[d][s:].float() == 7.0).all()

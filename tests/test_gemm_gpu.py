@@ -120,3 +120,42 @@ def test_grouped_bf16_gather_equals_copy(E, N, K, counts, T, epi):
         pad = (c + 127) // 128 * 128
         if pad > c:  # padding rows: computed on zero rows -> zero (SwiGLU(0,0) = 0)
             assert (out[rs + c:rs + pad].float() == 0).all(), e
+
+
+@pytest.mark.parametrize("E,N,K,counts,n_dst", [
+    (4, 512, 2048, [300, 0, 17, 1000], 3),
+    (8, 2048, 1408, [513, 129, 1, 0, 777, 256, 2048, 90], 8),   # Kimi down shape, EP8
+])
+def test_grouped_bf16_scatter_equals_store(E, N, K, counts, n_dst):
+    """realb_grouped_gemm_bf16_scatter (the down GEMM fused with the EP return):
+    every valid row lands bit-identical to the STORE epilogue's row at its mapped
+    (destination, row); rows of other destinations / padding are not written."""
+    torch.manual_seed(E + N)
+    prec_sel = np.zeros(E, np.int64)
+    lay, rows = host_layout(counts, prec_sel)
+    rows_cap = max(rows, 128)
+    A = torch.randn(rows_cap, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(E * N, K, device="cuda") / K**0.5).to(torch.bfloat16)
+    ref = run_bf16(A, W, lay, N, K, E, 0, _lib.EPI_STORE, rows_cap).cpu()
+    rng = np.random.default_rng(E)
+    valid = np.concatenate([int(lay[8 + e]) + np.arange(c) for e, c in enumerate(counts)])
+    d = rng.integers(0, n_dst, len(valid))
+    m = np.full(rows_cap, -1, np.int32)
+    sizes = []
+    for dd in range(n_dst):
+        sel = valid[d == dd]
+        m[sel] = (dd << 25) | rng.permutation(len(sel))
+        sizes.append(len(sel))
+    dsts = [torch.full((s + 1, N), 7.0, dtype=torch.bfloat16, device="cuda") for s in sizes]
+    bases = np.array([t.data_ptr() for t in dsts], np.uint64)
+    lay_t = torch.from_numpy(lay).cuda()
+    m_t = torch.from_numpy(m).cuda()
+    _lib.call("realb_grouped_gemm_bf16_scatter", A.data_ptr(), W.data_ptr(), rows_cap, N, K, E, lay_t.data_ptr(),
+              0, m_t.data_ptr(), n_dst, bases.ctypes.data, 0, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    got = [t.cpu() for t in dsts]
+    for g in valid:
+        dd, j = int(m[g]) >> 25, int(m[g]) & ((1 << 25) - 1)
+        assert torch.equal(got[dd][j], ref[g]), (g, dd, j)
+    for dd, s in enumerate(sizes):
+        assert (got[dd][s:].float() == 7.0).all()
