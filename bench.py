@@ -223,15 +223,24 @@ def roofline_gate_up(torch, layer, x, mod, shape, args):
     E, H, I = shape.num_experts, shape.hidden, shape.intermediate
     pairs = T * shape.top_k
     sp = _lib.stream_ptr()
-    durs = []
+    # the same flops as ONE dense cuBLAS GEMM ([pairs x H] @ [H x 2I], no grouping,
+    # no padding, no SwiGLU), timed alternately with K5: what the chip sustains on
+    # this work at the clock / power state of this run
+    a_dense = torch.randn(pairs, H, device=x.device).to(torch.bfloat16)
+    w_dense = (torch.randn(H, 2 * I, device=x.device) / H**0.5).to(torch.bfloat16)
+    durs, durs_ref = [], []
     for _ in range(max(5, args.steps)):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        layer._gate_up_bf16(layer.layout.data_ptr(), sp)  # the layer's own launch (gather form)
-        e.record()
-        e.synchronize()
-        durs.append(s.elapsed_time(e))
+        for fn, acc in ((lambda: layer._gate_up_bf16(layer.layout.data_ptr(), sp), durs),
+                        (lambda: torch.matmul(a_dense, w_dense), durs_ref)):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            acc.append(s.elapsed_time(e))
     t = sorted(durs)[len(durs) // 2] / 1e3
+    t_ref = sorted(durs_ref)[len(durs_ref) // 2] / 1e3
+    del a_dense, w_dense
     flops = 2.0 * pairs * (2 * I) * H
     achieved = flops / t / 1e12
     peak = float(peaks.get("bf16_tflops", 1641.1))
@@ -242,12 +251,16 @@ def roofline_gate_up(torch, layer, x, mod, shape, args):
             traffic = json.loads(tf.read_text()).get(f"gate_up_{args.config}_{T}")
         except Exception:
             traffic = None
-    kname = ("realb_grouped_gemm_bf16_gather (K5 gate_up, TMA gather4 rows of x, SwiGLU epilogue)"
+    kname = ("realb_grouped_gemm_bf16_gather (K5 gate_up, cp.async-gathered rows of x, SwiGLU epilogue)"
              if layer.gather_dispatch else "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)")
     return {"kernel": kname, "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": f"{src} bf16_tflops (burst)",
-            "algorithmic_flops_per_launch": flops, "launch_ms": t * 1e3}
+            "algorithmic_flops_per_launch": flops, "launch_ms": t * 1e3,
+            "cublas_dense_same_flops": {"tflops": flops / t_ref / 1e12, "ms": t_ref * 1e3,
+                                        "frac_of_peak": flops / t_ref / 1e12 / peak,
+                                        "what": "torch.matmul [pairs x H] @ [H x 2I] bf16, same flops, "
+                                                "timed alternately with K5 in this run"}}
 
 
 # ----------------------------------------------------------------------------- CPU arms
