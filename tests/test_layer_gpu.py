@@ -449,3 +449,62 @@ def test_realb_seq_equals_realb():
     b = layer.forward(x, mod, "realb-seq", params).y.clone()
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+def test_full_size_kimi_ep8_batch_properties():
+    """BASELINE configs[1] at full size: the Kimi-VL layer (E=64, top-6, H=2048,
+    I=1408) over the EP8 global batch (8 x 8192 tokens, 70 % vision, tracegen skew)
+    with the ReaLB plan over 8 ranks, checked through size-independent
+    properties: routing bit-exact (D1) on every token and equal to the planned
+    expert sets; per-expert (vision, text) counts == the oracle's; the device plan
+    == the host policy (pinned to the reference); the hot rank's K3 codes and
+    scales bit-exact with the oracle quantiser; and a token sample of the layer
+    output within the W4A4 tolerance of the FP4-emulating oracle."""
+    from paper_2604_19503_b200.policy import plan_for, rank_loads_from_counts
+    from paper_2604_19503_b200.quant import sf_mma_to_flat
+
+    shape = SHAPES["kimi"]
+    T, R = 65536, 8
+    layer, x, mod, router, gu, dn, planned = build_layer(shape, T, R=R)
+    params = RealbParams()
+    res = layer.forward(x, mod, "realb", params)
+    torch.cuda.synchronize()
+    layer.check_flag()
+    E, k, H, I = shape.num_experts, shape.top_k, shape.hidden, shape.intermediate
+    logits = layer.logits[:T].cpu().numpy()
+    idx = layer.topk_idx[:T].cpu().numpy()
+    w = layer.topk_w[:T].cpu().numpy()
+    _, idx_ref, w_ref = moe_ref.route(None, router.float().cpu().numpy(), k, shape.scoring,
+                                      routed_scaling=shape.routed_scaling, logits=logits)
+    assert (idx == idx_ref).all()
+    np.testing.assert_allclose(w, w_ref, rtol=2e-5, atol=2e-6)
+    assert (np.sort(idx, 1) == np.sort(planned, 1)).all()
+    modh = mod.cpu().numpy()
+    vt = res.expert_vt.astype(np.int64)
+    assert (vt == moe_ref.expert_counts(idx_ref, modh, E)).all()
+    assert int(vt.sum()) == T * k
+    cluster = layer.cluster
+    ref_plan = plan_for("realb", rank_loads_from_counts(vt, cluster), cluster, params)
+    assert res.plan.active and ref_plan.active
+    assert sorted(res.plan.accelerated_ranks) == sorted(ref_plan.accelerated_ranks) != []
+    prec = res.plan.expert_precision(layer.placement)
+    # K3 on the hot rank: codes + scales of its first expert's gate_up and down weights
+    ws = layer._fp4_ws()
+    e = int(np.nonzero(prec)[0][0])
+    for wt, codes, sf, rows, cols in ((layer.w.w_gu, ws["wgu_codes"], ws["wgu_sf"], 2 * I, H),
+                                      (layer.w.w_d, ws["wd_codes"], ws["wd_sf"], H, I)):
+        wbits = wt[e * rows:(e + 1) * rows].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        c_ref, s_ref = oracle.quantize_bf16(wbits)
+        c = codes[e * rows:(e + 1) * rows].cpu().numpy()
+        s = sf.view(-1)[e * rows * cols // 16:(e + 1) * rows * cols // 16].cpu().numpy()
+        assert (c == c_ref).all()
+        assert (sf_mma_to_flat(s, rows, cols) == s_ref).all()
+    # the layer output on a token sample (per-token independent given the routing)
+    sel = np.random.default_rng(5).choice(T, 48, replace=False)
+    sel_t = torch.from_numpy(sel).cuda()
+    ref = moe_ref.moe_layer(x[sel_t].float().cpu().numpy(), modh[sel], router.float().cpu().numpy(),
+                            gu.float().cpu().numpy(), dn.float().cpu().numpy(), k, shape.scoring,
+                            expert_prec=prec, routed_scaling=shape.routed_scaling, logits=logits[sel])
+    y = res.y[sel_t].float().cpu().numpy()
+    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
+    assert err < 2e-2, err
