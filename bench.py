@@ -251,8 +251,10 @@ def roofline_gate_up(torch, layer, x, mod, shape, args):
             traffic = json.loads(tf.read_text()).get(f"gate_up_{args.config}_{T}")
         except Exception:
             traffic = None
-    kname = ("realb_grouped_gemm_bf16_gather (K5 gate_up, cp.async-gathered rows of x, SwiGLU epilogue)"
-             if layer.gather_dispatch else "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)")
+    kname = {"gather": "realb_grouped_gemm_bf16_gather (K5 gate_up, cp.async-gathered rows of x, SwiGLU epilogue)",
+             "copyin": "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue; timed on the rows its copy-in "
+                       "form left in A)",
+             "copy": "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)"}[layer.dispatch_mode]
     return {"kernel": kname, "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": f"{src} bf16_tflops (burst)",

@@ -341,6 +341,18 @@ REALB_API int realb_grouped_gemm_bf16_gather(const void* d_x, int64_t n_src, con
                                              const int32_t* d_layout, int prec, int epilogue, void* d_out,
                                              int max_ctas, void* stream);
 
+/* K5, copy-in form: the dispatch row copy runs INSIDE the GEMM. Warps 2-3 of every
+ * CTA copy x[d_row_src[g]] -> d_a[g] for the class's valid grouped rows (in grouped
+ * order across the grid) while the mainloop runs; the producer's first load of an
+ * expert's tiles waits for that expert's rows (per-expert counters d_ready [E],
+ * int32, zero on entry and re-zeroed by the kernel). d_err bit 2 is set if a wait
+ * timed out. With realb_dispatch_index this replaces realb_dispatch_permute's row
+ * copy for W16A16 experts; the copy overlaps the GEMM instead of preceding it. */
+REALB_API int realb_grouped_gemm_bf16_copyin(const void* d_x, const int32_t* d_row_src, void* d_a, const void* d_w,
+                                             int64_t rows_cap, int N, int K, int E, const int32_t* d_layout,
+                                             int prec, int epilogue, void* d_out, int32_t* d_ready,
+                                             int32_t* d_err, int max_ctas, void* stream);
+
 /* K5 fused with the EP return (C3 over peer memory): the STORE epilogue, but
  * output row g goes to h_dst_bases[m >> 25] + (m & (2^25 - 1)) * N * 2 with
  * m = d_row_map[g] (int32 [rows_cap]; realb_p2p_return_map builds it), i.e.

@@ -80,14 +80,34 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 }
 constexpr int kGatherWarps = 2;  // warps 2..3 load A in the gather form
 
-template <int BN, int STAGES, int EPI, int CL, bool GATHER>
+// copy-in form: warps 2-3 of every CTA copy the dispatch rows x[row_src[g]] -> A[g]
+// (the class's valid rows, in grouped order across the grid) while the mainloop
+// runs; per-expert row counters (release) gate the producer's first load of an
+// expert's tiles (acquire). The copy overlaps the GEMM instead of preceding it.
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+struct CopyIn {
+  const __nv_bfloat16* x;  // token rows [*, K]
+  const int32_t* row_src;  // grouped row -> token
+  __nv_bfloat16* a;        // the A operand [rows_cap, K] (also read by TMA)
+  int32_t* ready;          // [E] rows copied per expert (zero on entry; the last CTA re-zeroes)
+  int32_t* err;            // bit 2: a producer wait timed out
+};
+
+template <int BN, int STAGES, int EPI, int CL, bool GATHER, bool COPYIN = false>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut, const int32_t* layout,
                              int E, int prec, int N, int K, uint32_t dbg,
                              const __nv_bfloat16* __restrict__ xsrc, const int32_t* __restrict__ row_src,
-                             const __grid_constant__ RowScatter scat) {
+                             const __grid_constant__ RowScatter scat, const CopyIn cin) {
   static_assert(!GATHER || CL == 1, "the gather form is 1-CTA only");
   using S = SmemBf16<BN, STAGES, CL>;
   extern __shared__ uint8_t smem_raw[];
@@ -161,6 +181,7 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t full0 = CL == 2 ? mapa_shared(&full[0], 0) : smem_u32(&full[0]);
     int stage = 0;
     uint32_t phase = 0;
+    int ready_group = -1;  // copy-in: last expert whose rows were seen complete
     for (int i = 0;; ++i) {
       const int slot = i % kTileRing;
       int t = 0;
@@ -193,6 +214,25 @@ __global__ void __launch_bounds__(256, 1)
       const int brow = __shfl_sync(0xffffffffu, c.group * N + c.n0, 0);
       dummy = __shfl_sync(0xffffffffu, (int)dummy, 0) != 0;
       dummy1 = __shfl_sync(0xffffffffu, (int)dummy1, 0) != 0;
+      if constexpr (COPYIN) {
+        const int grp = __shfl_sync(0xffffffffu, c.group, 0);
+        if (grp != ready_group) {
+          if (leader) {
+            const int need = sched.row_count[grp];
+            long long spins = 0;
+            while (ld_acquire_gpu(cin.ready + grp) < need) {
+              __nanosleep(64);
+              if (++spins > (1LL << 24)) {  // ~1 s: report instead of hanging
+                atomicOr(cin.err, 4);
+                break;
+              }
+            }
+            fence_proxy_async_global();  // generic-proxy row stores -> TMA reads
+          }
+          __syncwarp();
+          ready_group = grp;
+        }
+      }
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if constexpr (GATHER) {  // W only; A comes from the loader warps
@@ -266,6 +306,45 @@ __global__ void __launch_bounds__(256, 1)
       }
       __syncwarp();
     }
+  } else if (COPYIN && (warp == 2 || warp == 3)) {  // ---------------- dispatch row copy (copy-in form)
+    // compact index v over the class's valid rows (groups in glist order), strided
+    // over every copy warp of the grid: increasing v = increasing grouped row
+    const int nw = (int)gridDim.x * 2, wid = (int)blockIdx.x * 2 + (warp - 2);
+    const int rowv = K / 8;  // uint4 per row
+    int gi = 0, e = -1, cnt = 0, pending = 0;
+    int64_t cum0 = 0;
+    if (sched.G > 0) { e = sched.glist[0]; cnt = sched.row_count[e]; }
+    auto flush = [&]() {
+      if (pending) {  // all lanes: make this warp's row stores visible (both proxies), then count them
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(cin.ready + e, pending);
+        pending = 0;
+      }
+    };
+    for (int64_t v = wid;; v += nw) {
+      while (gi < sched.G && v >= cum0 + cnt) {
+        flush();
+        cum0 += cnt;
+        if (++gi < sched.G) { e = sched.glist[gi]; cnt = sched.row_count[e]; }
+      }
+      if (gi >= sched.G) break;
+      const int64_t g = sched.row_start[e] + (v - cum0);
+      const uint4* src = reinterpret_cast<const uint4*>(cin.x + (int64_t)__ldg(cin.row_src + g) * K);
+      uint4* dst = reinterpret_cast<uint4*>(cin.a + g * K);
+      for (int i0 = 0; i0 < rowv; i0 += 32 * 8) {  // 8 loads in flight per lane, then the stores
+        uint4 r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (i0 + j * 32 + lane < rowv) r[j] = __ldg(src + i0 + j * 32 + lane);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (i0 + j * 32 + lane < rowv) dst[i0 + j * 32 + lane] = r[j];
+      }
+      ++pending;
+    }
+    flush();
   } else if (GATHER && (warp == 2 || warp == 3)) {  // ---------------- A loaders (gather form)
     // warp w loads rows 64(w-2) .. +63 of the m-block: instruction i covers rows
     // 4i + lane/8 (16-B piece lane%8 of each), 16 instructions per k-block
@@ -388,14 +467,27 @@ __global__ void __launch_bounds__(256, 1)
     if constexpr (CL == 2) tmem_dealloc_2sm<2 * BN>(tmem_base);
     else tmem_dealloc<2 * BN>(tmem_base);
   }
-  if (threadIdx.x == 0) GroupedSched::finish(layout, prec);
+  if (threadIdx.x == 0) {
+    if constexpr (COPYIN) {  // the last CTA re-zeroes the row counters for the next launch
+      int* c = GroupedSched::counters(layout, prec);
+      __threadfence();
+      if (atomicAdd(c + 1, 1) == (int)gridDim.x - 1) {
+        for (int i = 0; i < E; ++i) cin.ready[i] = 0;
+        c[0] = 0;
+        c[1] = 0;
+        __threadfence();
+      }
+    } else {
+      GroupedSched::finish(layout, prec);
+    }
+  }
 }
 
-template <int BN, int STAGES, int EPI, int CL, bool GATHER = false>
+template <int BN, int STAGES, int EPI, int CL, bool GATHER = false, bool COPYIN = false>
 static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, int N, int K, int E,
                                const int32_t* layout, int prec, void* out, int max_ctas,
                                cudaStream_t st, const int32_t* row_src = nullptr,
-                               const RowScatter* scat = nullptr) {
+                               const RowScatter* scat = nullptr, const CopyIn* copyin = nullptr) {
   CUtensorMap ta, tb, to;
   // gather form: A is read by the loader warps (the A map is unused, built over x)
   int rc = make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a, K, GATHER ? 1 : rows_cap, (uint64_t)K * 2,
@@ -410,7 +502,7 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
                     EPI == kEpiScatter ? 1 : rows_cap, (uint64_t)NO * 2, 32, EPI == kEpiScatter ? 1 : 32,
                     CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
-  auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL, GATHER>;
+  auto kern = grouped_gemm_bf16_kernel<BN, STAGES, EPI, CL, GATHER, COPYIN>;
   const int smem = SmemBf16<BN, STAGES, CL>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_bf16: smem attribute");
   if (rc) return rc;
@@ -434,8 +526,10 @@ static int launch_grouped_bf16(const void* a, const void* w, int64_t rows_cap, i
   cfg.numAttrs = 1;
   RowScatter sc{};
   if (scat) sc = *scat;
+  CopyIn ci{};
+  if (copyin) ci = *copyin;
   rc = cuda_status(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, layout, E, prec, N, K, dbg,
-                                      reinterpret_cast<const __nv_bfloat16*>(a), row_src, sc),
+                                      reinterpret_cast<const __nv_bfloat16*>(a), row_src, sc, ci),
                    "realb_grouped_gemm_bf16 launch");
   if (rc) return rc;
   return check_launch("realb_grouped_gemm_bf16");
@@ -530,4 +624,31 @@ extern "C" int realb_grouped_gemm_bf16_scatter(const void* d_a, const void* d_w,
   sc.ld = (int64_t)N * 2;
   return launch_grouped_bf16<256, 4, kEpiScatter, 1>(d_a, d_w, rows_cap, N, K, E, d_layout, prec, nullptr,
                                                      max_ctas, (cudaStream_t)stream, nullptr, &sc);
+}
+
+extern "C" int realb_grouped_gemm_bf16_copyin(const void* d_x, const int32_t* d_row_src, void* d_a, const void* d_w,
+                                              int64_t rows_cap, int N, int K, int E, const int32_t* d_layout,
+                                              int prec, int epilogue, void* d_out, int32_t* d_ready,
+                                              int32_t* d_err, int max_ctas, void* stream) {
+  if (!d_x || !d_row_src || !d_a || !d_w || !d_layout || !d_out || !d_ready || !d_err || rows_cap <= 0 ||
+      E <= 0 || (prec != REALB_PREC_W16A16 && prec != REALB_PREC_W4A4)) {
+    set_error("realb_grouped_gemm_bf16_copyin: bad arguments");
+    return REALB_EINVAL;
+  }
+  if (K % kBK || N % 256) {
+    set_error("realb_grouped_gemm_bf16_copyin: needs K %% 64 == 0 and N %% 256 == 0 (N=%d K=%d)", N, K);
+    return REALB_EUNSUPPORTED;
+  }
+  CopyIn ci{reinterpret_cast<const __nv_bfloat16*>(d_x), d_row_src, reinterpret_cast<__nv_bfloat16*>(d_a), d_ready,
+            d_err};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (epilogue == REALB_EPI_STORE)
+    return launch_grouped_bf16<256, 4, REALB_EPI_STORE, 1, false, true>(d_a, d_w, rows_cap, N, K, E, d_layout, prec,
+                                                                        d_out, max_ctas, st, nullptr, nullptr, &ci);
+  if (epilogue == REALB_EPI_SWIGLU)
+    return launch_grouped_bf16<256, 4, REALB_EPI_SWIGLU, 1, false, true>(d_a, d_w, rows_cap, N, K, E, d_layout,
+                                                                         prec, d_out, max_ctas, st, nullptr,
+                                                                         nullptr, &ci);
+  set_error("realb_grouped_gemm_bf16_copyin: unknown epilogue %d", epilogue);
+  return REALB_EINVAL;
 }

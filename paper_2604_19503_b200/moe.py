@@ -313,13 +313,15 @@ class MoELayer:
         self.plan_host = torch.zeros(3 + self.cluster.num_ranks, dtype=i32, pin_memory=True)
         R = self.rows_cap
         self.a_bf16 = torch.empty(R, H, dtype=bf, device=dev)
-        # gather dispatch: the gate_up GEMM reads token rows straight from x through
-        # row_src (grouped row -> token, realb_dispatch_index) instead of a copy into
-        # a_bf16 (realb_dispatch_permute). Off by default: measured interleaved on the
-        # Kimi 8192-token layer the two are equal (0.977 ms both; the gather GEMM's
-        # cp.async loaders cost what the 39 us row copy saves; scripts/bench_dispatch.py)
-        self.gather_dispatch = False
+        # How the W16A16 rows reach K5 (scripts/bench_dispatch.py measures all three):
+        #   "copy"   realb_dispatch_permute copies them into a_bf16, then K5
+        #   "gather" K5 reads them from x through row_src (cp.async loaders)
+        #   "copyin" K5's spare warps copy them into a_bf16 while its mainloop runs,
+        #            gated per expert (realb_grouped_gemm_bf16_copyin)
+        self.dispatch_mode = "copy"
         self.row_src = torch.zeros(R, dtype=i32, device=dev)
+        self.ready = torch.zeros(E, dtype=i32, device=dev)     # copy-in per-expert row counters
+        self.copy_err = torch.zeros(1, dtype=i32, device=dev)  # copy-in wait timeout flag
         self._x_src = None  # (x, T) of the last forward: the gather GEMM's A
         self.h_bf16 = torch.empty(R, I, dtype=bf, device=dev)
         self.rows_out = torch.empty(R, H, dtype=bf, device=dev)
@@ -450,7 +452,7 @@ class MoELayer:
             ws = None
         mark("dispatch_start", main)
         self._x_src = (x, T)
-        if self.gather_dispatch:
+        if self.dispatch_mode in ("gather", "copyin"):
             _lib.call("realb_dispatch_index", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
                       self.prec_dev.data_ptr(), self.layout.data_ptr(), nch, self.rows_cap,
                       self.pair_pos.data_ptr(), self.row_src.data_ptr(),
@@ -464,7 +466,7 @@ class MoELayer:
                       self.flag.data_ptr(), sp)
         mark("dispatch_end", main)
         lay = self.layout.data_ptr()
-        self._gate_up_bf16(lay, sp)
+        self._gate_up_bf16(lay, sp, in_forward=True)
         if ws is not None:
             mark("fp4_ready", main)  # main stream reaches the first W4A4 GEMM
             if k3_stream is not main:
@@ -544,11 +546,18 @@ class MoELayer:
                   self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
                   self.rows_out.data_ptr(), 0, sp)
 
-    def _gate_up_bf16(self, lay: int, sp: int) -> None:
+    def _gate_up_bf16(self, lay: int, sp: int, in_forward: bool = False) -> None:
         """K5 gate_up (+ SwiGLU) of the W16A16 experts: the gather form reads the
-        rows of the last forward's x through row_src; the copy form reads a_bf16."""
+        rows of the last forward's x through row_src; the copy form reads a_bf16;
+        the copy-in form (forward only) fills a_bf16 inside the GEMM."""
         H, I, E = self.H, self.I, self.E
-        if self.gather_dispatch and self._x_src is not None:
+        if self.dispatch_mode == "copyin" and in_forward:
+            x, T = self._x_src
+            _lib.call("realb_grouped_gemm_bf16_copyin", x.data_ptr(), self.row_src.data_ptr(),
+                      self.a_bf16.data_ptr(), self.w.w_gu.data_ptr(), self.rows_cap, 2 * I, H, E, lay,
+                      _lib.PREC_W16A16, _lib.EPI_SWIGLU, self.h_bf16.data_ptr(), self.ready.data_ptr(),
+                      self.copy_err.data_ptr(), 0, sp)
+        elif self.dispatch_mode == "gather" and self._x_src is not None:
             x, T = self._x_src
             if T == 0:
                 return
@@ -563,6 +572,9 @@ class MoELayer:
     def check_flag(self):
         from .quant import QuantizationDomainError
 
+        if int(self.copy_err.item()):
+            self.copy_err.zero_()
+            raise RuntimeError("copy-in dispatch: a K5 producer timed out waiting for its rows")
         if int(self.flag.item()):
             self.flag.zero_()
             raise QuantizationDomainError("non-finite value reached the NVFP4 quantiser")

@@ -1,6 +1,7 @@
-"""A/B: the single-GPU layer with copy dispatch (realb_dispatch_permute + K5 on
-the grouped operand) vs gather dispatch (realb_dispatch_index + K5 reading x
-rows by TMA tile::gather4), each captured as one CUDA graph, timed interleaved
+"""A/B/C: the single-GPU layer with copy dispatch (realb_dispatch_permute + K5 on
+the grouped operand), gather dispatch (realb_dispatch_index + K5 reading x rows
+with cp.async loaders) and copy-in dispatch (realb_dispatch_index + K5 whose
+spare warps copy the rows while its mainloop runs), each captured as one CUDA graph, timed interleaved
 (bench_fp4.interleaved, L2 not flushed) with NVML clocks; plus the two gate_up
 kernels alone.
 
@@ -35,18 +36,19 @@ def main():
     x, mod, router, _ = make_batch(shape, WorkloadSpec(tokens=T, num_ranks=1, rank=0), device="cuda")
     gu, dn = make_experts(shape, device="cuda")
     layers, graphs = {}, {}
-    for mode in ("copy", "gather"):
+    for mode in ("copy", "gather", "copyin"):
         layer = MoELayer(MoEWeights.from_hf(shape, router, gu, dn), max_tokens=T,
                          cluster=ClusterConfig(1, 1, shape.num_experts, 1, shape.modality_isolated))
-        layer.gather_dispatch = mode == "gather"
+        layer.dispatch_mode = mode
         layers[mode] = layer
         graphs[mode] = layer.capture(x, mod, "realb")
     torch.cuda.synchronize()
-    assert torch.equal(graphs["copy"].y, graphs["gather"].y)
+    assert torch.equal(graphs["copy"].y, graphs["gather"].y) and torch.equal(graphs["copy"].y, graphs["copyin"].y)
     sp = _lib.stream_ptr()
     variants = {f"layer_{m}": ({}, graphs[m].replay) for m in graphs}
     for m, layer in layers.items():
-        variants[f"gate_up_{m}"] = ({}, lambda layer=layer: layer._gate_up_bf16(layer.layout.data_ptr(), sp))
+        variants[f"gate_up_{m}"] = ({}, lambda layer=layer: layer._gate_up_bf16(layer.layout.data_ptr(), sp,
+                                                                                 in_forward=True))
     with ClockSampler(0) as clk:
         res = interleaved(variants)
     out = {"config": a.config, "tokens": T, "ms": res, "clocks": clk.summary()}

@@ -153,17 +153,21 @@ def test_dispatch_index_inverse_map(name, E, T):
 @pytest.mark.parametrize("name,E,T,strategy", [("kimi", 16, 700, "baseline"), ("qwen", 32, 300, "fp4all"),
                                                ("tiny", None, 1024, "realb")])
 def test_gather_dispatch_equals_copy_dispatch(name, E, T, strategy):
-    """The layer with gather dispatch equals the copy-dispatch layer
-    bit for bit, W4A4 experts included."""
+    """The layer with gather dispatch and with copy-in dispatch equals the
+    copy-dispatch layer bit for bit, W4A4 experts included."""
     shape = small(SHAPES[name], E)
     layer, x, mod, *_ = build_layer(shape, T, R=2)
     params = RealbParams(global_batch_threshold=0)
-    layer.gather_dispatch = False
+    layer.dispatch_mode = "copy"
     y0 = layer.forward(x, mod, strategy, params).y.clone()
-    layer.gather_dispatch = True
-    y1 = layer.forward(x, mod, strategy, params).y.clone()
-    torch.cuda.synchronize()
-    assert torch.equal(y0, y1)
+    for mode in ("gather", "copyin", "copyin"):  # copy-in twice: its counters re-arm
+        layer.dispatch_mode = mode
+        layer.a_bf16.fill_(float("nan"))
+        y1 = layer.forward(x, mod, strategy, params).y.clone()
+        torch.cuda.synchronize()
+        layer.check_flag()
+        assert torch.equal(y0, y1), mode
+    assert int(layer.ready.abs().sum()) == 0
 
 
 def test_combine_weighted_sum():
