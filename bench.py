@@ -30,7 +30,7 @@ METRIC = "MoE-layer prefill tokens/s and speedup vs all-BF16 EP at 1/2/4/8 B200"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="kimi", choices=["tiny", "kimi", "kimi_shared", "qwen", "ernie_vision"])

@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t adesc = umma_desc_sw128(sa), bdesc = umma_desc_sw128(sa + S::A_BYTES);
 #pragma unroll
         for (int kk = 0; kk < kRBK / 16; ++kk)
-          umma_bf16(tmem_base, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
-                    (kb | kk) != 0);
+          if (!(dbg & 8u) || kk == 0)  // debug bit 8: one MMA per stage (timing probe)
+            umma_bf16(tmem_base, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                      (kb | kk) != 0);
         tc_commit(&empty[stage]);
         if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
       }

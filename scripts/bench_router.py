@@ -16,7 +16,7 @@ for T in (8192, 65536):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     for stages in ("4", "8"):
         os.environ["REALB_ROUTER_STAGES"] = stages
-        for dbg in (0, 1, 4, 5):
+        for dbg in (0, 1, 4, 5, 13):
             os.environ["REALB_DBG_ROUTER"] = str(dbg)
             for _ in range(3): f()
             torch.cuda.synchronize()
