@@ -35,7 +35,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .moe import MoEShape, MoEWeights
+from .moe import MoEShape, MoEWeights, operand_noise_
 from .policy import STRATEGIES, ClusterConfig, Precision, PrecisionPlan, RealbParams, plan_for, \
     rank_loads_from_counts
 
@@ -112,7 +112,7 @@ class CudaEPOps:
         self.cnt_dev = torch.empty(world, El, dtype=i32, device=dev)
         self.cnt_host = torch.empty(world, El, dtype=i32, pin_memory=True)
         self.prec_local = torch.zeros(El, dtype=u8, device=dev)
-        self.a_bf16 = torch.empty(self.rows_cap, H, dtype=bf, device=dev)
+        self.a_bf16 = operand_noise_(torch.empty(self.rows_cap, H, dtype=bf, device=dev))
         self.h_bf16 = torch.empty(self.rows_cap, I, dtype=bf, device=dev)
         self.rows_out = torch.empty(self.rows_cap, H, dtype=bf, device=dev)
         self.flag = torch.zeros(1, dtype=i32, device=dev)
@@ -130,8 +130,8 @@ class CudaEPOps:
             El, H, I, R = self.El, self.H, self.I, self.rows_cap
             u8, dev = torch.uint8, self.dev
             self._fp4 = dict(
-                a_codes=torch.empty(R, H // 2, dtype=u8, device=dev),
-                a_sf=torch.empty(R * H // 16, dtype=u8, device=dev),
+                a_codes=operand_noise_(torch.empty(R, H // 2, dtype=u8, device=dev), "codes"),
+                a_sf=operand_noise_(torch.empty(R * H // 16, dtype=u8, device=dev), "sf"),
                 h_codes=torch.empty(R, I // 2, dtype=u8, device=dev),
                 h_sf=torch.empty(R * I // 16, dtype=u8, device=dev),
                 wgu_codes=torch.empty(El * 2 * I, H // 2, dtype=u8, device=dev),
@@ -271,6 +271,19 @@ class CudaEPOps:
         # peers' operand bases (kept alive: the ABI reads them through a host pointer)
         self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "ops")]
         self.ret_bases = np.array(self.p2p["ret"], np.uint64)
+        # my operand windows (written by the senders) start as in-distribution values,
+        # not the allocation's zeros: their padding rows are multiplied too (moe.operand_noise_)
+        own = self._p2p_own
+        noise = operand_noise_(torch.empty(min(self.rows_cap, 1 << 16), H, dtype=torch.bfloat16, device=self.dev))
+        nb = noise.view(torch.uint8).view(-1)
+        va = _device_view(own["opa"], sizes["opa"], torch.uint8)
+        for i in range(0, va.numel(), nb.numel()):
+            n = min(nb.numel(), va.numel() - i)
+            va[i:i + n].copy_(nb[:n])
+        operand_noise_(_device_view(own["opc"], sizes["opc"], torch.uint8), "codes")
+        operand_noise_(_device_view(own["ops"], sizes["ops"], torch.uint8), "sf")
+        del noise, nb
+        torch.cuda.synchronize()
         # fused down-GEMM + return: grouped row -> (source, row of its return window)
         self.row_map = torch.empty(self.rows_cap, dtype=torch.int32, device=self.dev)
         # host-sync-free (device-plan) form: plan record, expected-counter words,
