@@ -367,10 +367,12 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t nbytes = 0;  // bit j: row of instruction j is real
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
+        // padding rows (results never read) repeat a valid row of the tile rather than
+        // zero-fill: zero operand rows slow the tensor pipe (data-dependent speed)
         const int r = rbase + 4 * j + rsub;
-        const bool ok = r < c.valid;
-        src[j] = xsrc + (ok ? (int64_t)__ldg(row_src + c.a_row + r) * ldx : 0) + piece * 8;
-        nbytes |= (ok ? 1u : 0u) << j;
+        const int rv = r < c.valid ? r : r % c.valid;
+        src[j] = xsrc + (int64_t)__ldg(row_src + c.a_row + rv) * ldx + piece * 8;
+        nbytes |= 1u << j;
       }
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);

@@ -96,8 +96,8 @@ def test_grouped_bf16_precision_subset():
 def test_grouped_bf16_gather_equals_copy(E, N, K, counts, T, epi):
     """The gather form (A rows read from x through row_src by TMA tile::gather4)
     gives bit-for-bit the rows the grouped-operand form gives on the copied rows
-    (same MMAs in the same order); padding rows of each group are never stored
-    from garbage (they read as zero)."""
+    (same MMAs in the same order); padding rows repeat valid rows of their tile
+    (activation-like operands), so their outputs are finite."""
     torch.manual_seed(E + N + K + T)
     prec_sel = np.zeros(E, np.int64)
     lay, rows = host_layout(counts, prec_sel)
@@ -118,8 +118,8 @@ def test_grouped_bf16_gather_equals_copy(E, N, K, counts, T, epi):
         c = counts[e]
         assert torch.equal(out[rs:rs + c], ref[rs:rs + c]), e
         pad = (c + 127) // 128 * 128
-        if pad > c:  # padding rows: computed on zero rows -> zero (SwiGLU(0,0) = 0)
-            assert (out[rs + c:rs + pad].float() == 0).all(), e
+        if pad > c:  # padding rows repeat valid rows of their tile: finite, never NaN garbage
+            assert torch.isfinite(out[rs + c:rs + pad].float()).all(), e
 
 
 @pytest.mark.parametrize("E,N,K,counts,n_dst", [
