@@ -455,9 +455,11 @@ def test_realb_seq_equals_realb():
     assert torch.equal(a, b)
 
 
-def test_full_size_kimi_ep8_batch_properties():
-    """BASELINE configs[1] at full size: the Kimi-VL layer (E=64, top-6, H=2048,
-    I=1408) over the EP8 global batch (8 x 8192 tokens, 70 % vision, tracegen skew)
+@pytest.mark.parametrize("name", ["kimi", "qwen"])
+def test_full_size_ep8_batch_properties(name):
+    """BASELINE configs[1] / [2] at full size: the Kimi-VL layer (E=64, top-6,
+    H=2048, I=1408) and the Qwen3-VL layer (E=128, top-8, I=768) over the EP8
+    global batch (8 x 8192 tokens, 70 % vision, tracegen skew)
     with the ReaLB plan over 8 ranks, checked through size-independent
     properties: routing bit-exact (D1) on every token and equal to the planned
     expert sets; per-expert (vision, text) counts == the oracle's; the device plan
@@ -467,7 +469,7 @@ def test_full_size_kimi_ep8_batch_properties():
     from paper_2604_19503_b200.policy import plan_for, rank_loads_from_counts
     from paper_2604_19503_b200.quant import sf_mma_to_flat
 
-    shape = SHAPES["kimi"]
+    shape = SHAPES[name]
     T, R = 65536, 8
     layer, x, mod, router, gu, dn, planned = build_layer(shape, T, R=R)
     params = RealbParams()
