@@ -119,8 +119,16 @@ def test_ep2_host_sync_free_layer_and_graph(tmp_path, shape_name, E, T, strategy
     _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=True, device_plan=True)
 
 
-def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False):
-    world = 2
+@pytest.mark.parametrize("world,shape_name,E,T,strategy,fp4_dispatch", [
+    (4, "kimi", 16, 256, "realb", True), (4, "qwen", 32, 192, "fp4all", False)])
+def test_ep4_host_sync_free_layer_and_graph(tmp_path, world, shape_name, E, T, strategy, fp4_dispatch):
+    """The host-sync-free peer-memory layer with FOUR ranks (processes sharing one
+    GPU): plan over 4 ranks, window offsets for 4 sources, direct dispatch and the
+    fused return into 4 windows; eager == graph replay == the single-GPU layer."""
+    _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=True, device_plan=True, world=world)
+
+
+def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False, world=2):
     mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path), p2p,
                             device_plan), nprocs=world)
     from paper_2604_19503_b200 import _lib
