@@ -70,7 +70,8 @@ struct Fp4Args {
   uint8_t* out_codes;   // SWIGLU: E2M1 [rows][N/4]
   uint8_t* out_sf;      // SWIGLU: MMA-layout scales of the [rows][N/2] result
   uint32_t sf_lbo, sf_sbo;
-  uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies, 4 skip MMAs
+  uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies, 4 skip MMAs,
+                 // 8 release the accumulator without reading it
   RowScatter scat;  // kEpiScatter: per-row destinations (down GEMM fused with the EP return)
 };
 
@@ -345,6 +346,12 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       mbar_wait(tfull, tile_it & 1);
       tc_fence_after();
       const uint32_t tb = tmem_base + kTmemAcc + ((uint32_t)(q * 32) << 16);
+      if (args.dbg & 8u) {  // debug: release the accumulator unread (cost of the TMEM drain)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(tempty);
+        continue;
+      }
       uint32_t v[4][32];
       if constexpr (EPI == REALB_EPI_SWIGLU) {
         tmem_ld32(tb + half * 64, v[0]);
