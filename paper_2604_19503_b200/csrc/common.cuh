@@ -178,17 +178,21 @@ struct RowScatter {
 __device__ __forceinline__ uint8_t* scatter_row(const RowScatter& s, int32_t m) {
   return s.base[m >> kScatterRowBits] + (int64_t)(m & ((1 << kScatterRowBits) - 1)) * s.ld;
 }
-// 32 rows x 64 B staged in the SWIZZLE_64B layout (piece c of row r at c ^ ((r >> 1) & 3))
-// -> 8 rows x 64 B per warp instruction to each row's destination; m = this lane's row map
-__device__ __forceinline__ void scatter_chunk64(uint32_t buf, const RowScatter& s, int32_t m, int64_t col_bytes) {
-  const int lane = threadIdx.x & 31, pc = lane & 3;
+// Q consecutive 32-column chunks of 32 rows, chunk q staged at buf + q * 2048 in the
+// SWIZZLE_64B layout (piece c of row r at c ^ ((r >> 1) & 3)) -> each row's Q x 64 B
+// as ONE contiguous segment: 4Q lanes per row, 8/Q rows per warp instruction. Wide
+// segments keep the peer-memory (NVLink) writes at 128-256 B; m = this lane's row map.
+template <int Q>
+__device__ __forceinline__ void scatter_chunks(uint32_t buf, const RowScatter& s, int32_t m, int64_t col_bytes) {
+  constexpr int LPR = 4 * Q, RPI = 32 / LPR;  // lanes per row, rows per instruction
+  const int lane = threadIdx.x & 31, p = lane % LPR, q = p >> 2, pc = p & 3;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int rr = 8 * j + (lane >> 2);
+  for (int j = 0; j < 32 / RPI; ++j) {
+    const int rr = RPI * j + lane / LPR;
     const int32_t mr = __shfl_sync(0xffffffffu, m, rr);
     if (mr >= 0) {
-      const uint4 v = ld_shared_v4(buf + rr * 64 + ((pc ^ ((rr >> 1) & 3)) << 4));
-      *reinterpret_cast<uint4*>(scatter_row(s, mr) + col_bytes + pc * 16) = v;
+      const uint4 v = ld_shared_v4(buf + q * 2048 + rr * 64 + ((pc ^ ((rr >> 1) & 3)) << 4));
+      *reinterpret_cast<uint4*>(scatter_row(s, mr) + col_bytes + p * 16) = v;
     }
   }
 }

@@ -434,11 +434,14 @@ __global__ void __launch_bounds__(256, 1)
             p[j] = pack_bf16x2(silu_mul(__uint_as_float(g[2 * j]), __uint_as_float(u[2 * j])),
                                silu_mul(__uint_as_float(g[2 * j + 1]), __uint_as_float(u[2 * j + 1])));
         }
-        if constexpr (EPI == kEpiScatter) {  // stage, then 8 rows x 64 B per store instruction
-          stage_row64(ebuf, lane, p);
-          __syncwarp();
-          scatter_chunk64(ebuf, scat, smap, (int64_t)(c.n0 + ch * 32) * 2);
-          __syncwarp();
+        if constexpr (EPI == kEpiScatter) {  // stage 4 chunks, then 256-B row segments
+          static_assert(kEpiBufs == 4, "the scatter epilogue stages four chunks");
+          stage_row64(ebuf + (ch & 3) * 2048, lane, p);
+          if ((ch & 3) == 3) {
+            __syncwarp();
+            scatter_chunks<4>(ebuf, scat, smap, (int64_t)(c.n0 + (ch - 3) * 32) * 2);
+            __syncwarp();
+          }
           continue;
         }
         // the buffer about to be reused must have been read out by its TMA store

@@ -377,13 +377,16 @@ __global__ void __launch_bounds__(kF4Threads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             p[j] = pack_bf16x2(__uint_as_float(v[i][2 * j]), __uint_as_float(v[i][2 * j + 1]));
+          const uint32_t b = ebuf + (i & 1) * 2048;  // two chunks staged -> 128-B row segments
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc)
-            st_shared_v4(ebuf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), p[4 * cc], p[4 * cc + 1],
+            st_shared_v4(b + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), p[4 * cc], p[4 * cc + 1],
                          p[4 * cc + 2], p[4 * cc + 3]);
-          __syncwarp();
-          scatter_chunk64(ebuf, args.scat, smap, (int64_t)(c.n0 + half * 128 + 32 * i) * 2);
-          __syncwarp();
+          if (i & 1) {
+            __syncwarp();
+            scatter_chunks<2>(ebuf, args.scat, smap, (int64_t)(c.n0 + half * 128 + 32 * (i - 1)) * 2);
+            __syncwarp();
+          }
         }
         continue;
       }
