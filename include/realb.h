@@ -301,14 +301,21 @@ REALB_API int realb_p2p_return_map(const int32_t* d_row_pos, int64_t n_cap, int 
 /* Direct dispatch: each (token, slot) row goes straight to its destination's GEMM
  * operand at its final grouped row (realb_ep_regroup's layout, derived from the
  * gathered counts in d_plan): bf16 into h_peer_a[d] for a W16A16 destination,
- * NVFP4 codes into h_peer_codes[d] + MMA-layout scales into h_peer_sf[d] (the K4
- * rule) for a W4A4 one. d_layout: my row_align-1 send layout (expert starts). The
- * receiver then needs no gather. */
+ * NVFP4 codes into h_peer_codes[d] (the K4 rule) for a W4A4 one, with its scales
+ * ROW-MAJOR ([rows_cap][H/16] bytes) into h_peer_sf[d]; the W4A4 receiver turns
+ * those into the MMA layout with realb_sf_rows_to_mma. Every warp store is one
+ * contiguous span (wide peer-memory writes). d_layout: my row_align-1 send layout
+ * (expert starts). The receiver runs no row gather. */
 REALB_API int realb_p2p_pack_direct(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
                                     const int32_t* d_layout, int nchunks, int R, const uint64_t* h_peer_a,
                                     const uint64_t* h_peer_codes, const uint64_t* h_peer_sf,
                                     const void* d_plan, int32_t* d_pair_pos, int32_t* d_nonfinite_flag,
                                     void* stream);
+
+/* Row-major NVFP4 scales [rows][K/16] -> the MMA 128x4 scale layout, for the valid
+ * rows of the groups of precision class `prec` in d_layout (E groups). */
+REALB_API int realb_sf_rows_to_mma(const uint8_t* d_sf_rows, int64_t rows_cap, int K, const int32_t* d_layout,
+                                   int E, int prec, uint8_t* d_sf_mma, void* stream);
 
 /* dst[i] = src[idx[i]] for bf16 rows of H (EP return path before C3). */
 REALB_API int realb_index_rows(const void* d_src, const int32_t* d_idx, int64_t n, int H,

@@ -65,6 +65,7 @@ SIGNATURES: dict[str, tuple] = {
     "realb_grouped_gemm_nvfp4_scatter": (
         _i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _i32, _vp]),
     "realb_p2p_return_map": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
+    "realb_sf_rows_to_mma": (_i32, [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _vp]),
     "realb_dispatch_index": (
         _i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "realb_grouped_gemm_nvfp4": (
@@ -102,7 +103,7 @@ LAUNCHES_KERNEL = {
     "realb_quantize_nvfp4": 1, "realb_router_topk_stats": 1, "realb_moe_align": 1,
     "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_bf16_gather": 1, "realb_grouped_gemm_nvfp4": 1,
-    "realb_grouped_gemm_bf16_copyin": 1, "realb_grouped_gemm_bf16_scatter": 1, "realb_grouped_gemm_nvfp4_scatter": 1, "realb_p2p_return_map": 1,
+    "realb_grouped_gemm_bf16_copyin": 1, "realb_grouped_gemm_bf16_scatter": 1, "realb_grouped_gemm_nvfp4_scatter": 1, "realb_p2p_return_map": 1, "realb_sf_rows_to_mma": 1,
     "realb_dispatch_index": 1,  # + 1 when NVFP4 rows are quantised (call() adds it) "realb_combine": 1,
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,

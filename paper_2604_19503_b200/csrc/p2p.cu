@@ -279,14 +279,18 @@ __global__ void __launch_bounds__(256) p2p_pack_dev_kernel(const __nv_bfloat16* 
 struct PeerOperands {
   __nv_bfloat16* a[kMaxPeers];  // peer d's bf16 GEMM operand rows [rows_cap][H]
   uint8_t* codes[kMaxPeers];    // peer d's NVFP4 operand codes [rows_cap][H/2]
-  uint8_t* sf[kMaxPeers];       // peer d's NVFP4 operand scales (MMA 128x4 layout)
+  uint8_t* sf[kMaxPeers];       // peer d's NVFP4 scales, ROW-MAJOR staging [rows_cap][H/16]
   int R, El;
 };
 
 // Direct dispatch: every (token, slot) row is written straight into its
 // destination's GEMM operand at its final grouped row — bf16 for a W16A16
-// destination, NVFP4 codes + MMA-layout scales (the K4 rule) for a W4A4 one —
-// so the receiver runs no gather at all.
+// destination, NVFP4 codes (the K4 rule) for a W4A4 one — so the receiver runs
+// no row gather. Every warp store is one contiguous 512-B span (wide peer-memory
+// writes): the NVFP4 codes are regrouped across lanes with shuffles, and the
+// scales go row-major (128 B per row) into a staging window that the receiver
+// turns into the MMA 128x4 layout locally (realb_sf_rows_to_mma); written in that
+// layout directly, a row's scales would be 32 separate 4-B remote writes.
 __global__ void __launch_bounds__(256) p2p_pack_direct_kernel(const __nv_bfloat16* __restrict__ x,
                                                               const int32_t* __restrict__ topk_idx,
                                                               const int32_t* __restrict__ pair_pos,
@@ -306,23 +310,41 @@ __global__ void __launch_bounds__(256) p2p_pack_direct_kernel(const __nv_bfloat1
       uint4* o = reinterpret_cast<uint4*>(ops.a[d] + g * H);
       for (int i = lane; i < H / 8; i += 32) o[i] = __ldg(src + i);
     } else {
-      for (int gi = lane; gi < nkb / 4; gi += 32) {
+      // lane l quantises 64-element group gi = gi0 + l (32 B of codes, one 4-B scale word);
+      // each store instruction then writes 512 contiguous code bytes: lane m stores half
+      // (m & 1) of the group held by lane (m >> 1) (+16 for the second instruction)
+      uint4* crow = reinterpret_cast<uint4*>(ops.codes[d] + g * (H / 2));
+      uint32_t* srow = reinterpret_cast<uint32_t*>(ops.sf[d] + g * (H / 16));
+      for (int gi0 = 0; gi0 < nkb / 4; gi0 += 32) {  // H % 64 == 0: nkb / 4 groups per row
+        const int gi = gi0 + lane;
+        const bool act = gi < nkb / 4;
         uint32_t sfw = 0;
-        uint2 cw[4];
+        uint2 cw[4] = {};
+        if (act) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const uint4 u0 = __ldg(src + (gi * 4 + b) * 2), u1 = __ldg(src + (gi * 4 + b) * 2 + 1);
-          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-          uint32_t sb;
-          bool nf;
-          cw[b] = quant_block16_bf16(w, sb, nf);
-          if (nf && flag) atomicOr(flag, 1);
-          sfw |= sb << (8 * b);
+          for (int b = 0; b < 4; ++b) {
+            const uint4 u0 = __ldg(src + (gi * 4 + b) * 2), u1 = __ldg(src + (gi * 4 + b) * 2 + 1);
+            const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+            uint32_t sb;
+            bool nf;
+            cw[b] = quant_block16_bf16(w, sb, nf);
+            if (nf && flag) atomicOr(flag, 1);
+            sfw |= sb << (8 * b);
+          }
+          srow[gi] = sfw;  // lanes write consecutive words: 128 contiguous bytes
         }
-        uint4* cdst = reinterpret_cast<uint4*>(ops.codes[d] + g * (H / 2) + gi * 32);
-        cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
-        cdst[1] = make_uint4(cw[2].x, cw[2].y, cw[3].x, cw[3].y);
-        *reinterpret_cast<uint32_t*>(ops.sf[d] + sf_mma_offset(g, (int64_t)gi * 4, nkb)) = sfw;
+        const int h = lane & 1;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const int srcl = part * 16 + (lane >> 1);
+          const uint32_t lo0 = __shfl_sync(0xffffffffu, cw[0].x, srcl), lo1 = __shfl_sync(0xffffffffu, cw[0].y, srcl);
+          const uint32_t lo2 = __shfl_sync(0xffffffffu, cw[1].x, srcl), lo3 = __shfl_sync(0xffffffffu, cw[1].y, srcl);
+          const uint32_t hi0 = __shfl_sync(0xffffffffu, cw[2].x, srcl), hi1 = __shfl_sync(0xffffffffu, cw[2].y, srcl);
+          const uint32_t hi2 = __shfl_sync(0xffffffffu, cw[3].x, srcl), hi3 = __shfl_sync(0xffffffffu, cw[3].y, srcl);
+          const int piece = gi0 * 2 + part * 32 + lane;  // 16-B piece index within the row
+          if (piece < nkb / 2)
+            crow[piece] = h ? make_uint4(hi0, hi1, hi2, hi3) : make_uint4(lo0, lo1, lo2, lo3);
+        }
       }
     }
   }
@@ -362,9 +384,42 @@ __global__ void __launch_bounds__(256) p2p_return_map_kernel(const int32_t* __re
   }
 }
 
+// row-major NVFP4 scales [rows][nkb] -> the MMA 128x4 layout, for the valid rows of the
+// groups of one precision class (the layout's group list): one thread per (row, 4-scale word)
+__global__ void __launch_bounds__(256) sf_rows_to_mma_kernel(const uint32_t* __restrict__ sf_rows,
+                                                             const int32_t* __restrict__ layout, int E,
+                                                             int prec, int nkb, uint8_t* __restrict__ sf_mma) {
+  const int G = layout[1 + prec];
+  const int32_t* glist = layout + LayoutView::off_glist(E, prec);
+  const int wpr = nkb / 4;  // words per row
+  for (int gi = blockIdx.y; gi < G; gi += gridDim.y) {
+    const int e = glist[gi];
+    const int64_t r0 = layout[LayoutView::off_row_start(E) + e];
+    const int64_t n = (int64_t)layout[LayoutView::off_row_count(E) + e] * wpr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = r0 + i / wpr;
+      const int w = (int)(i % wpr);
+      *reinterpret_cast<uint32_t*>(sf_mma + sf_mma_offset(r, (int64_t)w * 4, nkb)) = sf_rows[r * wpr + w];
+    }
+  }
+}
+
 }  // namespace realb
 
 using namespace realb;
+
+extern "C" int realb_sf_rows_to_mma(const uint8_t* d_sf_rows, int64_t rows_cap, int K, const int32_t* d_layout,
+                                    int E, int prec, uint8_t* d_sf_mma, void* stream) {
+  if (!d_sf_rows || !d_layout || !d_sf_mma || rows_cap <= 0 || K <= 0 || K % 64 || E < 1 || E > 256 ||
+      (prec != REALB_PREC_W16A16 && prec != REALB_PREC_W4A4)) {
+    set_error("realb_sf_rows_to_mma: bad arguments (K=%d E=%d)", K, E);
+    return REALB_EINVAL;
+  }
+  const dim3 grid((unsigned)(num_sms() * 4 / (E < 8 ? E : 8) + 1), (unsigned)(E < 8 ? E : 8));
+  sf_rows_to_mma_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint32_t*>(d_sf_rows),
+                                                                d_layout, E, prec, K / 16, d_sf_mma);
+  return check_launch("realb_sf_rows_to_mma");
+}
 
 extern "C" int realb_p2p_return_map(const int32_t* d_row_pos, int64_t n_cap, int R, const void* d_plan,
                                     int32_t* d_row_map, void* stream) {
@@ -615,7 +670,7 @@ extern "C" int realb_p2p_pack_direct(const void* d_x, const int32_t* d_topk_idx,
   o.R = R;
   o.El = E / R;
   for (int d = 0; d < R; ++d) {
-    if ((h_peer_a[d] | h_peer_codes[d]) & 15 || h_peer_sf[d] & 3) {
+    if ((h_peer_a[d] | h_peer_codes[d]) & 15 || h_peer_sf[d] & 15) {
       set_error("realb_p2p_pack_direct: peer %d operand addresses misaligned", d);
       return REALB_EINVAL;
     }

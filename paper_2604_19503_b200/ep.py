@@ -246,7 +246,9 @@ class CudaEPOps:
         rc = self.rows_cap
         sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256, "cnt": R * E * 2 * 4,
                  # the GEMM operands themselves, written directly by the senders (device-plan path)
-                 "opa": rc * H * 2, "opc": rc * (H // 2), "ops": rc * (H // 16)}
+                 "opa": rc * H * 2, "opc": rc * (H // 2), "ops": rc * (H // 16),
+                 # NVFP4 scales as sent (row-major); converted to "ops" (MMA layout) locally
+                 "opsr": rc * (H // 16)}
         self._p2p_own, handles = {}, {}
         for name, nbytes in sizes.items():
             ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
@@ -269,7 +271,7 @@ class CudaEPOps:
         self.p2p_epoch = 0
         self.p2p_rank = comm.rank
         # peers' operand bases (kept alive: the ABI reads them through a host pointer)
-        self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "ops")]
+        self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "opsr")]
         self.ret_bases = np.array(self.p2p["ret"], np.uint64)
         # my operand windows (written by the senders) start as in-distribution values,
         # not the allocation's zeros: their padding rows are multiplied too (moe.operand_noise_)
@@ -409,6 +411,9 @@ class CudaEPOps:
         # source's return window (row_map: grouped row -> source, row), over NVLink
         _lib.call("realb_p2p_return_map", self.row_pos.data_ptr(), cap, R, pl, self.row_map.data_ptr(), sp)
         a_bf16, a_codes, a_sf = self.p2p["opa"][r], self.p2p["opc"][r], self.p2p["ops"][r]
+        # the NVFP4 scales arrived row-major: into the MMA layout for the W4A4 groups
+        _lib.call("realb_sf_rows_to_mma", self.p2p["opsr"][r], self.rows_cap, H, self.local_layout.data_ptr(),
+                  El, _lib.PREC_W4A4, a_sf, sp)
         rb = self.ret_bases.ctypes.data
         # both precisions' GEMMs; each runs only the groups the device plan gave it
         lay = self.local_layout.data_ptr()
