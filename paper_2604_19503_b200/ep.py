@@ -705,17 +705,28 @@ def run_bench(args):
             transport_check = f"peer-memory setup failed ({type(e).__name__}): NCCL path"
     layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
     if auto and p2p:
+        # both strategies the bench times, each: NCCL-path layer vs host-sync-free layer
         ref_layer = EPMoELayer(shape, EPComm(staged=staged, p2p=False), ops, fp4_dispatch=fp4_dispatch)
-        y_ref, _, _ = ref_layer.forward(x, mod, "realb")
-        y_ref = y_ref.clone()
-        y_dev, _ = layer.forward_device(x, mod, "realb")
-        torch.cuda.synchronize()
-        ok = torch.tensor([int(torch.equal(y_ref, y_dev) and int(ops.p2p_err.item()) == 0)], device=dev_t)
+        diag = []
+        for strategy in ("realb", "baseline"):
+            y_ref, _, _ = ref_layer.forward(x, mod, strategy)
+            y_ref = y_ref.clone()
+            y_dev, _ = layer.forward_device(x, mod, strategy)
+            torch.cuda.synchronize()
+            d = (y_ref.float() - y_dev.float()).abs()
+            diag.append([float(d.max().nan_to_num(float("inf"))), int((y_ref != y_dev).sum()),
+                         int(ops.p2p_err.item())])
+        ok = torch.tensor([int(all(m == 0 and n == 0 and e == 0 for m, n, e in diag))], device=dev_t)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if int(ok.item()):
-            transport_check = "host-sync-free peer-memory layer == NCCL layer bit for bit on every rank"
+            transport_check = ("host-sync-free peer-memory layer == NCCL layer bit for bit on every rank "
+                               "(realb and baseline)")
         else:
-            transport_check = "peer-memory layer differed from the NCCL layer (or a wait timed out): NCCL path"
+            alld = [None] * world
+            dist.all_gather_object(alld, diag, group=comm.group)
+            transport_check = ("peer-memory layer differed from the NCCL layer (or a wait timed out): NCCL "
+                               f"path; per rank [[max |diff|, differing elements, wait error] x (realb, "
+                               f"baseline)] = {alld}")
             p2p = graph = False
             layer = ref_layer
             comm = layer.comm
