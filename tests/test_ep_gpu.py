@@ -111,7 +111,8 @@ def test_ep2_peer_memory_transport_equals_single_gpu_layer(tmp_path, shape_name,
 
 @pytest.mark.parametrize("shape_name,E,T,strategy,fp4_dispatch", [
     ("kimi", 16, 384, "realb", True), ("kimi", 16, 384, "realb", False), ("qwen", 16, 256, "fp4all", True),
-    ("tiny", 8, 512, "baseline", False), ("kimi_shared", 16, 384, "realb", True)])
+    ("tiny", 8, 512, "baseline", False), ("kimi_shared", 16, 384, "realb", True),
+    ("kimi", 16, 203, "fp4all", True)])  # ragged token count (not a multiple of the 64-token chunk)
 def test_ep2_host_sync_free_layer_and_graph(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
     """The host-sync-free EP layer: C1 through peer memory, plan and window offsets
     derived on the device, both precisions launched and selected by device-side
