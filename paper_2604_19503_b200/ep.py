@@ -354,7 +354,8 @@ class CudaEPOps:
         realb_p2p_plan_offsets), rows dispatched straight into the destinations'
         GEMM operands (NVFP4 towards W4A4 ranks, so the receivers run no gather),
         K3 and both GEMM precisions launched unconditionally and selected by the
-        device-side group lists.
+        device-side group lists, and the return fused into the down GEMMs (their
+        epilogues store every output row into its source's return window).
         -> y; the plan and counts are read back lazily (DevicePlanResult)."""
         from .moe import _STRATEGY_CODE
 
