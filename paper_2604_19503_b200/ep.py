@@ -660,7 +660,7 @@ def run_bench(args):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
-    # REALB_EP_COMM: "nccl" (default: NCCL all-to-alls, one GPU per rank); "p2p" (C2/C3
+    # REALB_EP_COMM: "nccl" (NCCL all-to-alls, one GPU per rank); "p2p" (C2/C3
     # through CUDA-IPC peer-memory windows, NCCL only for the C1 counts); "gloo" /
     # "p2p-gloo": validation modes for a one-GPU box (all ranks share cuda:0, C1
     # (and C2/C3 for "gloo") staged through the host).
