@@ -235,15 +235,18 @@ __global__ void __launch_bounds__(kF4Threads, 1)
               tma_load_2d_2sm(ssfb, &tmSfb, fb, 0, sfb_row + k_sf_row);
               tma_load_2d_2sm(ssfb + 2048, &tmSfb, fb, 0, sfb_row + atoms_per_row_tile * 2 + k_sf_row);
             } else {
-              mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES + S::SFB_BYTES +
-                                                      (load_a_sf ? S::SFA_BYTES : 0));
-              // 1-CTA: the scale runs are plain bulk copies (no 2-SM signalling needed)
+              // 1-CTA: the scale runs are plain bulk copies (no 2-SM signalling needed), one
+              // 512-B atom per 64-wide k-group of this stage: a short last stage (K % 256)
+              // must not read past its row tile's scales (or past the end of the buffer)
+              const uint32_t sf_bytes = (uint32_t)min(4, K / 64 - kb * 4) * 512u;
+              mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES + 2 * sf_bytes +
+                                                      (load_a_sf ? sf_bytes : 0));
               tma_load_2d(sa, &tmA, &full[stage], kb * kF4BKB, a_row);
               tma_load_2d(sb, &tmB, &full[stage], kb * kF4BKB, brow);
-              if (load_a_sf) bulk_load(ssfa, args.a_sf + (int64_t)(sfa_row + k_sf_row) * 256, 2048, &full[stage]);
-              bulk_load(ssfb, args.w_sf + (int64_t)(sfb_row + k_sf_row) * 256, 2048, &full[stage]);
+              if (load_a_sf) bulk_load(ssfa, args.a_sf + (int64_t)(sfa_row + k_sf_row) * 256, sf_bytes, &full[stage]);
+              bulk_load(ssfb, args.w_sf + (int64_t)(sfb_row + k_sf_row) * 256, sf_bytes, &full[stage]);
               bulk_load(ssfb + 2048, args.w_sf + (int64_t)(sfb_row + atoms_per_row_tile * 2 + k_sf_row) * 256,
-                        2048, &full[stage]);
+                        sf_bytes, &full[stage]);
             }
           }
           __syncwarp();
