@@ -129,6 +129,14 @@ def test_ep4_host_sync_free_layer_and_graph(tmp_path, world, shape_name, E, T, s
     _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p=True, device_plan=True, world=world)
 
 
+@pytest.mark.parametrize("strategy", ["fp4all", "baseline"])
+def test_ep1_host_sync_free_layer_own_windows(tmp_path, strategy):
+    """Degenerate EP (one rank, its own windows only): every peer-memory kernel in
+    one process (also the configuration scripts/exp/ep1_selfcheck.py runs under
+    compute-sanitizer); equals the single-GPU layer."""
+    _run_and_compare(tmp_path, "kimi", 16, 333, strategy, True, p2p=True, device_plan=True, world=1)
+
+
 def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False, world=2):
     mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path), p2p,
                             device_plan), nprocs=world)
