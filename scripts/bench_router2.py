@@ -1,3 +1,5 @@
+"""Router fixed-cost probe: tiny (T, H) cases next to a 64-element torch fill_ timed the
+same way (CUDA events around one launch), which gives the launch / event overhead."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
