@@ -179,7 +179,9 @@ __global__ void __launch_bounds__(256, 1)
             l4[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
         } else {
-          for (int i = 0; i < 16 && c0 + i < E; ++i) lrow[c0 + i] = __uint_as_float(v[i]);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)  // unrolled with a guard: v must not be indexed dynamically
+            if (c0 + i < E) lrow[c0 + i] = __uint_as_float(v[i]);
         }
       }
       if (scoring != REALB_SCORE_SIGMOID_RENORM) {  // one rescale per 16 logits
@@ -194,12 +196,18 @@ __global__ void __launch_bounds__(256, 1)
         run_sum = run_sum * __expf(run_max - m) + acc;
         run_max = m;
       }
+      // fully unrolled (no early exit): v stays in registers; the 16 bias values are
+      // loaded up front rather than inside the dependent insertion chain
+      float bv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) bv[i] = (bias && c0 + i < E) ? __ldg(bias + c0 + i) : 0.f;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int e = c0 + i;
-        if (e >= E) break;
-        const float l = __uint_as_float(v[i]);
-        insert(bias ? l + __ldg(bias + e) : l, l, e);
+        if (e < E) {
+          const float l = __uint_as_float(v[i]);
+          insert(l + bv[i], l, e);
+        }
       }
     }
     // hand the high half's state to the primary thread of the same row
