@@ -455,7 +455,7 @@ def test_realb_seq_equals_realb():
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("name", ["kimi", "qwen"])
+@pytest.mark.parametrize("name", ["kimi", "qwen", "ernie_vision"])
 def test_full_size_ep8_batch_properties(name):
     """BASELINE configs[1] / [2] at full size: the Kimi-VL layer (E=64, top-6,
     H=2048, I=1408) and the Qwen3-VL layer (E=128, top-8, I=768) over the EP8
