@@ -122,6 +122,11 @@ def run_ours(args):
     with ClockSampler(0) as clk:
         t_realb = time_steps(torch, step_realb, args.steps, args.warmup, flush)
     gate_up_live_ms = [tm.ms("gate_up_start", "gate_up_end") for tm in timers]
+    # the step's phases, from the same in-graph events (means over the last NS timed steps)
+    spans = {"router_and_plan": ("route_start", "plan_end"), "dispatch": ("dispatch_start", "dispatch_end"),
+             "gate_up": ("gate_up_start", "gate_up_end"), "down": ("down_start", "down_end"),
+             "combine": ("down_end", "combine_end")}
+    step_phases = {k: float(np.mean([tm.ms(a, b) for tm in timers])) for k, (a, b) in spans.items()}
     t_bf16 = time_steps(torch, g_bf16.replay, args.steps, args.warmup, flush)
     # all experts W4A4 (FP4-All, balancers.py:77-86): K3 of all 64 experts' weights on the
     # side stream every step, K4 in dispatch, K6 GEMMs -- the NVFP4 machinery at full size
@@ -168,6 +173,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1],
                 "pipeline": "double-buffered: H2D(i+1) || compute(i) || D2H(i-1)"},
         "roofline": roof,
+        "step_phases_ms": dict(step_phases, what="CUDA events captured in the step graphs (last NS timed steps); "
+                                                 "gate_up..down also spans the W4A4 GEMMs when the plan has any"),
         "gpu_launches": int(launches_per_step * args.steps),
         "cuda_graph": True,
         "clocks": clk.summary(),

@@ -444,10 +444,13 @@ class MoELayer:
         main = torch.cuda.current_stream()
         sp = _lib.stream_ptr(main)
         shared = self.shared is not None and T > 0
+        mark = timer.mark if timer is not None else (lambda *a, **kw: None)
         if shared:  # overlapped with the whole routed path, joined before the combine
             self.shared.start(x)
+        mark("route_start", main)
         self.route(x, modality)
         self.align_plan(T, strategy, params)
+        mark("plan_end", main)
         # NVFP4 launches are needed unless the plan provably stays all-W16A16: the
         # baseline strategies, or realb on one rank with C >= 1 (a rank's load is
         # then exactly the mean, never > C x mean; balancers.py:103-104). This is a
@@ -455,7 +458,6 @@ class MoELayer:
         code = _STRATEGY_CODE[strategy]
         mixed = code == 1 or (code == 2 and not (self.cluster.num_ranks == 1
                                                  and params.capacity_factor >= 1.0))
-        mark = timer.mark if timer is not None else (lambda *a, **kw: None)
         # realb-seq: the reference's sequential ablation (engine.py:162-167): K3 on the
         # main stream, so the transform is NOT hidden behind dispatch
         k3_stream = main if strategy == "realb-seq" else self.side
@@ -502,6 +504,7 @@ class MoELayer:
             _lib.call("realb_grouped_gemm_nvfp4", ws["a_codes"].data_ptr(), ws["a_sf"].data_ptr(),
                       ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, E,
                       lay, _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
+        mark("down_start", main)
         _lib.call("realb_grouped_gemm_bf16", self.h_bf16.data_ptr(), self.w.w_d.data_ptr(),
                   self.rows_cap, H, I, E, lay, _lib.PREC_W16A16, _lib.EPI_STORE,
                   self.rows_out.data_ptr(), 0, sp)
@@ -509,10 +512,12 @@ class MoELayer:
             _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
                       ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, E, lay,
                       _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+        mark("down_end", main)
         y = self.y_buf[:T] if out is None else out
         addend = self.shared.join() if shared else None
         _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
                   self.topk_w.data_ptr(), T, H, k, addend, y.data_ptr(), sp)
+        mark("combine_end", main)
         if torch.cuda.is_current_stream_capturing():
             return LayerResult(y, self, self.plan_host, self.expert_vt_host, None, self.placement,
                                self.cluster)
