@@ -249,25 +249,46 @@ class CudaEPOps:
                  "opa": rc * H * 2, "opc": rc * (H // 2), "ops": rc * (H // 16),
                  # NVFP4 scales as sent (row-major); converted to "ops" (MMA layout) locally
                  "opsr": rc * (H // 16)}
-        self._p2p_own, handles = {}, {}
-        for name, nbytes in sizes.items():
-            ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
-            _lib.call("realb_ipc_alloc", nbytes, Cty.byref(ptr), h)
-            self._p2p_own[name] = ptr.value
-            handles[name] = bytes(h)
+        # Every rank runs the same collectives whatever fails locally (allocation, mapping),
+        # and failures are agreed on, so all ranks raise together and fall back together
+        # instead of one rank leaving the others blocked in a collective.
+        self._p2p_own, handles, err = {}, {}, None
+        try:
+            for name, nbytes in sizes.items():
+                ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
+                _lib.call("realb_ipc_alloc", nbytes, Cty.byref(ptr), h)
+                self._p2p_own[name] = ptr.value
+                handles[name] = bytes(h)
+        except Exception as e:  # noqa: BLE001 - reported to every rank below
+            err, handles = f"rank {comm.rank}: {type(e).__name__}: {e}", None
         allh = [None] * R
         dist.all_gather_object(allh, handles, group=comm.group)
+        if any(h is None for h in allh):
+            self._free_own_windows()
+            raise RuntimeError(f"peer-memory windows: allocation failed on some rank ({err or 'peer'})")
         self.p2p = {name: [0] * R for name in sizes}
         self._p2p_opened = []
-        for r in range(R):
-            for name in sizes:
-                if r == comm.rank:
-                    self.p2p[name][r] = self._p2p_own[name]
-                else:
-                    ptr = Cty.c_void_p()
-                    _lib.call("realb_ipc_open", allh[r][name], Cty.byref(ptr))
-                    self.p2p[name][r] = ptr.value
-                    self._p2p_opened.append(ptr.value)
+        try:
+            for r in range(R):
+                for name in sizes:
+                    if r == comm.rank:
+                        self.p2p[name][r] = self._p2p_own[name]
+                    else:
+                        ptr = Cty.c_void_p()
+                        _lib.call("realb_ipc_open", allh[r][name], Cty.byref(ptr))
+                        self.p2p[name][r] = ptr.value
+                        self._p2p_opened.append(ptr.value)
+            err = None
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {comm.rank}: {type(e).__name__}: {e}"
+        allerr = [None] * R
+        dist.all_gather_object(allerr, err, group=comm.group)
+        if any(allerr):
+            for ptr in self._p2p_opened:
+                _lib.call("realb_ipc_close", ptr)
+            self._p2p_opened = []
+            self._free_own_windows()
+            raise RuntimeError(f"peer-memory windows: mapping failed: {[e for e in allerr if e]}")
         self.p2p_epoch = 0
         self.p2p_rank = comm.rank
         # peers' operand bases (kept alive: the ABI reads them through a host pointer)
@@ -455,6 +476,11 @@ class CudaEPOps:
         _lib.call("realb_p2p_signal", ctrs.ctypes.data, R, sp)
         _lib.call("realb_p2p_wait_next", self.d_expected.data_ptr() + 4 * slot, R,
                   self._p2p_own["ctr"] + ctr_off, self.p2p_err.data_ptr(), sp)
+
+    def _free_own_windows(self):
+        for ptr in getattr(self, "_p2p_own", {}).values():
+            _lib.call("realb_ipc_free", ptr)
+        self._p2p_own = {}
 
     def close_p2p(self):
         torch.cuda.synchronize()
@@ -712,11 +738,14 @@ def run_bench(args):
         for strategy in ("realb", "baseline"):
             y_ref, _, _ = ref_layer.forward(x, mod, strategy)
             y_ref = y_ref.clone()
-            y_dev, _ = layer.forward_device(x, mod, strategy)
-            torch.cuda.synchronize()
-            d = (y_ref.float() - y_dev.float()).abs()
-            diag.append([float(d.max().nan_to_num(float("inf"))), int((y_ref != y_dev).sum()),
-                         int(ops.p2p_err.item())])
+            try:  # a failure here must still reach the agreement below (no rank left waiting)
+                y_dev, _ = layer.forward_device(x, mod, strategy)
+                torch.cuda.synchronize()
+                d = (y_ref.float() - y_dev.float()).abs()
+                diag.append([float(d.max().nan_to_num(float("inf"))), int((y_ref != y_dev).sum()),
+                             int(ops.p2p_err.item())])
+            except Exception as e:  # noqa: BLE001
+                diag.append([float("inf"), -1, f"{type(e).__name__}: {str(e)[:120]}"])
         ok = torch.tensor([int(all(m == 0 and n == 0 and e == 0 for m, n, e in diag))], device=dev_t)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if int(ok.item()):
