@@ -254,6 +254,8 @@ class CudaEPOps:
         # instead of one rank leaving the others blocked in a collective.
         self._p2p_own, handles, err = {}, {}, None
         try:
+            if os.environ.get("REALB_TEST_P2P_FAIL_RANK") == str(comm.rank):  # fault injection (tests)
+                raise RuntimeError("injected peer-memory allocation failure")
             for name, nbytes in sizes.items():
                 ptr, h = Cty.c_void_p(), (Cty.c_uint8 * 64)()
                 _lib.call("realb_ipc_alloc", nbytes, Cty.byref(ptr), h)

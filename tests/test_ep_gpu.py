@@ -157,3 +157,35 @@ def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, de
     y = np.concatenate([a["y"] for a in r])
     assert list(r[0]["acc"]) == sorted(res.plan.accelerated_ranks)
     np.testing.assert_array_equal(y, ref)
+
+
+def _setup_fail_worker(rank, world, port, outdir):
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "tests")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), REALB_TEST_P2P_FAIL_RANK="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_19503_b200.ep import CudaEPOps, EPComm, split_weights
+
+    shape, x, mod, router, gu, dn, sh = _setup("kimi", 16, 128, world, rank)
+    ops = CudaEPOps(shape, router.contiguous(), None, split_weights(shape, router, gu, dn, rank, world), world, 128)
+    raised = ""
+    try:
+        ops.setup_p2p(EPComm(staged=True, p2p=True))
+    except RuntimeError as e:
+        raised = str(e)
+    dist.barrier()  # both ranks got here: nobody was left inside a collective
+    open(os.path.join(outdir, f"r{rank}.txt"), "w").write(raised)
+    dist.destroy_process_group()
+
+
+def test_p2p_setup_failure_is_agreed_by_all_ranks(tmp_path):
+    """A peer-memory setup failure on ONE rank (fault injection) makes every rank
+    raise, so the bench's auto transport falls back to the collective path on all
+    ranks together instead of leaving the healthy ranks blocked in a collective."""
+    mp.spawn(_setup_fail_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2)
+    msgs = [(tmp_path / f"r{r}.txt").read_text() for r in range(2)]
+    assert all("allocation failed" in m for m in msgs), msgs
