@@ -22,8 +22,6 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2604_19503_b200.clocks import ClockSampler, measured_peaks  # noqa: E402
-
 METRIC = "MoE-layer prefill tokens/s and speedup vs all-BF16 EP at 1/2/4/8 B200"
 
 
@@ -36,7 +34,8 @@ def parse():
     p.add_argument("--config", default="kimi", choices=["tiny", "kimi", "kimi_shared", "qwen", "ernie_vision"])
     p.add_argument("--tokens", type=int, default=8192, help="local tokens per GPU")
     p.add_argument("--vision-frac", type=float, default=0.7)
-    p.add_argument("--cpu-sample-tokens", type=int, default=256)
+    p.add_argument("--cpu-sample-tokens", type=int, default=1024,
+                   help="tokens per step of the cpu_baseline leg (the --impl reference arm uses --tokens)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-virtual-ep", action="store_true")
     p.add_argument("--no-l2-flush", action="store_true",
@@ -86,6 +85,7 @@ def run_ours(args):
     import torch
 
     from paper_2604_19503_b200 import _lib
+    from paper_2604_19503_b200.clocks import ClockSampler
     from paper_2604_19503_b200.moe import MoELayer
     from paper_2604_19503_b200.policy import RealbParams
 
@@ -155,6 +155,23 @@ def run_ours(args):
     ms_e2e, e2e_bytes = run_e2e(torch, layer, x, mod, params, args)
     # --- roofline of the dominant kernel (K5 gate_up grouped GEMM), events on its stream
     roof = roofline_gate_up(torch, layer, x, mod, shape, args, gate_up_live_ms, ms)
+    # --- SURVEY §8(d) layer roofline: t_roof = max_r F_r / Peak(plan_r), F_r = pairs_r * 6HI
+    # (one rank here, all experts W16A16 under the inactive R = 1 plan)
+    from paper_2604_19503_b200.clocks import measured_peaks
+
+    peaks, psrc = measured_peaks()
+    F = float(T * shape.top_k) * 6.0 * shape.hidden * shape.intermediate
+    t_roof = F / (float(peaks.get("bf16_tflops", 1641.1)) * 1e12) * 1e3
+    roof["layer"] = {"t_roof_ms": t_roof, "t_meas_ms": ms, "frac": t_roof / ms, "flops": F,
+                     "peak": f"{psrc} bf16_tflops (burst) {peaks.get('bf16_tflops')}",
+                     "what": "max over ranks of (pairs_r x 6HI) / peak of rank r's precision (SURVEY.md §8(d)); "
+                             "the step also runs router, dispatch and combine, which this bound leaves out"}
+    # --- sustained: the same step back to back for >= 1000 steps (the power cap settles;
+    # the headline above is the short-region figure the driver's K steps measure)
+    n_sus = max(1000, args.steps)
+    with ClockSampler(0) as clk_sus:
+        t_sus = time_steps(torch, step_realb, n_sus, 10, flush)
+    ms_sus = float(np.mean(t_sus))
 
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
@@ -182,6 +199,10 @@ def run_ours(args):
         "gpu_launches": int(launches_per_step * args.steps),
         "cuda_graph": True,
         "clocks": clk.summary(),
+        "sustained": {"steps": n_sus, "ms_per_step": ms_sus, "tokens_per_s": T / (ms_sus / 1e3),
+                      "clocks": clk_sus.summary(),
+                      "what": "the headline step back to back (L2 flushed between steps as above) after the "
+                              "timed region; the power cap settles over this many steps"},
     }
     if not args.no_virtual_ep:
         try:
@@ -190,6 +211,14 @@ def run_ours(args):
             out["virtual_ep8"] = virtual_ep_report(args, torch)
         except Exception as e:  # reported, never silently dropped
             out["virtual_ep8"] = {"error": repr(e)[:300]}
+    # the accuracy proxy: at R = 1 the plan is inactive, so the headline
+    # layer is all-BF16 (exposure 0); the EP8 plan's figures come from virtual_ep8
+    v8 = out.get("virtual_ep8", {})
+    out["accuracy"] = {"headline_plan_w4a4_ranks": [], "headline_text_exposure": 0.0,
+                       "virtual_ep8_text_exposure": v8.get("text_exposure"),
+                       "virtual_ep8": v8.get("accuracy"),
+                       "what": "text exposure = text (token, expert) pairs on W4A4 ranks / all text pairs "
+                               "(metrics.py:72-90); W4A4 weight error and layer-output deltas vs all-BF16"}
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, sample=args.cpu_sample_tokens)
     print(json.dumps(out), flush=True)
@@ -272,11 +301,13 @@ def roofline_gate_up(torch, layer, x, mod, shape, args, live_ms, step_ms):
     """achieved = algorithmic flops of the K5 gate_up launch (2 * pairs * 2I * H)
     / its duration measured live inside the timed region (CUDA events recorded by
     the step graphs on the launching stream, the last NS timed steps), against the
-    SUSTAINED bf16 peak (a kernel inside a long step). Also reported: the same
+    BURST bf16 peak (the timed region is short; the sustained-peak fraction is
+    reported beside it). Also reported: the same
     launch timed alone after an idle gap (burst) next to one dense cuBLAS GEMM of
     the same flops timed the same way."""
     import time
     from paper_2604_19503_b200 import _lib
+    from paper_2604_19503_b200.clocks import measured_peaks
 
     peaks, src = measured_peaks()
     T = x.shape[0]
@@ -307,7 +338,7 @@ def roofline_gate_up(torch, layer, x, mod, shape, args, live_ms, step_ms):
     t = float(sum(live_ms) / len(live_ms)) / 1e3
     flops = 2.0 * pairs * (2 * I) * H
     achieved = flops / t / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", 1368.2))
+    peak_sus = float(peaks.get("bf16_tflops_sustained", 1368.2))
     peak_burst = float(peaks.get("bf16_tflops", 1641.1))
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
@@ -321,8 +352,11 @@ def roofline_gate_up(torch, layer, x, mod, shape, args, live_ms, step_ms):
                        "form left in A)",
              "copy": "realb_grouped_gemm_bf16 (K5 gate_up, SwiGLU epilogue)"}[layer.dispatch_mode]
     return {"kernel": kname, "bound": "tensor",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside the step)",
+            "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst,
+            "traffic": traffic,
+            "peak_source": f"{src} bf16_tflops (burst: the timed region is {args.steps} steps of ~1 ms, "
+                           "not a multi-second power-capped loop)",
+            "frac_of_sustained_peak": achieved / peak_sus,
             "algorithmic_flops_per_launch": flops, "launch_ms": t * 1e3,
             "launch_timing": f"CUDA events captured around the launch in the step graphs, last {len(live_ms)} "
                              "timed steps (live, inside the timed region)",
@@ -337,93 +371,93 @@ def roofline_gate_up(torch, layer, x, mod, shape, args, live_ms, step_ms):
 
 
 # ----------------------------------------------------------------------------- CPU arms
-class CpuOracleArm:
-    """The CPU oracle port of the whole path (oracle/moe_ref.py + the C quantiser),
-    on a bounded token sample of the same workload. Weights are built once."""
+def cpu_baseline(args, sample: int, world: int = 1):
+    """The CPU oracle port of the whole layer (oracle/cpu_arm.py: no product code,
+    no librealb_b200.so) on a bounded token sample, plus BASELINE.md §3's pieces:
+    the reference quantiser rule and the reference policy, on the box's host."""
+    from oracle.cpu_arm import CpuLayerArm
 
-    def __init__(self, args, sample: int):
-        import numpy as np
-        import torch
-
-        from paper_2604_19503_b200.moe import SHAPES
-        from paper_2604_19503_b200.policy import ClusterConfig
-        from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_experts
-
-        self.threads = os.cpu_count() or 1
-        torch.set_num_threads(self.threads)
-        self.shape = shape = SHAPES[args.config]
-        self.sample = sample
-        spec = WorkloadSpec(tokens=sample, vision_frac=args.vision_frac,
-                            num_ranks=8 if shape.num_experts % 8 == 0 else 1)
-        x, mod, router, _ = make_batch(shape, spec, device="cpu")
-        gu, dn = make_experts(shape, device="cpu")
-        self.x, self.mod, self.router = x.float().numpy(), mod.numpy(), router.float().numpy()
-        self.gu, self.dn = gu.float().numpy(), dn.float().numpy()
-        self.wbits = gu[0].contiguous().view(torch.int16).numpy().view(np.uint16)
-        R = max(1, int(os.environ.get("WORLD_SIZE", "1")))
-        self.R = R
-        self.cluster = ClusterConfig(R, 1, shape.num_experts // R, 1, shape.modality_isolated)
-
-    def step(self) -> float:
-        from oracle import moe_ref
-        from paper_2604_19503_b200.policy import RealbParams, place_experts_static, plan_for, \
-            rank_loads_from_counts
-
-        s = self.shape
-        t0 = time.perf_counter()
-        logits, idx, _ = moe_ref.route(self.x, self.router, s.top_k, s.scoring, routed_scaling=s.routed_scaling)
-        vt = moe_ref.expert_counts(idx, self.mod, s.num_experts)
-        plan = plan_for("realb", rank_loads_from_counts(vt, self.cluster), self.cluster, RealbParams())
-        prec = plan.expert_precision(place_experts_static(self.cluster))
-        moe_ref.moe_layer(self.x, self.mod, self.router, self.gu, self.dn, s.top_k, s.scoring,
-                          expert_prec=prec, routed_scaling=s.routed_scaling, logits=logits)
-        return time.perf_counter() - t0
-
-    def quantiser_mbps(self) -> float:
-        import oracle
-
-        t = time.perf_counter()
-        oracle.quantize_bf16(self.wbits)
-        return self.wbits.nbytes / (time.perf_counter() - t) / 1e6
-
-    def describe(self, value: float) -> dict:
-        return {"value": value, "unit": "tokens/s", "cores": self.threads, "kind": "port",
-                "sample": f"{self.sample} tokens of the {self.shape.name} workload through the full CPU oracle "
-                          f"layer (numpy fp32, {self.threads} BLAS threads), plan over R={self.R}"}
-
-
-def cpu_baseline(args, sample: int):
-    arm = CpuOracleArm(args, sample)
+    arm = CpuLayerArm(args.config, sample, args.vision_frac, num_ranks=world)
     dt = min(arm.step() for _ in range(2))
     d = arm.describe(sample / dt)
-    d["quantiser_MBps_bf16_in"] = arm.quantiser_mbps()
-    d["quantiser_cores"] = 1
+    d["quantiser"] = arm.quantiser_rates()
+    d["policy"] = arm.policy_us_per_layer()
     return d
 
 
 def run_reference(args):
     """--impl reference: the reference's CPU implementation of the path. The
     reference (moesim) is an analytic simulator with no executable MoE layer, so
-    this arm runs the CPU oracle port of it (oracle/), on rank 0 only."""
+    this arm runs the oracle's CPU restatement of it (oracle/cpu_arm.py: numpy
+    router + the reference policy + fp32 expert GEMMs on every host thread), on
+    rank 0 only, over the SAME per-GPU batch as our arm (--tokens), each step one
+    full layer."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import numpy as np
 
-    arm = CpuOracleArm(args, args.cpu_sample_tokens)
-    for _ in range(args.warmup):
-        arm.step()
-    secs = [arm.step() for _ in range(args.steps)]
-    v = args.cpu_sample_tokens / float(np.mean(secs))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    from oracle.cpu_arm import CpuLayerArm
+
+    world = int(os.environ.get("WORLD_SIZE", str(max(1, args.gpus))))
+    T = args.tokens
+    arm = CpuLayerArm(args.config, T, args.vision_frac, num_ranks=world)
+    # bounded: the CPU layer takes seconds per step; all K steps run unless they
+    # would take more than ~150 s, then as many as fit (at least 3; in the line)
+    warm = max(1, min(args.warmup, 2))
+    t_first = min(arm.step() for _ in range(warm))
+    steps = max(3, min(args.steps, int(150.0 / max(t_first, 1e-3))))
+    secs = [arm.step() for _ in range(steps)]
+    ms = float(np.mean(secs)) * 1e3
+    v = T / (ms / 1e3)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": f"{arm.shape.name} MoE layer prefill (CPU oracle port, bounded sample)",
-                      "tokens_per_step": args.cpu_sample_tokens},
+           "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32 (bf16 values)", "data": "synthetic",
+           "config": {"workload": workload_name(args, arm.E, arm.k, arm.H, arm.I),
+                      "strategy": "realb", "ep_ranks": world, "tokens_per_gpu": T,
+                      "steps_requested": args.steps, "warmup_requested": args.warmup,
+                      "what": "oracle/cpu_arm.py: the CPU restatement of the path (no product code)"},
            "cpu_baseline": arm.describe(v),
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def workload_name(args, E, k, H, I):
+    names = {"tiny": "tiny-mmoe", "kimi": "kimi-vl-a3b", "kimi_shared": "kimi-vl-a3b+shared",
+             "qwen": "qwen3-vl-30b-a3b", "ernie_vision": "ernie-4.5-vl-a3b-vision"}
+    return (f"{names[args.config]} MoE layer prefill, {args.tokens} tokens/GPU, {args.vision_frac:.0%} vision, "
+            f"E={E} top-{k} H={H} I={I}")
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-launch this script
+    under torch.distributed.run with N local ranks (127.0.0.1 rendezvous), so the
+    driver's plain command times N GPUs. With fewer visible GPUs than N the ranks
+    share cuda:0 through host-staged collectives (REALB_EP_COMM=auto-gloo): a
+    validation run, labelled as such in the line."""
+    import socket
+    import subprocess
+
+    env = dict(os.environ)
+    try:
+        import torch
+
+        ngpu = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        ngpu = 0
+    if ngpu < args.gpus and "REALB_EP_COMM" not in env:
+        env["REALB_EP_COMM"] = "auto-gloo"
+    # NCCL communicator set-up lines (NVLink / NVLS) on stderr, stdout stays one JSON line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -431,6 +465,8 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     run_ours(args)
 
 

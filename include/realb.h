@@ -100,6 +100,29 @@ REALB_API int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows_
                                            int32_t* d_nonfinite_flag, int max_ctas,
                                            void* stream);
 
+/* Q5 — quantize_tensor + ErrorSummary (fp4.py:130-170) on the device.
+ *   d_x        : n flat values (dtype REALB_DT_BF16 / F32 / F64), n > 0; the
+ *                last block is zero-padded
+ *   d_records  : ceil(n/16) x 9 bytes, each the FP4REF01 block record of
+ *                pack_block (fp4.py:246-252): 8 code bytes (element 2i in the low
+ *                nibble) + the E4M3 scale byte; i.e. the body of write_blocks
+ *   d_block_max_rel : fp64 [ceil(n/16)] max over unpadded x != 0 of |x - d|/|x|
+ *                (bit-exact with the reference), or NULL
+ *   d_sums     : fp64 [2], ACCUMULATED (zero it first): sum (x - d)^2 and sum x^2
+ *                over the unpadded elements -> rmse = sqrt(s0 / n),
+ *                relative_rmse = sqrt(s0 / s1) (s1 > 0), or NULL
+ *   d_nonfinite_flag : set on Inf/NaN input (QuantizationDomainError), or NULL
+ * The block rule runs in fp64 (the reference's arithmetic) for every dtype. */
+REALB_API int realb_quantize_tensor_nvfp4(const void* d_x, int dtype, int64_t n, uint8_t* d_records,
+                                          double* d_block_max_rel, double* d_sums,
+                                          int32_t* d_nonfinite_flag, void* stream);
+
+/* Q4/Q6 decode — dequantize_blocks (fp4.py:230-243): nblocks blocks of packed
+ * codes (8 bytes, element 2i in the low nibble) and flat E4M3 scale bytes ->
+ * 16 values each, code magnitude x scale (exact), dtype_out REALB_DT_F32 / F64. */
+REALB_API int realb_dequantize_blocks(const uint8_t* d_codes, const uint8_t* d_sf, int64_t nblocks,
+                                      int dtype_out, void* d_out, void* stream);
+
 /* ------------------------------------------------------------------------ *
  * K1 + K2 — router / top-k / modality statistics (new: the reference
  * synthesises routing, tracegen.py:141-185; the counts it produces feed
@@ -374,7 +397,10 @@ REALB_API int realb_grouped_gemm_bf16_scatter(const void* d_a, const void* d_w, 
  * groups of d_layout. Weight rows are indexed by global expert id
  * (W row g*N + n), so only the W4A4 experts' rows need to be quantised.
  * With REALB_EPI_SWIGLU and d_out_codes/d_out_sf non-NULL, the SwiGLU output
- * is written directly as NVFP4 codes + MMA-layout scales for the next GEMM. */
+ * is written directly as NVFP4 codes + MMA-layout scales for the next GEMM;
+ * d_out may then be NULL or a bf16 [rows_cap][N/2] buffer that receives the
+ * bf16 SwiGLU values the re-quantisation consumed (parity hook: the codes and
+ * scales must equal the reference block rule applied to exactly these values). */
 REALB_API int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t* d_a_sf,
                              const uint8_t* d_w_codes, const uint8_t* d_w_sf,
                              int64_t rows_cap, int N, int K, int E,

@@ -11,6 +11,11 @@ Contents
   moe_ref.py     numpy restatement of the MoE-layer path (router D1 contract,
                  stats, reference policy, reference block quantiser, expert
                  MLPs in fp32, combine)
+  policy_ref.py  aggregate_rank_loads + plan_realb (core.py:106-130,
+                 balancers.py:89-122) in plain Python
+  fp4_numpy.py   numpy float64 restatement of quantize_blocks (fp4.py:173-227),
+                 the "reference quantiser" CPU baseline bench.py times
+  cpu_arm.py     bench.py's CPU arms (cpu_baseline, --impl reference)
 
 Pinning: tests/test_oracle.py checks the C oracle against fixtures generated
 by running the reference itself (tests/golden/make_golden.py) and against the
@@ -96,3 +101,29 @@ def fake_quant(x: np.ndarray) -> np.ndarray:
     shp = x.shape
     c, s = quantize_blocks(np.asarray(x, np.float64).reshape(-1, 16))
     return dequantize_blocks(c, s).reshape(shp)
+
+
+def quantize_tensor(values):
+    """quantize_tensor + ErrorSummary (fp4.py:137-170): flat values, the tail block
+    zero-padded -> (9-byte block records uint8 [nb, 9], rmse, relative_rmse,
+    per-block max relative error [nb]). The sums are sequential fp64 running sums
+    in element order (np.cumsum), i.e. the reference's own accumulation order."""
+    v = np.asarray(values, dtype=np.float64).reshape(-1)
+    n = v.size
+    if n == 0:
+        raise ValueError("values must be non-empty")
+    nb = (n + 15) // 16
+    pad = np.zeros(nb * 16)
+    pad[:n] = v
+    c, s = quantize_blocks(pad.reshape(nb, 16))
+    d = dequantize_blocks(c, s).reshape(-1)[:n]
+    err = v - d
+    sq_err = float(np.cumsum(err * err)[-1])
+    sq_val = float(np.cumsum(v * v)[-1])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rel = np.where(v != 0.0, np.abs(err) / np.abs(v), 0.0)
+    relp = np.zeros(nb * 16)
+    relp[:n] = rel
+    max_rel = relp.reshape(nb, 16).max(axis=1)
+    rec = np.concatenate([(c[:, 0::2] | (c[:, 1::2] << 4)).astype(np.uint8), s[:, None]], axis=1)
+    return rec, float(np.sqrt(sq_err / n)), (float(np.sqrt(sq_err / sq_val)) if sq_val > 0 else 0.0), max_rel

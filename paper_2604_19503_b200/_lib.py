@@ -49,6 +49,8 @@ SIGNATURES: dict[str, tuple] = {
     "realb_layout_words": (_i64, [_i32, _i32]),
     "realb_moe_align_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _f64, _f64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_quantize_experts_nvfp4": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "realb_quantize_tensor_nvfp4": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "realb_dequantize_blocks": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "realb_moe_align": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
     "realb_gather_rows": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "realb_ep_regroup": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
@@ -104,7 +106,8 @@ LAUNCHES_KERNEL = {
     "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_bf16_gather": 1, "realb_grouped_gemm_nvfp4": 1,
     "realb_grouped_gemm_bf16_copyin": 1, "realb_grouped_gemm_bf16_scatter": 1, "realb_grouped_gemm_nvfp4_scatter": 1, "realb_p2p_return_map": 1, "realb_sf_rows_to_mma": 1,
-    "realb_dispatch_index": 1,  # + 1 when NVFP4 rows are quantised (call() adds it) "realb_combine": 1,
+    "realb_dispatch_index": 1,  # + 1 when NVFP4 rows are quantised (call() adds it)
+    "realb_combine": 1, "realb_quantize_tensor_nvfp4": 1, "realb_dequantize_blocks": 1,
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
     "realb_p2p_pack": 2, "realb_p2p_return": 1, "realb_p2p_signal": 1, "realb_p2p_wait": 1,

@@ -412,6 +412,14 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           uint32_t sb;
           cw[b] = quant_block16_bf16vals(h, sb);
           sfw |= sb << (8 * b);
+          if (args.out) {  // parity hook: the bf16 SwiGLU values the re-quantisation consumed
+            uint32_t hp[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) hp[i] = pack_bf16x2(h[2 * i], h[2 * i + 1]);
+            uint4* hd = reinterpret_cast<uint4*>(args.out + r * I + ocol + b * 16);
+            hd[0] = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+            hd[1] = make_uint4(hp[4], hp[5], hp[6], hp[7]);
+          }
         }
         uint4* cdst = reinterpret_cast<uint4*>(args.out_codes + r * (I / 2) + ocol / 2);
         cdst[0] = make_uint4(cw[0].x, cw[0].y, cw[1].x, cw[1].y);
@@ -574,10 +582,11 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
       set_error("realb_grouped_gemm_nvfp4: SWIGLU needs d_out_codes/d_out_sf and (N/2) %% 64 == 0");
       return REALB_EINVAL;
     }
+    // d_out (optional, SWIGLU): also store the bf16 SwiGLU values the re-quantisation consumed
     return pair ? launch_fp4<REALB_EPI_SWIGLU, 2>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
-                                                  d_layout, nullptr, d_out_codes, d_out_sf, max_ctas, st)
+                                                  d_layout, d_out, d_out_codes, d_out_sf, max_ctas, st)
                 : launch_fp4<REALB_EPI_SWIGLU, 1>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
-                                                  d_layout, nullptr, d_out_codes, d_out_sf, max_ctas, st);
+                                                  d_layout, d_out, d_out_codes, d_out_sf, max_ctas, st);
   }
   set_error("realb_grouped_gemm_nvfp4: unknown epilogue %d", epilogue);
   return REALB_EINVAL;

@@ -40,6 +40,20 @@ from .policy import STRATEGIES, ClusterConfig, Precision, PrecisionPlan, RealbPa
     rank_loads_from_counts
 
 
+# Counter words (byte offsets) in every rank's 256-B counter window. The two
+# transports keep separate words: the host-plan path tracks its expected value on
+# the host (p2p_epoch * R), the host-sync-free path in device memory (d_expected),
+# so calling forward() and forward_device() on the same ops cannot let one path's
+# wait pass on the other path's signals.
+_DEV_CTR_DISPATCH, _DEV_CTR_RETURN, _DEV_CTR_COUNTS = 0, 4, 8
+_HOST_CTR_DISPATCH, _HOST_CTR_RETURN = 16, 20
+
+
+class PeerWaitTimeout(RuntimeError):
+    """A peer-memory wait gave up after 10 s (a peer never signalled): the
+    layer's output is invalid."""
+
+
 # ----------------------------------------------------------------------------- comm
 class EPComm:
     """Collectives of the EP layer. ``staged`` copies device tensors through the
@@ -345,7 +359,7 @@ class CudaEPOps:
                   self.send_layout.data_ptr(), (T + 63) // 64, R, fmt.ctypes.data, row0.ctypes.data,
                   dst.ctypes.data, self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
         self.p2p_epoch += 1
-        self._p2p_signal_wait(0)
+        self._p2p_signal_wait(_HOST_CTR_DISPATCH)
         return self.p2p["recv"][rank], self.send_pos[:T]
 
     def p2p_return(self, cnt: np.ndarray, pairs: np.ndarray, rank: int):
@@ -358,7 +372,7 @@ class CudaEPOps:
         dst = np.array([self.p2p["ret"][s_] + int(send_row0[s_, rank]) * 2 * H for s_ in range(R)], np.uint64)
         _lib.call("realb_p2p_return", self.rows_out.data_ptr(), self.row_pos.data_ptr(), n, H, R,
                   recv_prefix.ctypes.data, dst.ctypes.data, _lib.stream_ptr())
-        self._p2p_signal_wait(4)
+        self._p2p_signal_wait(_HOST_CTR_RETURN)
         return self.p2p["ret"][rank]
 
     def _p2p_signal_wait(self, ctr_off: int):
@@ -393,7 +407,7 @@ class CudaEPOps:
         # C1: my [E][2] counts into every rank's counts window, slot r
         cnt_bases = np.array(self.p2p["cnt"], np.uint64)
         _lib.call("realb_p2p_publish", self.vt_local.data_ptr(), E * 2, R, cnt_bases.ctypes.data, r * E * 2, sp)
-        self._signal_wait_dev(8, 2)
+        self._signal_wait_dev(_DEV_CTR_COUNTS, 2)
         # P1 on the device over the global counts (R "chunks" of [E][2]), then the window plan
         _lib.call("realb_moe_align_plan", self.p2p["cnt"][r], R, E, R, _STRATEGY_CODE[strategy],
                   float(params.capacity_factor), float(params.modality_threshold),
@@ -423,7 +437,7 @@ class CudaEPOps:
                   self.op_bases[0].ctypes.data, self.op_bases[1].ctypes.data, self.op_bases[2].ctypes.data,
                   self.d_plan.data_ptr(),
                   self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
-        self._signal_wait_dev(0, 0)
+        self._signal_wait_dev(_DEV_CTR_DISPATCH, 0)
         mark("dispatch")
         # receive side: only the grouped layout and the row map for the return (no row copies)
         cap = self.recv_cap
@@ -453,7 +467,7 @@ class CudaEPOps:
                   ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
                   self.row_map.data_ptr(), R, rb, 0, sp)
         mark("compute")
-        self._signal_wait_dev(4, 1)
+        self._signal_wait_dev(_DEV_CTR_RETURN, 1)
         y = torch.empty(T, H, dtype=torch.bfloat16, device=self.dev)
         addend = self.shared.join() if self.shared is not None and T > 0 else None
         _lib.call("realb_combine", self.p2p["ret"][r], self.send_pos.data_ptr(), self.topk_w.data_ptr(),
@@ -561,6 +575,11 @@ class EPMoELayer:
             raise ValueError("the device-plan EP layer needs the peer-memory transport")
         if strategy not in STRATEGIES:
             raise ValueError(f"unknown strategy {strategy!r}")
+        if not self.fp4_dispatch:
+            # direct dispatch writes each row into its owner's GEMM operand in the
+            # owner's precision: a W4A4 owner always receives NVFP4 rows
+            raise ValueError("the device-plan EP layer always sends NVFP4 rows to W4A4 ranks "
+                             "(fp4_dispatch=True); use forward() for bf16 dispatch")
         return self.ops.forward_device(x, mod, strategy, params or RealbParams(), self.fp4_dispatch, timer)
 
     def forward(self, x, mod, strategy: str = "realb", params: RealbParams | None = None, timer=None):
@@ -617,10 +636,16 @@ class DevicePlanResult:
     def __init__(self, ops, event):
         self.ops, self.event, self._plan = ops, event, None
 
+    def check(self) -> None:
+        """Raise PeerWaitTimeout if a peer-memory wait of this rank timed out."""
+        self.event.synchronize()
+        if int(self.ops.p2p_err.item()) != 0:
+            raise PeerWaitTimeout("a peer-memory wait timed out (a peer never signalled); output invalid")
+
     @property
     def plan(self) -> PrecisionPlan:
         if self._plan is None:
-            self.event.synchronize()
+            self.check()
             po = self.ops.plan_host.numpy()
             R = self.ops.R
             flags = po[3:3 + R]
@@ -698,6 +723,8 @@ def run_bench(args):
     # NCCL path bit for bit (and that no wait timed out) on every rank, and use it if
     # so; otherwise fall back to the NCCL path. The line reports which one ran.
     mode = os.environ.get("REALB_EP_COMM", "auto")
+    if mode == "auto" and torch.cuda.device_count() < world:
+        mode = "auto-gloo"  # fewer GPUs than ranks: validation run, ranks share cuda:0
     staged = mode in ("gloo", "p2p-gloo", "p2p-graph-gloo", "auto-gloo")
     auto = mode in ("auto", "auto-gloo")
     p2p = mode in ("p2p", "p2p-gloo", "p2p-graph", "p2p-graph-gloo") or auto
@@ -721,6 +748,8 @@ def run_bench(args):
     comm = EPComm(staged=staged, p2p=p2p)
     ops = CudaEPOps(shape, router.contiguous(), bias, local, world, T)
     fp4_dispatch = not getattr(args, "bf16_dispatch", False)
+    if not fp4_dispatch:
+        graph = False  # the host-sync-free layer always sends NVFP4 rows to W4A4 owners
     dev_t = "cpu" if staged else "cuda"
     transport_check = None
     if p2p:
@@ -922,12 +951,46 @@ def run_bench(args):
     g_ms, g_flops, g_fp4 = ops.time_gate_up()
     allg = [None] * world
     dist.all_gather_object(allg, (g_ms, g_flops, g_fp4))
+    # a timed-out peer-memory wait anywhere voids the run: reported, never hidden
+    wait_err = int(ops.p2p_err.item()) if getattr(ops, "_p2p_own", None) else 0
+    wait_errs = [None] * world
+    dist.all_gather_object(wait_errs, wait_err)
+    cpu = None
+    if rank == 0 and not getattr(args, "no_cpu_baseline", False):
+        import sys as _sys
+        from pathlib import Path as _P
+
+        _sys.path.insert(0, str(_P(__file__).resolve().parents[1]))
+        from oracle.cpu_arm import CpuLayerArm  # the CPU restatement (test infrastructure), rank 0 only
+
+        arm = CpuLayerArm(args.config, args.cpu_sample_tokens, args.vision_frac, num_ranks=world)
+        dt = min(arm.step() for _ in range(2))
+        cpu = arm.describe(args.cpu_sample_tokens / dt)
+        cpu["quantiser"] = arm.quantiser_rates()
+        cpu["policy"] = arm.policy_us_per_layer()
+        del arm
+    dist.barrier()
     if rank == 0:
         peaks, src = measured_peaks()
         crit = max(range(world), key=lambda i: allg[i][0])
         gm, gf, g4 = allg[crit]
         peak = FP4_TFLOPS_MEASURED if g4 else float(peaks.get("bf16_tflops", 1641.1))
         achieved = gf / (gm / 1e3) / 1e12
+        # SURVEY §8(d) layer roofline: t_roof = max_r F_r / Peak(plan_r), F_r = pairs_r x 6HI;
+        # full path adds 2 x max_r(bytes received by r) / 900 GB/s (dispatch + return)
+        H_, I_ = shape.hidden, shape.intermediate
+        rp = vt_all.sum(0).reshape(world, -1, 2).sum(axis=(1, 2))
+        w4 = [p is Precision.W4A4 for p in plan.per_rank_precision]
+        bf16_peak = float(peaks.get("bf16_tflops", 1641.1)) * 1e12
+        t_rank = [float(rp[i]) * 6 * H_ * I_ / ((FP4_TFLOPS_MEASURED * 1e12) if w4[i] else bf16_peak)
+                  for i in range(world)]
+        row_b = [(H_ // 2 + H_ // 16) if (w4[i] and fp4_dispatch) else 2 * H_ for i in range(world)]
+        t_comm = 2.0 * max(float(rp[i]) * row_b[i] for i in range(world)) / 900e9
+        layer_roof = {"t_roof_ms": max(t_rank) * 1e3, "t_roof_full_path_ms": (max(t_rank) + t_comm) * 1e3,
+                      "t_meas_ms": ms, "frac": max(t_rank) * 1e3 / ms,
+                      "frac_full_path": (max(t_rank) + t_comm) * 1e3 / ms,
+                      "what": "max_r pairs_r x 6HI / peak(plan_r) (BF16 burst / measured NVFP4); full path adds "
+                              "2 x max_r received bytes / 900 GB/s"}
         names = ("schedule_ns", "transform_ns", "dispatch_ns", "compute_ns", "combine_ns", "total_ns")
         out = {"metric": "MoE-layer prefill tokens/s and speedup vs all-BF16 EP at 1/2/4/8 B200",
                "value": world * T / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -953,8 +1016,10 @@ def run_bench(args):
                             "frac": achieved / peak, "traffic": None,
                             "peak_source": "measured cuBLASLt NVFP4 (DESIGN.md §4)" if g4
                             else f"{src} bf16_tflops (burst)",
-                            "algorithmic_flops_per_launch": gf, "launch_ms": gm},
+                            "algorithmic_flops_per_launch": gf, "launch_ms": gm, "layer": layer_roof},
                "plan_w4a4_ranks": sorted(plan.accelerated_ranks),
+               "p2p_wait_timeouts": wait_errs,
+               "cpu_baseline": cpu,
                "rank_pairs": vt_all.sum(0).reshape(world, -1, 2).sum(axis=(1, 2)).tolist(),
                "rank_phases_ns": {s: [dict(zip(names, r)) for r in rows] for s, rows in phases.items()},
                "gpu_launches": int(launches),

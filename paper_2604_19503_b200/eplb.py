@@ -101,9 +101,9 @@ def eplb_rebalance(state: EplbState, config: ClusterConfig,
 def memory_overhead(config: ClusterConfig, placement: ExpertPlacement) -> tuple[int, int]:
     """Per-rank expert weight bytes and the delta over a replica-free placement
     (costmodel.py:96-112; round half to even)."""
-    per = config.num_layers * config.bytes_per_expert / config.num_ranks
-    total = round(per * (placement.num_experts + placement.redundant_count))
-    base = round(per * placement.num_experts)
+    lb = config.num_layers * config.bytes_per_expert  # the reference's operation order
+    total = round(lb * (placement.num_experts + placement.redundant_count) / config.num_ranks)
+    base = round(lb * placement.num_experts / config.num_ranks)
     return total, total - base
 
 

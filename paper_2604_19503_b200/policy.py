@@ -216,10 +216,16 @@ def plan_realb(loads: Sequence[RankLoad], params: RealbParams, config: ClusterCo
         flags.ctypes.data_as(C.c_void_p))
     if not active:
         return plan_baseline(loads)
+    # the C routine flags list positions; the reference collects the hot and
+    # vision-heavy sets by RankLoad.rank and indexes precision by rank id
+    # (balancers.py:104-118), so the sets are mapped back through l.rank
+    hot = frozenset(int(loads[i].rank) for i in np.flatnonzero(flags & 1))
+    vision = frozenset(int(loads[i].rank) for i in np.flatnonzero(flags & 2))
+    accelerated = hot & vision
     return PrecisionPlan(
-        tuple(Precision.W4A4 if p else Precision.W16A16 for p in prec),
-        frozenset(int(r) for r in np.flatnonzero(flags & 1)),
-        frozenset(int(r) for r in np.flatnonzero(flags & 2)),
+        tuple(Precision.W4A4 if r in accelerated else Precision.W16A16 for r in range(R)),
+        hot,
+        vision,
         True,
     )
 

@@ -244,9 +244,9 @@ def text_exposure(run: MeasuredRun, trace: IterationTrace) -> float:
 def _mem_delta(run: MeasuredRun, config: ClusterConfig) -> int:
     """metrics.summarize_run's memory delta (metrics.py:105-129 via
     costmodel.memory_overhead): it depends only on the replica count."""
-    per = config.num_layers * config.bytes_per_expert / config.num_ranks
+    lb = config.num_layers * config.bytes_per_expert  # costmodel.py:105-111 operation order
     E = config.total_experts
-    return round(per * (E + run.max_redundant_count)) - round(per * E)
+    return round(lb * (E + run.max_redundant_count) / config.num_ranks) - round(lb * E / config.num_ranks)
 
 
 def write_run(run: MeasuredRun, trace: IterationTrace, out_dir, trace_sha256: str,

@@ -308,9 +308,10 @@ class VirtualEP:
 
         # baseline first (bf16 rows of every expert), then realb (NVFP4 rows and weights
         # of its W4A4 experts): both arms' per-rank compute then reads valid operands
-        layer.forward(x, mod, "baseline")
+        y_base = layer.forward(x, mod, "baseline").y.clone()
         res = layer.forward(x, mod, "realb", params)
         torch.cuda.synchronize()
+        accuracy = self.accuracy(x, mod, y_base, res.y, res.plan, layer)
         plan = res.plan
         prec = plan.expert_precision(layer.placement).astype(np.int64)
         vt = res.expert_vt.astype(np.int64)
@@ -391,7 +392,44 @@ class VirtualEP:
             "projected_p2p_layer_speedup": p2p_bf16.layer_latency_ns / p2p_realb.layer_latency_ns,
             "transform_hidden": all(t <= disp_bf16 for t in transform_ms),
             "k3_overlap_one_gpu": k3_timeline,
+            "accuracy": accuracy,
         }
+
+    def accuracy(self, x, mod, y_base, y_realb, plan, layer) -> dict:
+        """Per-layer accuracy proxy (the paper's <= 1.2-point downstream delta is not
+        reproducible offline): the W4A4 ranks' FP4 weight-error summary
+        (quantize_tensor / ErrorSummary, fp4.py:137-170, on the device), the ReaLB
+        and FP4-All layer outputs against the all-BF16 layer on the same batch
+        (relative RMS, over all / text / vision tokens) and the text exposure
+        (metrics.py:72-90)."""
+        from .quant import weight_error_summary
+
+        torch, R, epr = self.torch, self.R, self.epr
+        I, H = self.shape.intermediate, self.shape.hidden
+        vis = mod.bool()
+        y_realb = y_realb.clone()  # a view of the layer's output buffer: the next forward reuses it
+
+        def rel(a, b, sel=None):
+            if sel is not None:
+                a, b = a[sel], b[sel]
+            a, b = a.float(), b.float()
+            d = float(torch.linalg.vector_norm(b))
+            return float(torch.linalg.vector_norm(a - b)) / d if d > 0 else 0.0
+
+        acc_ranks = sorted(plan.accelerated_ranks)
+        werr = {}
+        for r in acc_ranks:
+            e0, e1 = r * epr, (r + 1) * epr
+            werr[str(r)] = weight_error_summary([layer.w.w_gu[e0 * 2 * I:e1 * 2 * I], layer.w.w_d[e0 * H:e1 * H]])
+        y_fp4 = layer.forward(x, mod, "fp4all", RealbParams(global_batch_threshold=0)).y
+        torch.cuda.synchronize()
+        return {"fp4_weight_error_w4a4_ranks": werr,
+                "realb_vs_bf16_layer_rel": {"all": rel(y_realb, y_base), "text": rel(y_realb, y_base, ~vis),
+                                            "vision": rel(y_realb, y_base, vis)},
+                "fp4all_vs_bf16_layer_rel": {"all": rel(y_fp4, y_base), "text": rel(y_fp4, y_base, ~vis),
+                                             "vision": rel(y_fp4, y_base, vis)},
+                "what": "W4A4 ranks' FP4 weight error (device quantize_tensor / ErrorSummary) and layer-output "
+                        "deltas vs the all-BF16 layer on the same batch; text exposure is reported beside"}
 
 
 def virtual_ep_report(args, torch, R: int = 8) -> dict:

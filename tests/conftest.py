@@ -42,3 +42,24 @@ def reference():
 @pytest.fixture(scope="session")
 def golden():
     return ROOT / "tests" / "golden"
+
+
+@pytest.fixture
+def parity_log(request):
+    """parity_log(name, measured, bar): append the measured error of a parity
+    check and its bar to gpurun_out/parity_log.jsonl (REALB_PARITY_LOG overrides),
+    so the margins the tolerances leave are on record."""
+    import json
+
+    path = Path(os.environ.get("REALB_PARITY_LOG", ROOT / "gpurun_out" / "parity_log.jsonl"))
+
+    def log(name, measured, bar):
+        try:
+            path.parent.mkdir(parents=True, exist_ok=True)
+            with open(path, "a") as f:
+                f.write(json.dumps({"test": request.node.nodeid, "check": name, "measured": float(measured),
+                                    "bar": float(bar)}) + "\n")
+        except OSError:
+            pass
+
+    return log

@@ -97,3 +97,20 @@ def policy_cases(n: int = 400, seed: int = 77):
         cases.append(dict(v=[int(a) for a in v], t=[int(a) for a in (tot - v)], C=C, Md=Md,
                           thr=thr, iso=iso))
     return cases
+
+
+ON_GRID = GOLDEN_FILE_INPUT[:16]
+
+
+def tensor_cases() -> list[np.ndarray]:
+    """Flat inputs for quantize_tensor + ErrorSummary (fp4.py:137-170): the
+    reference tests' cases (tests/test_fp4.py:151-179) plus ragged, wide-range and
+    bf16-weight inputs."""
+    rng = np.random.default_rng(2604)
+    wide = rng.normal(0, 1, 1001) * np.exp2(rng.integers(-24, 14, 1001).astype(float))
+    wide[rng.integers(0, 1001, 40)] = 0.0
+    w = (rng.normal(0, 0.02, 4099)).astype(np.float32)
+    wbf16 = ((w.view(np.uint32) + 0x7FFF + ((w.view(np.uint32) >> 16) & 1)) & 0xFFFF0000).view(np.float32)
+    return [np.array(ON_GRID, float), np.full(17, 6.0), np.array([6.0] * 16 + [1.25]), np.array([1.25]),
+            np.random.default_rng(0).standard_normal(4096), wide, wbf16.astype(np.float64),
+            np.array(GOLDEN_FILE_INPUT, float)]

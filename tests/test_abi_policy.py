@@ -112,6 +112,38 @@ def test_policy_fuzz_against_live_reference(reference, totals, fracs, C, Md, thr
     assert got.active == ref.active
 
 
+@given(totals=st.lists(st.integers(0, 10_000), min_size=4, max_size=4),
+       fracs=st.lists(st.floats(0.0, 1.0), min_size=4, max_size=4),
+       perm=st.permutations(range(4)), dup=st.booleans(), iso=st.booleans())
+@settings(max_examples=200, deadline=None)
+def test_policy_rank_ids_not_positions(reference, totals, fracs, perm, dup, iso):
+    """Loads out of rank order (and duplicate rank ids): the hot / vision sets are
+    rank ids and precision is indexed by rank id (balancers.py:104-118)."""
+    from moesim import ClusterConfig as RC, RankLoad as RL, RealbParams as RP, plan_realb as rplan
+
+    base = _mk(totals, fracs)
+    ranks = list(perm)
+    if dup:
+        ranks[1] = ranks[0]
+    loads = [RankLoad(r, l.vision_tokens, l.text_tokens) for r, l in zip(ranks, base)]
+    ref = rplan([RL(l.rank, l.vision_tokens, l.text_tokens) for l in loads], RP(1.0, 0.7, 0),
+                RC(4, 1, 1, 1, iso))
+    got = plan_realb(loads, RealbParams(1.0, 0.7, 0), _cfg(4, iso))
+    assert [p.value for p in got.per_rank_precision] == [p.value for p in ref.per_rank_precision]
+    assert got.hot_ranks == ref.hot_ranks and got.vision_heavy_ranks == ref.vision_heavy_ranks
+    assert got.active == ref.active
+
+
+def test_policy_advisor_case(reference):
+    from moesim import ClusterConfig as RC, RankLoad as RL, RealbParams as RP, plan_realb as rplan
+
+    raw = [(1, 900, 100), (0, 10, 10), (2, 10, 10)]
+    ref = rplan([RL(*t) for t in raw], RP(1.0, 0.7, 0), RC(3, 1, 1, 1))
+    got = plan_realb([RankLoad(*t) for t in raw], RealbParams(1.0, 0.7, 0), _cfg(3))
+    assert [p.value for p in got.per_rank_precision] == [p.value for p in ref.per_rank_precision]
+    assert got.per_rank_precision[1] is Precision.W4A4
+
+
 def test_aggregation_matches_reference(reference):
     import random
 

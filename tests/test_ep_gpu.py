@@ -75,10 +75,15 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir,
         torch.cuda.synchronize()
         assert torch.equal(y0, y1) and torch.equal(yg, y0)
         y = yg
+        assert int(ops.p2p_err.item()) == 0, "a peer-memory wait timed out"
+        res.check()
+        _dump_operands(ops, x, outdir, rank)
     else:
         y, plan, vt = layer.forward(x, mod, strategy, params)
         if p2p:  # a second layer call exercises window reuse and the epoch counters
             y, plan, vt = layer.forward(x, mod, strategy, params)
+            torch.cuda.synchronize()
+            assert int(ops.p2p_err.item()) == 0, "a peer-memory wait timed out"
     torch.cuda.synchronize()
     if p2p:
         dist.barrier()
@@ -110,8 +115,8 @@ def test_ep2_peer_memory_transport_equals_single_gpu_layer(tmp_path, shape_name,
 
 
 @pytest.mark.parametrize("shape_name,E,T,strategy,fp4_dispatch", [
-    ("kimi", 16, 384, "realb", True), ("kimi", 16, 384, "realb", False), ("qwen", 16, 256, "fp4all", True),
-    ("tiny", 8, 512, "baseline", False), ("kimi_shared", 16, 384, "realb", True),
+    ("kimi", 16, 384, "realb", True), ("kimi", 40, 384, "realb", True), ("qwen", 16, 256, "fp4all", True),
+    ("tiny", 8, 512, "baseline", True), ("kimi_shared", 16, 384, "realb", True),
     ("kimi", 16, 203, "fp4all", True)])  # ragged token count (not a multiple of the 64-token chunk)
 def test_ep2_host_sync_free_layer_and_graph(tmp_path, shape_name, E, T, strategy, fp4_dispatch):
     """The host-sync-free EP layer: C1 through peer memory, plan and window offsets
@@ -121,7 +126,7 @@ def test_ep2_host_sync_free_layer_and_graph(tmp_path, shape_name, E, T, strategy
 
 
 @pytest.mark.parametrize("world,shape_name,E,T,strategy,fp4_dispatch", [
-    (4, "kimi", 16, 256, "realb", True), (4, "qwen", 32, 192, "fp4all", False)])
+    (4, "kimi", 16, 256, "realb", True), (4, "qwen", 32, 192, "fp4all", True)])
 def test_ep4_host_sync_free_layer_and_graph(tmp_path, world, shape_name, E, T, strategy, fp4_dispatch):
     """The host-sync-free peer-memory layer with FOUR ranks (processes sharing one
     GPU): plan over 4 ranks, window offsets for 4 sources, direct dispatch and the
@@ -135,6 +140,81 @@ def test_ep1_host_sync_free_layer_own_windows(tmp_path, strategy):
     one process (also the configuration scripts/exp/ep1_selfcheck.py runs under
     compute-sanitizer); equals the single-GPU layer."""
     _run_and_compare(tmp_path, "kimi", 16, 333, strategy, True, p2p=True, device_plan=True, world=1)
+
+
+def test_device_plan_layer_rejects_bf16_dispatch():
+    """The host-sync-free layer always sends NVFP4 rows to W4A4 owners; asking it
+    for bf16 dispatch is an error (not a silently different measurement)."""
+    from paper_2604_19503_b200.ep import EPMoELayer
+    from paper_2604_19503_b200.moe import SHAPES
+
+    class _Comm:
+        world, rank, p2p = 2, 0, True
+
+    class _Ops:
+        def forward_device(self, *a):
+            raise AssertionError("must not run")
+
+    layer = EPMoELayer(SHAPES["tiny"], _Comm(), _Ops(), fp4_dispatch=False)
+    with pytest.raises(ValueError, match="NVFP4"):
+        layer.forward_device(None, None, "realb")
+
+
+def _dump_operands(ops, x, outdir, rank):
+    """What direct dispatch wrote into THIS rank's GEMM operand windows (valid
+    grouped rows only), with the row map back to (source rank, send-order row),
+    plus this rank's own tokens and send positions: the parent process checks
+    every received row against the oracle (K4 bit-exactness on the wire)."""
+    from paper_2604_19503_b200.ep import _device_view
+    from paper_2604_19503_b200.quant import sf_mma_to_flat
+
+    H, rc, El = ops.H, ops.rows_cap, ops.El
+    r = ops.p2p_rank
+    torch.cuda.synchronize()
+    lay = ops.local_layout.cpu().numpy()
+    starts, counts = lay[8:8 + El].astype(np.int64), lay[8 + El:8 + 2 * El].astype(np.int64)
+    g = np.concatenate([s + np.arange(c) for s, c in zip(starts, counts)]) if counts.sum() else np.zeros(0, np.int64)
+    gt = torch.from_numpy(g).cuda()
+    opa = _device_view(ops.p2p["opa"][r], rc * H, torch.bfloat16).view(rc, H)
+    opc = _device_view(ops.p2p["opc"][r], rc * H // 2, torch.uint8).view(rc, H // 2)
+    ops_mma = _device_view(ops.p2p["ops"][r], rc * H // 16, torch.uint8).cpu().numpy()
+    np.savez(os.path.join(outdir, f"ops{rank}.npz"), g=g, row_map=ops.row_map[gt].cpu().numpy(),
+             a=opa[gt].view(torch.int16).cpu().numpy(), codes=opc[gt].cpu().numpy(),
+             sf=sf_mma_to_flat(ops_mma, rc, H)[g], w4a4=ops.prec_local.cpu().numpy(),
+             x=x.view(torch.int16).cpu().numpy(), send_pos=ops.send_pos[:x.shape[0]].cpu().numpy())
+
+
+def _check_direct_dispatch_operands(tmp_path, world):
+    """Every row direct dispatch placed in an owner's operand is its source token:
+    bf16 bits equal for a W16A16 owner; for a W4A4 owner the NVFP4 codes and the
+    scales (after realb_sf_rows_to_mma) equal oracle.quantize_bf16 of the token's
+    bf16 row (the reference block rule, fp4.py:173-227), bit for bit."""
+    import oracle
+
+    d = [np.load(tmp_path / f"ops{r}.npz") for r in range(world)]
+    inv, oq = [], []
+    for s in range(world):
+        sp = d[s]["send_pos"]
+        iv = np.full(sp.size, -1, np.int64)
+        iv[sp.reshape(-1)] = np.repeat(np.arange(sp.shape[0]), sp.shape[1])
+        inv.append(iv)
+        oq.append(oracle.quantize_bf16(d[s]["x"].view(np.uint16)))
+    checked = 0
+    for r in range(world):
+        m = d[r]["row_map"].astype(np.int64)
+        src, row = m >> 25, m & ((1 << 25) - 1)
+        w4a4 = bool(d[r]["w4a4"].any())
+        for s in range(world):
+            sel = src == s
+            tok = inv[s][row[sel]]
+            assert (tok >= 0).all()
+            if w4a4:
+                assert (d[r]["codes"][sel] == oq[s][0][tok]).all(), (r, s)
+                assert (d[r]["sf"][sel] == oq[s][1][tok]).all(), (r, s)
+            else:
+                assert (d[r]["a"][sel] == d[s]["x"][tok]).all(), (r, s)
+            checked += int(sel.sum())
+    assert checked > 0
 
 
 def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False, world=2):
@@ -157,6 +237,21 @@ def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, de
     y = np.concatenate([a["y"] for a in r])
     assert list(r[0]["acc"]) == sorted(res.plan.accelerated_ranks)
     np.testing.assert_array_equal(y, ref)
+    # and the EP layer against the CPU oracle directly (same plan, the device logits)
+    from oracle import moe_ref
+
+    prec = res.plan.expert_precision(single.placement)
+    oref = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                             gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
+                             expert_prec=prec, routed_scaling=shape.routed_scaling,
+                             logits=single.logits[:world * T].cpu().numpy(),
+                             shared=None if sh is None else (sh[0].float().cpu().numpy(), sh[1].float().cpu().numpy()))
+    assert (single.topk_idx[:world * T].cpu().numpy() == oref["idx"]).all()
+    err = float(np.linalg.norm(y - oref["y"]) / np.linalg.norm(oref["y"]))
+    bar = 1e-3 if (strategy == "fp4all" and sh is None) else 2e-3  # tests/test_layer_gpu.py BAR
+    assert err < bar, err
+    if device_plan:
+        _check_direct_dispatch_operands(tmp_path, world)
 
 
 def _setup_fail_worker(rank, world, port, outdir):

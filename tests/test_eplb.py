@@ -99,3 +99,28 @@ def test_schedule_matches_reference_run(reference, golden, kw):
     ours = [(it, m) for it, (_, m) in enumerate(sched) if m is not None]
     assert ours == [(e.iteration, e.replicas_moved) for e in rrun.migration_events]
     assert max(p.redundant_count for p, _ in sched) == rrun.max_redundant_count
+
+
+def test_memory_overhead_rounding_matches_reference(reference):
+    """Odd bytes_per_expert and non-power-of-two rank counts: the half-to-even
+    rounding must see the reference's operation order (costmodel.py:105-111)."""
+    from moesim.costmodel import memory_overhead
+
+    rng = np.random.default_rng(11)
+    cases = [(1, 7, 10, 45, 0)] + [
+        (int(rng.integers(1, 6)), int(rng.integers(1, 4000)), int(rng.integers(1, 13)),
+         int(rng.integers(1, 9)), int(rng.integers(0, 20))) for _ in range(3000)]
+    for L, bpe, R, epr, red in cases:
+        cfg = ClusterConfig(R, L, epr, bpe)
+        E = R * epr
+        hosts = [(e // epr,) for e in range(E)]
+        for j in range(red):  # replicas on other ranks
+            e = j % E
+            extra = (hosts[e][-1] + 1) % R
+            if extra not in hosts[e]:
+                hosts[e] = hosts[e] + (extra,)
+        red_n = sum(len(h) - 1 for h in hosts)
+        place = ExpertPlacement(tuple(hosts), red_n)
+        rplace = reference.ExpertPlacement(assignment=tuple(hosts), redundant_count=red_n)
+        assert eplb.memory_overhead(cfg, place) == memory_overhead(_ref_cfg(reference, cfg), rplace), \
+            (L, bpe, R, epr, red_n)

@@ -53,7 +53,7 @@ def cluster(request, monkeypatch):
     (8, 2048, 1408, [513, 129, 1, 0, 777, 256, 2048, 90]),   # Kimi down shape
 ])
 @pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_SWIGLU])
-def test_grouped_bf16(E, N, K, counts, epi, cluster):
+def test_grouped_bf16(E, N, K, counts, epi, cluster, parity_log):
     torch.manual_seed(E * 31 + N + K)
     prec_sel = np.zeros(E, np.int64)
     lay, rows = host_layout(counts, prec_sel)
@@ -63,8 +63,12 @@ def test_grouped_bf16(E, N, K, counts, epi, cluster):
     out = run_bf16(A, W, lay, N, K, E, 0, epi, rows_cap)
     for e, (rs, y) in ref_rows(A, W, lay, E, N, counts, prec_sel, 0, epi).items():
         got = out[rs:rs + counts[e]].float()
-        err = (got - y).norm() / y.norm().clamp_min(1e-30)
-        assert err < 1e-2, (e, float(err))   # bf16 output rounding ~ 3e-3
+        # against the fp32 reference rounded to bf16 (the kernel's one output rounding):
+        # what remains is fp32 accumulation order (+ __expf in SwiGLU) flipping roundings
+        yb = y.to(torch.bfloat16).float()
+        err = float((got - yb).norm() / yb.norm().clamp_min(1e-30))
+        parity_log("k5_vs_fp32_torch_bf16_rounded", err, 2e-3)
+        assert err < 2e-3, (e, err)
 
 
 def test_grouped_bf16_precision_subset():

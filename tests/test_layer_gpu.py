@@ -15,6 +15,19 @@ from paper_2604_19503_b200.workload import WorkloadSpec, make_batch, make_expert
 pytestmark = pytest.mark.gpu
 
 
+# Layer parity bars (relative RMS error vs the oracle), about 10x the measured
+# error (measured values: gpurun_out/parity_log.jsonl -> profiles/):
+#   all-BF16 layer                      2e-3  (GEMM accumulation order; the bf16
+#                                              roundings are the oracle's own)
+#   all-W4A4 layer vs the FP4 emulation 1e-3  (operands are exact on the FP4 grid)
+#   mixed (ReaLB) layer                 2e-3
+BAR = {"baseline": 2e-3, "fp4all": 1e-3, "realb": 2e-3, "realb-seq": 2e-3}
+
+
+def rel_err(y, ref):
+    return float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+
+
 def small(shape: MoEShape, E=None):
     from dataclasses import replace
 
@@ -180,12 +193,14 @@ def test_combine_weighted_sum():
     _lib.call("realb_combine", rows.data_ptr(), pos.data_ptr(), w.data_ptr(), T, H, k, None, y.data_ptr(),
               _lib.stream_ptr())
     ref = (w[:, :, None] * rows[pos.long()].float()).sum(1)
-    assert ((y.float() - ref).abs() <= 1e-2 * ref.abs() + 1e-2).all()
+    # fp32 accumulation then ONE bf16 rounding: within half a bf16 ulp (2^-8 relative)
+    # of the fp32 sum, plus fp32 summation-order slack
+    assert ((y.float() - ref).abs() <= 2.0**-8 * ref.abs() + 1e-6).all()
 
 
 @pytest.mark.parametrize("name,E,T", [("tiny", None, 1024), ("kimi", 16, 512), ("qwen", 32, 384),
                                       ("ernie_vision", 16, 256)])
-def test_layer_bf16_vs_oracle(name, E, T):
+def test_layer_bf16_vs_oracle(name, E, T, parity_log):
     shape = small(SHAPES[name], E)
     layer, x, mod, router, gu, dn, _ = build_layer(shape, T)
     res = layer.forward(x, mod, strategy="baseline")
@@ -195,15 +210,16 @@ def test_layer_bf16_vs_oracle(name, E, T):
                             shape.scoring, routed_scaling=shape.routed_scaling,
                             logits=layer.logits[:T].cpu().numpy())
     y = res.y.float().cpu().numpy()
-    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
-    assert err < 1e-2, err
+    err = rel_err(y, ref["y"])
+    parity_log("layer_bf16", err, BAR["baseline"])
+    assert err < BAR["baseline"], err
 
 
 @pytest.mark.parametrize("name,E,T,strategy,R", [("tiny", None, 1024, "fp4all", 2),
                                                   ("kimi", 16, 512, "fp4all", 8),
                                                   ("kimi", 64, 2048, "realb", 8),
                                                   ("qwen", 32, 512, "realb", 8)])
-def test_layer_w4a4_vs_oracle(name, E, T, strategy, R):
+def test_layer_w4a4_vs_oracle(name, E, T, strategy, R, parity_log):
     """Mixed-precision layer: W4A4 experts run the NVFP4 path (K3 weights, K4
     activations + SwiGLU output, K6 GEMMs) and match the FP4-emulating oracle."""
     shape = small(SHAPES[name], E)
@@ -220,8 +236,9 @@ def test_layer_w4a4_vs_oracle(name, E, T, strategy, R):
                             shape.scoring, expert_prec=prec, routed_scaling=shape.routed_scaling,
                             logits=layer.logits[:T].cpu().numpy())
     y = res.y.float().cpu().numpy()
-    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
-    assert err < 2e-2, err
+    err = rel_err(y, ref["y"])
+    parity_log(f"layer_{strategy}", err, BAR[strategy])
+    assert err < BAR[strategy], err
     # and the FP4 path is genuinely different from all-BF16 (documented accuracy delta)
     ref16 = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
                               gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k,
@@ -311,7 +328,7 @@ def test_cuda_graph_capture_matches_eager(strategy, R):
 
 
 @pytest.mark.parametrize("strategy", ["baseline", "fp4all"])
-def test_ernie_modality_split_layer_vs_oracle(strategy):
+def test_ernie_modality_split_layer_vs_oracle(strategy, parity_log):
     """BASELINE configs[3]: text tokens -> text group (W16A16), vision tokens ->
     vision group (ReaLB / FP4 policy, modality-isolated), vs the oracle per group."""
     from paper_2604_19503_b200.moe import ModalitySplitMoELayer
@@ -336,8 +353,10 @@ def test_ernie_modality_split_layer_vs_oracle(strategy):
                                 gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
                                 expert_prec=prec)
         got = y.float().cpu().numpy()[sel]
-        err = np.linalg.norm(got - ref["y"]) / np.linalg.norm(ref["y"])
-        assert err < 2e-2, (shape.name, err)
+        err = rel_err(got, ref["y"])
+        bar = BAR["baseline"] if shape is st else BAR[strategy]
+        parity_log(f"ernie_split_{shape.name}_{strategy}", err, bar)
+        assert err < bar, (shape.name, err)
     # the vision group is modality-isolated: under fp4all every vision expert runs W4A4
     if strategy == "fp4all":
         assert res_v.plan.expert_precision(vision.placement).all()
@@ -346,7 +365,7 @@ def test_ernie_modality_split_layer_vs_oracle(strategy):
 
 @pytest.mark.parametrize("T", [1, 63, 64, 65, 129])
 @pytest.mark.parametrize("strategy", ["baseline", "fp4all"])
-def test_layer_ragged_token_counts(T, strategy):
+def test_layer_ragged_token_counts(T, strategy, parity_log):
     """Token counts off the 64-token chunk and 128-row tile grids (partial chunks,
     single-row experts, experts with no rows) match the oracle."""
     shape = SHAPES["tiny"]
@@ -360,8 +379,9 @@ def test_layer_ragged_token_counts(T, strategy):
     assert (layer.topk_idx[:T].cpu().numpy() == ref["idx"]).all()
     assert (res.expert_vt == ref["vt"]).all()
     y = res.y.float().cpu().numpy()
-    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
-    assert err < 2e-2, err
+    err = rel_err(y, ref["y"])
+    parity_log(f"layer_ragged_{strategy}", err, BAR[strategy])
+    assert err < BAR[strategy], err
 
 
 def test_layer_zero_tokens():
@@ -374,7 +394,7 @@ def test_layer_zero_tokens():
     assert (res.expert_vt == 0).all() and not res.plan.active
 
 
-def test_layer_all_tokens_on_one_expert_set():
+def test_layer_all_tokens_on_one_expert_set(parity_log):
     """Maximum skew: every token routes to the same k experts (one group holds all
     T rows, the others none) — BF16 and W4A4 paths vs the oracle."""
     shape = small(SHAPES["kimi"], 16)
@@ -392,8 +412,9 @@ def test_layer_all_tokens_on_one_expert_set():
                                 expert_prec=prec, routed_scaling=shape.routed_scaling,
                                 logits=layer.logits[:T].cpu().numpy())
         y = res.y.float().cpu().numpy()
-        err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
-        assert err < 2e-2, (strategy, err)
+        err = rel_err(y, ref["y"])
+        parity_log(f"layer_one_expert_set_{strategy}", err, BAR[strategy])
+        assert err < BAR[strategy], (strategy, err)
 
 
 def test_nonfinite_weights_raise_quantization_domain_error():
@@ -411,7 +432,7 @@ def test_nonfinite_weights_raise_quantization_domain_error():
 
 
 @pytest.mark.parametrize("strategy,R", [("baseline", 1), ("fp4all", 2), ("realb", 8)])
-def test_layer_with_shared_expert_vs_oracle(strategy, R):
+def test_layer_with_shared_expert_vs_oracle(strategy, R, parity_log):
     """Kimi-VL with its shared-expert MLP: computed on its own stream, overlapped
     with the routed path and added in the combine; vs the oracle, eager and as a
     CUDA graph."""
@@ -435,8 +456,10 @@ def test_layer_with_shared_expert_vs_oracle(strategy, R):
                             logits=layer.logits[:T].cpu().numpy(),
                             shared=(sh[0].float().cpu().numpy(), sh[1].float().cpu().numpy()))
     y = res.y.float().cpu().numpy()
-    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
-    assert err < 2e-2, err
+    err = rel_err(y, ref["y"])
+    bar = max(BAR[strategy], BAR["baseline"])  # the shared MLP is BF16 in every strategy
+    parity_log(f"layer_shared_{strategy}", err, bar)
+    assert err < bar, err
     eager = res.y.clone()
     cap = layer.capture(x, mod, strategy, params)
     assert torch.equal(cap.replay(), eager)
@@ -456,7 +479,7 @@ def test_realb_seq_equals_realb():
 
 
 @pytest.mark.parametrize("name", ["kimi", "qwen", "ernie_vision"])
-def test_full_size_ep8_batch_properties(name):
+def test_full_size_ep8_batch_properties(name, parity_log):
     """BASELINE configs[1] / [2] at full size: the Kimi-VL layer (E=64, top-6,
     H=2048, I=1408) and the Qwen3-VL layer (E=128, top-8, I=768) over the EP8
     global batch (8 x 8192 tokens, 70 % vision, tracegen skew)
@@ -512,5 +535,75 @@ def test_full_size_ep8_batch_properties(name):
                             gu.float().cpu().numpy(), dn.float().cpu().numpy(), k, shape.scoring,
                             expert_prec=prec, routed_scaling=shape.routed_scaling, logits=logits[sel])
     y = res.y[sel_t].float().cpu().numpy()
-    err = np.linalg.norm(y - ref["y"]) / np.linalg.norm(ref["y"])
-    assert err < 2e-2, err
+    err = rel_err(y, ref["y"])
+    parity_log(f"full_size_{name}_realb_sample", err, BAR["realb"])
+    assert err < BAR["realb"], err
+
+
+def test_full_size_ernie_modality_split_ep8(parity_log):
+    """BASELINE configs[3] at full size: ERNIE-4.5-VL's text group (64 experts,
+    I = 1536) and vision group (64 experts, I = 512), H = 2560, top-6, over the
+    EP8 global batch (65,536 tokens, 70 % vision) with the vision group's
+    modality-isolated ReaLB plan over 8 ranks. Both groups: routing bit-exact (D1)
+    and equal to the planned sets, counts == the oracle's, the device plan == the
+    host policy; the W4A4 vision expert's K3 codes bit-exact; a sample of text AND
+    vision tokens within the layer bars of the oracle."""
+    from paper_2604_19503_b200.moe import ModalitySplitMoELayer
+    from paper_2604_19503_b200.policy import plan_for, rank_loads_from_counts
+    from paper_2604_19503_b200.quant import sf_mma_to_flat
+    from paper_2604_19503_b200.workload import make_split_batch
+
+    st, sv = SHAPES["ernie_text"], SHAPES["ernie_vision"]
+    T, R = 65536, 8
+    x, mod, rt, rv, pt, pv = make_split_batch(st, sv, WorkloadSpec(tokens=T, vision_frac=0.7, num_ranks=R))
+    gt, dt = make_experts(st, seed=11)
+    gv, dv = make_experts(sv, seed=12)
+    vis = mod.bool()
+    n_vis = int(vis.sum())
+    text = MoELayer(MoEWeights.from_hf(st, rt, gt, dt), max_tokens=T - n_vis, cluster=ClusterConfig(R, 1, 8, 1))
+    vision = MoELayer(MoEWeights.from_hf(sv, rv, gv, dv), max_tokens=n_vis, cluster=ClusterConfig(R, 1, 8, 1, True))
+    layer = ModalitySplitMoELayer(text, vision)
+    params = RealbParams()
+    y, res_t, res_v = layer.forward(x, mod, "realb", params)
+    torch.cuda.synchronize()
+    vision.check_flag()
+    assert res_v.plan.active and res_v.plan.accelerated_ranks and not res_t.plan.active
+    visn = vis.cpu().numpy()
+    modh = mod.cpu().numpy()
+    yh = y.float().cpu().numpy()
+    for grp, shape, router, gu, dn, res, planned, sel in (
+            (text, st, rt, gt, dt, res_t, pt, ~visn), (vision, sv, rv, gv, dv, res_v, pv, visn)):
+        n = int(sel.sum())
+        logits = grp.logits[:n].cpu().numpy()
+        idx = grp.topk_idx[:n].cpu().numpy()
+        _, idx_ref, w_ref = moe_ref.route(None, None, shape.top_k, shape.scoring, logits=logits)
+        assert (idx == idx_ref).all()
+        assert (np.sort(idx, 1) == np.sort(planned, 1)).all()
+        vt = res.expert_vt.astype(np.int64)
+        assert (vt == moe_ref.expert_counts(idx_ref, modh[sel], shape.num_experts)).all()
+        ref_plan = plan_for("realb" if grp is vision else "baseline", rank_loads_from_counts(vt, grp.cluster),
+                            grp.cluster, params)
+        assert sorted(res.plan.accelerated_ranks) == sorted(ref_plan.accelerated_ranks)
+        prec = res.plan.expert_precision(grp.placement)
+        # a token sample of this group vs the oracle
+        pick = np.random.default_rng(9).choice(n, 40, replace=False)
+        tok = np.nonzero(sel)[0][pick]
+        ref = moe_ref.moe_layer(x[torch.from_numpy(tok).cuda()].float().cpu().numpy(), modh[tok],
+                                router.float().cpu().numpy(), gu.float().cpu().numpy(), dn.float().cpu().numpy(),
+                                shape.top_k, shape.scoring, expert_prec=prec, logits=logits[pick])
+        err = rel_err(yh[tok], ref["y"])
+        bar = BAR["realb"] if grp is vision else BAR["baseline"]
+        parity_log(f"full_size_ernie_split_{shape.name}", err, bar)
+        assert err < bar, (shape.name, err)
+    # K3 on a W4A4 vision expert: codes + scales bit-exact with the oracle quantiser
+    prec = res_v.plan.expert_precision(vision.placement)
+    ws = vision._fp4_ws()
+    e = int(np.nonzero(prec)[0][0])
+    H, I = sv.hidden, sv.intermediate
+    for wt, codes, sf, rows, cols in ((vision.w.w_gu, ws["wgu_codes"], ws["wgu_sf"], 2 * I, H),
+                                      (vision.w.w_d, ws["wd_codes"], ws["wd_sf"], H, I)):
+        wbits = wt[e * rows:(e + 1) * rows].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        c_ref, s_ref = oracle.quantize_bf16(wbits)
+        assert (codes[e * rows:(e + 1) * rows].cpu().numpy() == c_ref).all()
+        s = sf.view(-1)[e * rows * cols // 16:(e + 1) * rows * cols // 16].cpu().numpy()
+        assert (sf_mma_to_flat(s, rows, cols) == s_ref).all()

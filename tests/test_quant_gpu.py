@@ -136,3 +136,87 @@ def test_bf16_path_row_tail_and_flat_layout(q):
         codes, sf = q.quantize_nvfp4(w.cuda(), layout="flat")
         oc, osf = oracle.quantize_bf16(w.view(torch.int16).numpy().view(np.uint16))
         assert (codes.cpu().numpy() == oc).all() and (sf.cpu().numpy() == osf).all(), (rows, cols)
+
+
+# ---------------------------------------------------------------- Q5 / Q6 on the device
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_quantize_tensor_vs_reference_fixture(q, golden, dtype, parity_log):
+    """realb_quantize_tensor_nvfp4 == the reference's quantize_tensor +
+    ErrorSummary + pack_block (fixture from the reference itself): block records
+    and per-block max relative errors bit-exact; rmse / relative rmse within
+    1e-12 (device tree-order sums vs the reference's sequential sums)."""
+    import torch
+
+    d = np.load(golden / "fp4_tensor_cases.npz")
+    for i in range(int(d["n"])):
+        v = d[f"c{i}_values"]
+        if dtype == "f32" and not (v.astype(np.float32).astype(np.float64) == v).all():
+            continue  # f32 input must hold the same values
+        t = torch.from_numpy(v.astype(np.float64 if dtype == "f64" else np.float32)).cuda()
+        r = q.quantize_tensor_device(t)
+        torch.cuda.synchronize()
+        assert int(r["flag"].item()) == 0
+        assert (r["records"].cpu().numpy() == d[f"c{i}_records"]).all(), i
+        assert (r["max_rel"].cpu().numpy() == d[f"c{i}_max_rel"]).all(), i
+        s = q.summary_from_sums(r["sums"], r["n"])
+        for got, ref in ((s.rmse, float(d[f"c{i}_rmse"])), (s.relative_rmse, float(d[f"c{i}_rel_rmse"]))):
+            assert abs(got - ref) <= 1e-12 * max(abs(ref), 1e-300), (i, got, ref)
+            parity_log("quantize_tensor_rmse_rel_diff", abs(got - ref) / max(abs(ref), 1e-300), 1e-12)
+
+
+def test_quantize_tensor_reference_api(q, golden, tmp_path):
+    """The reference-shaped API (list in -> (list[Fp4Block], ErrorSummary)), its
+    error behaviour, the reference test cases (tests/test_fp4.py:151-179) and the
+    golden file written from device-produced blocks."""
+    import math
+
+    blocks, s = q.quantize_tensor(gen.ON_GRID)
+    assert s.rmse == 0.0
+    blocks, s = q.quantize_tensor([6.0] * 17)
+    assert len(blocks) == 2 and s.rmse == 0.0 and s.max_relative_error_per_block == (0.0, 0.0)
+    _, s = q.quantize_tensor([6.0] * 16 + [1.25])
+    tail = q.dequantize_block(q.quantize_tensor([1.25])[0][0])[0]
+    assert s.rmse == math.sqrt((1.25 - tail) ** 2 / 17)
+    _, s = q.quantize_tensor(list(map(float, np.random.default_rng(0).standard_normal(4096))))
+    assert s.relative_rmse < 0.10
+    with pytest.raises(ValueError):
+        q.quantize_tensor([])
+    with pytest.raises(ValueError):
+        q.quantize_tensor([1.0] * 16, block_size=32)
+    with pytest.raises(q.QuantizationDomainError):
+        q.quantize_tensor([1.0, float("nan")])
+    blocks, _ = q.quantize_tensor(gen.GOLDEN_FILE_INPUT)
+    p = tmp_path / "g.fp4"
+    q.write_blocks(blocks, 32, p)
+    assert hashlib.sha256(p.read_bytes()).hexdigest() == gen.GOLDEN_FILE_SHA256
+    back, count = q.read_blocks(p)
+    assert count == 32 and back == blocks
+    assert q.quantize_block(gen.ON_GRID) == blocks[0]
+    assert q.dequantize_block(blocks[0]) == gen.ON_GRID
+    assert blocks[0].scale == 1.0
+
+
+def test_dequantize_blocks_vs_oracle(q, golden):
+    d = np.load(golden / "fp4_regimes.npz")
+    got = q.dequantize_blocks(d["codes"], d["scale_bits"])
+    assert (got == oracle.dequantize_blocks(d["codes"], d["scale_bits"])).all()
+    # every (code, scale) pattern, including 0x7F (decodes to 480, fp4.py:59-66)
+    codes = np.tile(np.arange(16, dtype=np.uint8), (128, 1))
+    sb = np.arange(128, dtype=np.uint8)
+    assert (q.dequantize_blocks(codes, sb) == oracle.dequantize_blocks(codes, sb)).all()
+
+
+def test_weight_error_summary_bf16_weights(q):
+    """The accuracy proxy the bench reports for W4A4 ranks: bf16 N(0, 0.02) weights
+    through the device summary == the oracle's quantize_tensor on the same values."""
+    import torch
+
+    w = (torch.randn(256, 1408, generator=torch.Generator().manual_seed(4)) * 0.02).to(torch.bfloat16)
+    r = q.quantize_tensor_device(w.cuda())
+    torch.cuda.synchronize()
+    rec, rmse, rel, mr = oracle.quantize_tensor(w.float().numpy().astype(np.float64).reshape(-1))
+    assert (r["records"].cpu().numpy() == rec).all()
+    assert (r["max_rel"].cpu().numpy() == mr).all()
+    s = q.summary_from_sums(r["sums"], r["n"])
+    assert abs(s.relative_rmse - rel) <= 1e-12 * rel and abs(s.rmse - rmse) <= 1e-12 * rmse
+    assert 0.09 < s.relative_rmse < 0.12  # subnormal-scale regime (SURVEY §0: 0.103)
