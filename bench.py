@@ -447,6 +447,9 @@ def spawn_ranks(args) -> int:
         ngpu = 0
     if ngpu < args.gpus and "REALB_EP_COMM" not in env:
         env["REALB_EP_COMM"] = "auto-gloo"
+    # torchrun would pin OMP_NUM_THREADS=1, which caps the BLAS pool of rank 0's CPU
+    # baseline leg at one thread for the whole process: give it the host's threads
+    env.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
     # NCCL communicator set-up lines (NVLink / NVLS) on stderr, stdout stays one JSON line
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")

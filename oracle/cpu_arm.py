@@ -162,7 +162,17 @@ class CpuLayerArm:
         return {"us_per_layer": us, "what": f"aggregate_rank_loads + plan_realb, E={self.E}, R={self.R}",
                 "cores": 1}
 
+    def blas_threads(self) -> int:
+        try:
+            from threadpoolctl import threadpool_info
+
+            return max((int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas"),
+                       default=self.threads)
+        except Exception:  # noqa: BLE001
+            return self.threads
+
     def describe(self, value: float, kind: str = "port") -> dict:
+        self.threads = self.blas_threads()
         return {"value": value, "unit": "tokens/s", "cores": self.threads, "kind": kind,
                 "sample": f"{self.T} tokens of the {NAMES[self.config]} workload per step through the full CPU "
                           f"oracle layer (numpy fp32 GEMMs on {self.threads} BLAS threads), plan over R={self.R}",

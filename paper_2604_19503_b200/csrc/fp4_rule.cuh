@@ -235,6 +235,65 @@ __device__ __forceinline__ uint2 quant_block16_bf16vals(const float (&v)[16], ui
   return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
 }
 
+// ---------------------------------------------------------------------------
+// Packed-FP32 (FFMA2 / FMUL2, sm_100) form of quant_block16_bf16_tab: the same
+// q1 = q0 + (v - q0*sc) * r residual step, two elements per instruction.
+__device__ __forceinline__ uint64_t f32x2_pack(float lo, float hi) {
+  return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+// one bf16x2 word -> the f32x2 pair (lo element, hi element)
+__device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) {
+  return ((uint64_t)(w & 0xFFFF0000u) << 32) | (uint64_t)(w << 16);
+}
+__device__ __forceinline__ uint64_t q1_div2(uint64_t v, uint64_t r2, uint64_t nsc2) {
+  uint64_t q0, rho, q1;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q0) : "l"(v), "l"(r2));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rho) : "l"(q0), "l"(nsc2), "l"(v));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(q1) : "l"(rho), "l"(r2), "l"(q0));
+  return q1;
+}
+// two f32x2 quotients (4 elements, in order) -> 4 E2M1 codes in the low 16 bits
+__device__ __forceinline__ uint32_t cvt_e2m1x4_2(uint64_t a, uint64_t b) {
+  uint32_t out;
+  asm("{\n\t.reg .b8 b0, b1;\n\t.reg .f32 a0, a1, a2, a3;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\tmov.b64 {a2, a3}, %2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, a1, a0;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, a3, a2;\n\t"
+      "mov.b32 %0, {b0, b1, 0, 0};\n\t}"
+      : "=r"(out)
+      : "l"(a), "l"(b));
+  return out;
+}
+// E4M3 scale bits by the hardware conversion: cvt.rn.satfinite.e4m3x2.f32 is RNE
+// with subnormals and saturation at 448 (0x7E), i.e. encode_e4m3 (fp4.py:36-56)
+// for every non-negative finite input (checked over every bf16 amax,
+// tests/test_quant_gpu.py::test_all_bf16_amax_bf16_path); nonzero -> at least 1.
+__device__ __forceinline__ uint32_t block_scale_bits_bf16amax_hw(float amax) {
+  const float r6 = 0.16666667163372039794921875f;  // rn(1/6)
+  const float q0 = amax * r6;
+  const float q = fmaf(fmaf(-q0, 6.0f, amax), r6, q0);  // rn(amax / 6) for bf16 amax
+  uint16_t h;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %1;" : "=h"(h) : "f"(q));
+  const uint32_t b = h & 0xFFu;
+  return (b == 0u && amax > 0.0f) ? 1u : b;
+}
+
+__device__ __forceinline__ uint2 quant_block16_bf16_x2(const uint32_t (&w)[8], uint32_t& sbits,
+                                                       bool& nonfinite, const float2* tab) {
+  const uint32_t ab = amax_bits_bf16x16(w);
+  nonfinite = ab >= 0x7F80u;
+  sbits = block_scale_bits_bf16amax_hw(__uint_as_float(ab << 16));
+  if (sbits == 0u) return make_uint2(0u, 0u);
+  const float2 t = tab[sbits];
+  const uint64_t r2 = f32x2_pack(t.y, t.y), nsc2 = f32x2_pack(-t.x, -t.x);
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    c[i] = cvt_e2m1x4_2(q1_div2(bf16x2_to_f32x2(w[2 * i]), r2, nsc2),
+                        q1_div2(bf16x2_to_f32x2(w[2 * i + 1]), r2, nsc2));
+  return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
+}
+
 // byte offset of scale (row r, k-block kb) in the REALB_SF_MMA128x4 layout
 __host__ __device__ __forceinline__ int64_t sf_mma_offset(int64_t r, int64_t kb, int64_t nkb) {
   const int64_t atom = (r >> 7) * (nkb >> 2) + (kb >> 2);

@@ -7,6 +7,9 @@
 // as one contiguous, coalesced 512-byte run. Thread -> (row = b / 4,
 // kb = b % 4): four consecutive threads read one row's 128 contiguous input
 // bytes (bf16) and write its 32 contiguous code bytes.
+#include <cstdlib>
+#include <climits>
+
 #include "common.cuh"
 #include "fp4_rule.cuh"
 
@@ -138,6 +141,255 @@ __global__ void __launch_bounds__(256) quant_experts_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 (v2): persistent and register double-buffered. Tiles are 128 rows x 64
+// columns (one 512-B scale atom), enumerated group by group (an expert's rows
+// are a group; only the groups the device plan made W4A4, or all of them), k-tile
+// fastest; CTA c owns a CONTIGUOUS range of tiles and walks it incrementally (no
+// per-tile divisions). Thread -> (row = tid / 2, half = tid % 2): its 2 blocks are
+// 64 contiguous input bytes (4 x 16-B loads; a warp reads 16 full 128-B lines),
+// 16 contiguous code bytes (one 16-B store) and 2 adjacent scale bytes (one 16-bit
+// store into the atom). The NEXT tile's loads are issued before the current tile
+// is converted, so every thread keeps 64 B in flight through the conversion, and
+// the conversion runs two elements per instruction (FFMA2 / FMUL2).
+// one whole block (16 bf16 = one 32-B sector) per load: LDG.256 (sm_100), so no
+// sector is requested twice (16-B loads without L1 allocation split every sector
+// into two L2 requests)
+__device__ __forceinline__ void ldg_nc_v8(uint32_t (&v)[8], const void* p) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(256) quant_tiles_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
+                                                          int64_t cols, int mt_per_group, int G,
+                                                          const uint8_t* __restrict__ prec,
+                                                          uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
+                                                          int32_t* flag) {
+  __shared__ float2 tab[128];
+  __shared__ int s_list[256];
+  __shared__ int s_n;
+  sf_table_init(tab);
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int g = 0; g < G; ++g)
+      if (!prec || prec[g] == REALB_PREC_W4A4) s_list[n++] = g;
+    s_n = n;
+  }
+  __syncthreads();
+  const int64_t nkb = cols >> 4;
+  const int tiles_k = (int)(cols >> 6);
+  const int per_group = mt_per_group * tiles_k;
+  const int64_t tiles = (int64_t)s_n * per_group;
+  const int64_t q = tiles / gridDim.x, rem = tiles % gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * q + min((int64_t)blockIdx.x, rem);
+  const int64_t t1 = t0 + q + ((int64_t)blockIdx.x < rem ? 1 : 0);
+  if (t0 >= t1) return;
+  const int row_in = threadIdx.x >> 1, half = threadIdx.x & 1;
+  int g = (int)(t0 / per_group);
+  const int w0 = (int)(t0 - (int64_t)g * per_group);
+  int mt = w0 / tiles_k, kt = w0 - (w0 / tiles_k) * tiles_k;
+  auto row_of = [&](int gg, int mm) { return ((int64_t)s_list[gg] * mt_per_group + mm) * 128 + row_in; };
+  int64_t r = row_of(g, mt);
+  bool ok = r < rows;
+  uint32_t cur[2][8], nxt[2][8];
+  if (ok) {
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(x + r * cols + kt * 64 + half * 32);
+    ldg_nc_v8(cur[0], p);
+    ldg_nc_v8(cur[1], p + 32);
+  }
+  for (int64_t t = t0; t < t1; ++t) {
+    int g2 = g, mt2 = mt, kt2 = kt + 1;
+    if (kt2 == tiles_k) {
+      kt2 = 0;
+      if (++mt2 == mt_per_group) { mt2 = 0; ++g2; }
+    }
+    int64_t r2 = 0;
+    bool ok2 = false;
+    if (t + 1 < t1) {
+      r2 = row_of(g2, mt2);
+      ok2 = r2 < rows;
+      if (ok2) {
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(x + r2 * cols + kt2 * 64 + half * 32);
+        ldg_nc_v8(nxt[0], p);
+        ldg_nc_v8(nxt[1], p + 32);
+      }
+    }
+    if (ok) {
+      uint32_t sa, sb;
+      bool nfa, nfb;
+      const uint2 ca = quant_block16_bf16_x2(cur[0], sa, nfa, tab);
+      const uint2 cb = quant_block16_bf16_x2(cur[1], sb, nfb, tab);
+      if (nfa || nfb) flag_nonfinite(flag);
+      *reinterpret_cast<uint4*>(codes + r * (cols >> 1) + kt * 32 + half * 16) = make_uint4(ca.x, ca.y, cb.x, cb.y);
+      const int64_t kb0 = (int64_t)kt * 4 + half * 2;
+      const int64_t so = LAYOUT == REALB_SF_FLAT ? r * nkb + kb0 : sf_mma_offset(r, kb0, nkb);
+      *reinterpret_cast<uint16_t*>(sf + so) = (uint16_t)(sa | (sb << 8));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cur[0][i] = nxt[0][i];
+      cur[1][i] = nxt[1][i];
+    }
+    g = g2; mt = mt2; kt = kt2; r = r2; ok = ok2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 (v3): TMA-fed, full-row stages. One persistent CTA per SM. Warp 16 streams
+// the CTA's CONTIGUOUS range of 8-row slices of the weight matrix (8 whole rows
+// = one contiguous run of 8 x cols x 2 bytes, so every DRAM page is read in one
+// pass) into a 5-8-stage shared-memory ring with ONE cp.async.bulk.tensor per
+// stage: a 3-D box [64 columns] x [cols/64 k-tiles] x [8 rows], SWIZZLE_128B. Two
+// groups of 8 converter warps take alternate stages. Converter item (row r,
+// k-tile j) = one 128-B line of the stage: the 4 blocks of row r in k-tile j = one
+// row of one scale atom; a quarter-warp reads 8 consecutive lines (swizzled,
+// conflict-free); it writes 32 contiguous code bytes (one 32-B store; a warp writes
+// 1 KB contiguous) and the atom row's 4 scale bytes (one 32-bit store). No register cost
+// for the bytes in flight, no address arithmetic on the converting threads
+// beyond the item's row and column.
+constexpr int kQ3MaxStages = 8;
+constexpr int kQ3MaxCols = 2560;                    // 40 boxes: 40 KB per stage
+constexpr int kQ3RingBytes = 200 * 1024;            // stages = ring / stage bytes (5..8)
+constexpr int kQ3Threads = 544;  // 2 converter groups of 8 warps + the producer warp
+
+__device__ __forceinline__ void stg_v8(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kQ3Threads, 1) quant_tma_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                                  int64_t cols, int slices_per_group, int G,
+                                                                  const uint8_t* __restrict__ prec,
+                                                                  uint8_t* __restrict__ codes,
+                                                                  uint8_t* __restrict__ sf, int32_t* flag) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kQ3RingBytes);
+  uint64_t* empty = full + kQ3MaxStages;
+  float2* tab = reinterpret_cast<float2*>(empty + kQ3MaxStages);
+  int* s_list = reinterpret_cast<int*>(tab + 128);
+  int* s_n = s_list + 256;
+  const int64_t nkb = cols >> 4;
+  const int nbox = (int)(cols >> 6);
+  const uint32_t stage_bytes = (uint32_t)nbox * 1024u;
+  const int kQ3Stages = min(kQ3MaxStages, (int)(kQ3RingBytes / stage_bytes));
+  const uint32_t kQ3StageBytes = stage_bytes;
+  sf_table_init(tab);
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int g = 0; g < G; ++g)
+      if (!prec || prec[g] == REALB_PREC_W4A4) s_list[n++] = g;
+    *s_n = n;
+    for (int i = 0; i < kQ3Stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t slices = (int64_t)(*s_n) * slices_per_group;
+  const int64_t q = slices / gridDim.x, rem = slices % gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * q + min((int64_t)blockIdx.x, rem);
+  const int n_t = (int)(q + ((int64_t)blockIdx.x < rem ? 1 : 0));
+  if (n_t <= 0) return;
+  const int warp = threadIdx.x >> 5;
+  auto row0_of = [&](int i) -> int64_t {  // first row of this CTA's slice i
+    const int64_t t = t0 + i;
+    const int g = (int)(t / slices_per_group);
+    return ((int64_t)s_list[g] * slices_per_group + (t - (int64_t)g * slices_per_group)) * 8;
+  };
+  if (warp == 16) {  // ------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch_desc(&tmx);
+      for (int i = 0; i < n_t; ++i) {
+        const int stage = i % kQ3Stages;
+        mbar_wait(&empty[stage], ((i / kQ3Stages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[stage], stage_bytes);
+        const int row0 = (int)row0_of(i);
+        // one 3-D box per stage: [64 columns] x [cols/64 k-tiles] x [8 rows]
+        tma_load_3d(smem + stage * kQ3StageBytes, &tmx, &full[stage], 0, 0, row0);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ converters
+  const int cg = warp >> 3, tt = threadIdx.x & 255;
+  bool nonfinite = false;
+  for (int i = cg; i < n_t; i += 2) {
+    const int stage = i % kQ3Stages;
+    const int64_t row0 = row0_of(i);
+    mbar_wait(&full[stage], (i / kQ3Stages) & 1);
+    const uint32_t sbase = smem_u32(smem + stage * kQ3StageBytes);
+    for (int L = tt; L < nbox * 8; L += 256) {
+      // 128-B line L of the stage = (row r_in, k-tile j); a quarter-warp reads 8
+      // consecutive lines, whose swizzled chunks hit 8 distinct bank groups
+      const int r_in = L / nbox, j = L - r_in * nbox;
+      const uint32_t rowbase = sbase + (uint32_t)L * 128u;
+      uint32_t w[4][8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = ld_shared_v4(rowbase + ((uint32_t)(c ^ (L & 7)) << 4));
+        w[c >> 1][(c & 1) * 4 + 0] = v.x;
+        w[c >> 1][(c & 1) * 4 + 1] = v.y;
+        w[c >> 1][(c & 1) * 4 + 2] = v.z;
+        w[c >> 1][(c & 1) * 4 + 3] = v.w;
+      }
+      uint32_t cw[8], sw = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t sb;
+        bool nf;
+        const uint2 c = quant_block16_bf16_x2(w[b], sb, nf, tab);
+        nonfinite |= nf;
+        cw[2 * b] = c.x;
+        cw[2 * b + 1] = c.y;
+        sw |= sb << (8 * b);
+      }
+      const int64_t r = row0 + r_in;
+      stg_v8(codes + r * (cols >> 1) + (int64_t)j * 32, cw);
+      *reinterpret_cast<uint32_t*>(sf + sf_mma_offset(r, (int64_t)j * 4, nkb)) = sw;
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+  }
+  if (nonfinite) flag_nonfinite(flag);
+}
+
+// v3 launch over a [groups x rows_per_group, cols] bf16 matrix (rows_per_group % 8 == 0,
+// cols % 64 == 0, cols <= kQ3MaxCols)
+static int launch_quant_tma(const void* x, int64_t rows, int64_t cols, int64_t rows_per_group, int G,
+                            const uint8_t* prec, uint8_t* codes, uint8_t* sf, int32_t* flag, int max_ctas,
+                            cudaStream_t st) {
+  CUtensorMap tm;
+  const uint64_t dims[3] = {64, (uint64_t)cols / 64, (uint64_t)rows};
+  const uint64_t strides[2] = {128, (uint64_t)cols * 2};
+  const uint32_t box[3] = {64, (uint32_t)(cols / 64), 8};
+  int rc = make_tmap_3d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  constexpr int smem = kQ3RingBytes + 2 * kQ3MaxStages * 8 + 128 * 8 + 257 * 4 + 1024;
+  static_assert(smem <= 227 * 1024, "K3 v3 shared memory");
+  rc = set_smem_once(reinterpret_cast<const void*>(quant_tma_kernel), smem, "quant_tma_kernel: smem attribute");
+  if (rc) return rc;
+  int grid = num_sms();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  quant_tma_kernel<<<grid, kQ3Threads, smem, st>>>(tm, cols, (int)(rows_per_group / 8), G, prec, codes, sf, flag);
+  return check_launch("realb_quantize (K3 v3)");
+}
+
+// K3 form (REALB_K3_VERSION, for A/B runs; scripts/bench_quant.py). Measured on the
+// EP8 hot rank's Kimi weights (ncu, gate_up / down): v1 30.6 / 19.3 us, v2 27.1 / 17.8,
+// v3 26.8 / 20.6 -> v2 is the default (K3).
+static int k3_version() {
+  const char* e = getenv("REALB_K3_VERSION");
+  if (e && (e[0] == '1' || e[0] == '2' || e[0] == '3')) return e[0] - '0';
+  return 2;
+}
+
+static bool k3_v1() { return k3_version() == 1; }
+
 // resident CTAs per SM x SMs (no partial last wave); capped by the work
 static int quant_grid(const void* kern, int64_t tiles, int max_ctas) {
   int per_sm = 0;
@@ -266,6 +518,17 @@ extern "C" int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, in
   const bool flat = sf_layout == REALB_SF_FLAT;
   switch (dtype) {
     case REALB_DT_BF16:
+      if (!flat && cols % 64 == 0 && cols <= kQ3MaxCols && rows % 128 == 0 && k3_version() == 3 &&
+          rows / 8 <= INT32_MAX)
+        return launch_quant_tma(d_x, rows, cols, rows, 1, nullptr, d_codes, d_sf, d_flag, max_ctas, st);
+      if (cols % 64 == 0 && !k3_v1() && (rows + 127) / 128 <= INT32_MAX / 64) {
+        const int64_t mt = (rows + 127) / 128;
+        auto kern = flat ? quant_tiles_kernel<REALB_SF_FLAT> : quant_tiles_kernel<REALB_SF_MMA128x4>;
+        const int grid = quant_grid(reinterpret_cast<const void*>(kern), mt * (cols / 64), max_ctas);
+        kern<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(d_x), rows, cols, (int)mt, 1, nullptr,
+                                   d_codes, d_sf, d_flag);
+        return check_launch("realb_quantize_nvfp4");
+      }
       return flat ? launch_quant(quant_kernel_bf16<REALB_SF_FLAT>, d_x, rows, cols, d_codes,
                                  d_sf, d_flag, max_ctas, st)
                   : launch_quant(quant_kernel_bf16<REALB_SF_MMA128x4>, d_x, rows, cols, d_codes,
@@ -295,6 +558,18 @@ extern "C" int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows
     set_error("realb_quantize_experts_nvfp4: bad arguments (E=%d rows/expert=%lld cols=%lld)", E,
               (long long)rows_per_expert, (long long)cols);
     return REALB_EINVAL;
+  }
+  if (cols <= kQ3MaxCols && k3_version() == 3 && rows_per_expert / 8 <= INT32_MAX)
+    return launch_quant_tma(d_w, (int64_t)E * rows_per_expert, cols, rows_per_expert, E, d_expert_prec, d_codes,
+                            d_sf, d_flag, max_ctas, (cudaStream_t)stream);
+  if (!k3_v1()) {
+    auto kern = quant_tiles_kernel<REALB_SF_MMA128x4>;
+    const int grid = quant_grid(reinterpret_cast<const void*>(kern),
+                               (int64_t)E * (rows_per_expert / 128) * (cols / 64), max_ctas);
+    kern<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(d_w),
+                                                 (int64_t)E * rows_per_expert, cols, (int)(rows_per_expert / 128), E,
+                                                 d_expert_prec, d_codes, d_sf, d_flag);
+    return check_launch("realb_quantize_experts_nvfp4");
   }
   const int grid = quant_grid(reinterpret_cast<const void*>(quant_experts_kernel),
                              (int64_t)E * (rows_per_expert / 128) * (cols / 64), max_ctas);

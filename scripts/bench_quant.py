@@ -1,50 +1,90 @@
-"""K3 microbenchmark: the hot rank's expert weights (Kimi EP8: 8 experts gate_up + down)
-through realb_quantize_experts_nvfp4, L2 flushed between launches; achieved HBM GB/s
-on the algorithmic bytes (2 B read + 0.5625 B written per weight)."""
-import os, sys, json
+"""K3 microbenchmark: the hot rank's expert weights (Kimi EP8: 8 W4A4 experts'
+gate_up + down) through realb_quantize_experts_nvfp4, L2 flushed between
+launches, v1 / v2 / v3 (REALB_K3_VERSION) interleaved; achieved HBM GB/s on the
+algorithmic bytes (2 B read + 0.5625 B written per weight) against two device
+copies timed the same way: the same weights (read + write 2 B/weight) and a
+copy moving the same total bytes as K3 (the "same-size copy")."""
+import json
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-from paper_2604_19503_b200 import _lib
+import torch  # noqa: E402
+
+from paper_2604_19503_b200 import _lib  # noqa: E402
+
 E, H, I = 64, 2048, 1408
 wgu = (torch.randn(E * 2 * I, H, device="cuda") * 0.02).to(torch.bfloat16)
 wd = (torch.randn(E * H, I, device="cuda") * 0.02).to(torch.bfloat16)
-prec = torch.zeros(E, dtype=torch.uint8, device="cuda"); prec[56:] = 1
-cg = torch.empty(E * 2 * I, H // 2, dtype=torch.uint8, device="cuda"); sg = torch.empty(E * 2 * I * H // 16, dtype=torch.uint8, device="cuda")
-cd = torch.empty(E * H, I // 2, dtype=torch.uint8, device="cuda"); sd = torch.empty(E * H * I // 16, dtype=torch.uint8, device="cuda")
+prec = torch.zeros(E, dtype=torch.uint8, device="cuda")
+prec[56:] = 1
+cg = torch.empty(E * 2 * I, H // 2, dtype=torch.uint8, device="cuda")
+sg = torch.empty(E * 2 * I * H // 16, dtype=torch.uint8, device="cuda")
+cd = torch.empty(E * H, I // 2, dtype=torch.uint8, device="cuda")
+sd = torch.empty(E * H * I // 16, dtype=torch.uint8, device="cuda")
 flag = torch.zeros(1, dtype=torch.int32, device="cuda")
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+
+def l2_flush():
+    # read-only pass over 256 MB: L2 ends up holding CLEAN lines, so the timed kernel
+    # pays no write-back of a previous flush's dirty lines (a zero_() flush leaves
+    # ~126 MB dirty, written back inside the next timed launch)
+    flush.sum()
+
+
+def timed(f, reps=30):
+    for _ in range(3):
+        f()
+    ts = []
+    for _ in range(reps):
+        l2_flush()
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record()
+        f()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sorted(ts)[reps // 2] / 1e3
+
+
 out = {}
-for legacy in (False,):
-  for name, w, rpe, cols, c, s in (("gate_up", wgu, 2 * I, H, cg, sg), ("down", wd, H, I, cd, sd)):
-      name = "k3_" + name
-      f = lambda: _lib.call("realb_quantize_experts_nvfp4", w.data_ptr(), E, rpe, cols, prec.data_ptr(), c.data_ptr(),
-                            s.data_ptr(), flag.data_ptr(), 0, _lib.stream_ptr())
-      for _ in range(3): f()
-      ts = []
-      for _ in range(20):
-          flush.zero_()
-          a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-          a.record(); f(); b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
-      t = sorted(ts)[10] / 1e3
-      nbytes = 8 * rpe * cols * 2.5625
-      out[name] = dict(us=t * 1e6, GBps=nbytes / t / 1e9)
-print(json.dumps(out))
-# reference: a plain device copy of the same hot-rank weights (read + write), same flushing
+shapes = (("gate_up", wgu, 2 * I, H, cg, sg), ("down", wd, H, I, cd, sd))
+VERS = ("v1", "v2", "v3")
+res = {v: {n: [] for n, *_ in shapes} for v in VERS}
+for rnd in range(5):
+    for ver in VERS:
+        os.environ["REALB_K3_VERSION"] = ver[1]
+        for name, w, rpe, cols, c, s in shapes:
+            f = lambda: _lib.call("realb_quantize_experts_nvfp4", w.data_ptr(), E, rpe, cols, prec.data_ptr(),
+                                  c.data_ptr(), s.data_ptr(), flag.data_ptr(), 0, _lib.stream_ptr())
+            res[ver][name].append(timed(f, 11))
+os.environ.pop("REALB_K3_VERSION")
+for ver in res:
+    for name, w, rpe, cols, c, s in shapes:
+        t = sorted(res[ver][name])[2]
+        nbytes = 8 * rpe * cols * 2.5625
+        out[f"k3_{ver}_{name}"] = dict(us=t * 1e6, GBps=nbytes / t / 1e9, algorithmic_bytes=nbytes)
+# references: copies timed the same way
 src = wgu[56 * 2 * I:]
 dst = torch.empty_like(src)
-for _ in range(3): dst.copy_(src)
-ts = []
-for _ in range(20):
-    flush.zero_()
-    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-    a.record(); dst.copy_(src); b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
-t = sorted(ts)[10] / 1e3
-print(json.dumps({"torch_copy_gate_up_hot": dict(us=t * 1e6, GBps=2 * src.numel() * 2 / t / 1e9)}))
-# read-only reduction of the same bytes (a read-bound reference)
-ts = []
-for _ in range(20):
-    flush.zero_()
-    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-    a.record(); src.view(torch.int16).max(); b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
-t = sorted(ts)[10] / 1e3
-print(json.dumps({"torch_max_gate_up_hot": dict(us=t * 1e6, GBps=src.numel() * 2 / t / 1e9)}))
+t = timed(lambda: dst.copy_(src))
+out["torch_copy_gate_up_hot"] = dict(us=t * 1e6, GBps=2 * src.numel() * 2 / t / 1e9)
+nb = int(8 * 2 * I * H * 2.5625) // 2  # same total bytes as K3's gate_up: half read, half written
+a8 = torch.empty(nb, dtype=torch.uint8, device="cuda")
+b8 = torch.empty_like(a8)
+t = timed(lambda: b8.copy_(a8))
+out["same_size_copy_gate_up"] = dict(us=t * 1e6, GBps=2 * nb / t / 1e9)
+for ver in VERS:
+    out[f"k3_{ver}_gate_up"]["frac_of_same_size_copy"] = out["same_size_copy_gate_up"]["us"] / out[f"k3_{ver}_gate_up"]["us"]
+# parity spot check v1 == v2 (bit-exact codes / scales)
+outs = []
+for ver in VERS:
+    os.environ["REALB_K3_VERSION"] = ver[1]
+    cg.zero_()
+    sg.zero_()
+    _lib.call("realb_quantize_experts_nvfp4", wgu.data_ptr(), E, 2 * I, H, prec.data_ptr(), cg.data_ptr(),
+              sg.data_ptr(), flag.data_ptr(), 0, _lib.stream_ptr())
+    outs.append((cg.clone(), sg.clone()))
+out["all_versions_equal"] = all(torch.equal(outs[0][0], o[0]) and torch.equal(outs[0][1], o[1]) for o in outs[1:])
+print(json.dumps(out, indent=1))
