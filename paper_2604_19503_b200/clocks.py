@@ -21,9 +21,19 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-# dense NVFP4 reference peak measured on this B200 pool: cuBLASLt torch._scaled_mm
-# 8192^3 block-scaled NVFP4 (scripts/bench_fp4.py; MEASURED_PEAKS.json has no FP4 entry)
-FP4_TFLOPS_MEASURED = 5950.0
+def fp4_peaks():
+    """Dense NVFP4 peak measured on this B200 pool (MEASURED_PEAKS.json has no FP4
+    entry): cuBLASLt block-scaled NVFP4 8192^3 (scripts/measure_fp4_peak.py ->
+    profiles/r02/fp4_peak.json), burst and sustained, with the clocks they ran at.
+    -> (burst TFLOP/s, sustained TFLOP/s, source)."""
+    f = ROOT / "profiles" / "r02" / "fp4_peak.json"
+    if f.exists():
+        d = json.loads(f.read_text())["nvfp4"]
+        return float(d["burst_tflops"]), float(d["sustained_tflops"]), "profiles/r02/fp4_peak.json (measured)"
+    return 5950.0, 5950.0, "round-1 constant (scripts/bench_fp4.py)"
+
+
+FP4_TFLOPS_MEASURED = fp4_peaks()[0]
 
 
 class ClockSampler:
