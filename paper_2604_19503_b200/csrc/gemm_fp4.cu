@@ -43,17 +43,20 @@ constexpr int kF4Threads = 384;
 constexpr int kSfBoxRows = 8;             // scale TMA box: 8 x 256 B = 2 KB = 4 atoms
 constexpr int kF4EpiBufs = 3;             // TMA-store staging buffers per epilogue warp (STORE)
 
-template <int EPI, int CL>
+// XST (experiment): 4 operand stages and NO epilogue staging for the STORE kernel,
+// valid only with the epilogue stores skipped (REALB_DBG_FP4 bit 1): measures how
+// much of the down GEMM is the operand feed of a 3-stage ring (K6)
+template <int EPI, int CL, int XST = 0>
 struct SmemFp4 {
-  // STORE (bf16 out) needs 32 KB of TMA-store staging
-  static constexpr int STAGES = CL == 1 ? (EPI != REALB_EPI_SWIGLU ? 3 : 4) : (EPI != REALB_EPI_SWIGLU ? 4 : 5);
+  // STORE (bf16 out) needs 48 KB of TMA-store staging
+  static constexpr int STAGES = XST ? XST : CL == 1 ? (EPI != REALB_EPI_SWIGLU ? 3 : 4) : (EPI != REALB_EPI_SWIGLU ? 4 : 5);
   static constexpr int A_BYTES = kF4BM * kF4BKB;              // 16 KB
   static constexpr int B_BYTES = (kF4BN / CL) * kF4BKB;       // 32 KB (16 KB per CTA of a pair)
   static constexpr int SFA_BYTES = 4 * 512;                   // 128 rows x 16 scales
   static constexpr int SFB_BYTES = 2 * 4 * 512;               // 256 rows x 16 scales (full W tile)
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
   static constexpr int EPI_OFF = STAGES * STAGE;    // 8 warps x kF4EpiBufs x 2 KB (STORE only)
-  static constexpr int EPI_BYTES = EPI != REALB_EPI_SWIGLU ? 8 * kF4EpiBufs * 2048 : 0;
+  static constexpr int EPI_BYTES = (EPI != REALB_EPI_SWIGLU && !XST) ? 8 * kF4EpiBufs * 2048 : 0;
   static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -84,14 +87,14 @@ __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr, uint32_t lbo, uint32
   return d;
 }
 
-template <int EPI, int CL>
+template <int EPI, int CL, int XST = 0>
 __global__ void __launch_bounds__(kF4Threads, 1)
     grouped_gemm_fp4_kernel(const __grid_constant__ CUtensorMap tmA,
                             const __grid_constant__ CUtensorMap tmB,
                             const __grid_constant__ CUtensorMap tmSfa,
                             const __grid_constant__ CUtensorMap tmSfb,
                             const __grid_constant__ CUtensorMap tmOut, const Fp4Args args) {
-  using S = SmemFp4<EPI, CL>;
+  using S = SmemFp4<EPI, CL, XST>;
   constexpr int kF4Stages = S::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -480,7 +483,7 @@ static int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int K) {
                       CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-template <int EPI, int CL>
+template <int EPI, int CL, int XST = 0>
 static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, const uint8_t* w_sf,
                       int64_t rows_cap, int N, int K, int E, const int32_t* layout, void* out,
                       uint8_t* out_codes, uint8_t* out_sf, int max_ctas, cudaStream_t st,
@@ -517,8 +520,8 @@ static int launch_fp4(const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, c
   args.sf_sbo = env_u32("REALB_DBG_SF_SBO", 128);
   args.dbg = env_u32("REALB_DBG_FP4", 0);
   args.scat = scat ? *scat : RowScatter{};
-  auto kern = grouped_gemm_fp4_kernel<EPI, CL>;
-  const int smem = SmemFp4<EPI, CL>::TOTAL;
+  auto kern = grouped_gemm_fp4_kernel<EPI, CL, XST>;
+  const int smem = SmemFp4<EPI, CL, XST>::TOTAL;
   rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "grouped_gemm_nvfp4: smem attribute");
   if (rc) return rc;
   int grid = num_sms();
@@ -572,6 +575,15 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
   const bool pair = cl_env && cl_env[0] == '2';
   if (epilogue == REALB_EPI_STORE) {
     if (!d_out) { set_error("realb_grouped_gemm_nvfp4: STORE needs d_out"); return REALB_EINVAL; }
+    const char* xst = getenv("REALB_DBG_FP4_STORE4");
+    if (xst && xst[0] == '1' && !pair) {
+      if (!(env_u32("REALB_DBG_FP4", 0) & 1u)) {
+        set_error("REALB_DBG_FP4_STORE4 is an experiment: it needs REALB_DBG_FP4 bit 1 (no epilogue stores)");
+        return REALB_EINVAL;
+      }
+      return launch_fp4<REALB_EPI_STORE, 1, 4>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E, d_layout,
+                                               d_out, nullptr, nullptr, max_ctas, st);
+    }
     return pair ? launch_fp4<REALB_EPI_STORE, 2>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
                                                  d_layout, d_out, nullptr, nullptr, max_ctas, st)
                 : launch_fp4<REALB_EPI_STORE, 1>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,

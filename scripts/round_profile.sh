@@ -15,9 +15,10 @@ timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > "$O/referen
 # launch list (cold cache, serialised): kernel shares of the step
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file "$O/launches.csv" python bench.py --steps 2 --warmup 1 --no-virtual-ep --no-cpu-baseline \
+  --sustained-steps 0 \
   > "$O/launches_bench.log" 2>&1
 # full captures: the bench layer's K5 gate_up (the roofline kernel) and down, router, dispatch, combine
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"grouped_gemm_bf16|router|combine|gather|permute" \
-  -c 6 -o "$O/layer_full" python bench.py --steps 1 --warmup 1 --no-virtual-ep --no-cpu-baseline \
+  -c 6 -o "$O/layer_full" python bench.py --steps 1 --warmup 1 --no-virtual-ep --no-cpu-baseline --sustained-steps 0 \
   > "$O/layer_full.log" 2>&1
 echo done
