@@ -120,7 +120,8 @@ def run_ours(args):
     light = ("gate_up_start", "gate_up_end")
     timers = [GraphMarks(torch, only=light) for _ in range(NS)]
     g_realbs = [layer.capture(x, mod, "realb", params, timer=tm) for tm in timers]
-    g_bf16 = layer.capture(x, mod, "baseline", timer=GraphMarks(torch, only=light))
+    bf16_timer = GraphMarks(torch, only=light)  # kept alive: the graph's event-record nodes use its events
+    g_bf16 = layer.capture(x, mod, "baseline", timer=bf16_timer)
     rr = {"i": 0}
 
     def step_realb():
@@ -167,7 +168,6 @@ def run_ours(args):
              "gate_up": ("gate_up_start", "gate_up_end"), "down": ("down_start", "down_end"),
              "combine": ("down_end", "combine_end")}
     step_phases = {k: float(np.mean([tm.ms(a, b) for tm in ptimers])) for k, (a, b) in spans.items()}
-    del g_ph
     # --- roofline of the dominant kernel (K5 gate_up grouped GEMM), events on its stream
     roof = roofline_gate_up(torch, layer, x, mod, shape, args, gate_up_live_ms, ms)
     # --- SURVEY §8(d) layer roofline: t_roof = max_r F_r / Peak(plan_r), F_r = pairs_r * 6HI
