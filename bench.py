@@ -31,7 +31,10 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="kimi", choices=["tiny", "kimi", "kimi_shared", "qwen", "ernie_vision"])
+    p.add_argument("--config", default="kimi",
+                   choices=["tiny", "kimi", "kimi_shared", "qwen", "ernie_vision", "ernie_split"],
+                   help="ernie_split: BASELINE configs[3], ERNIE-4.5-VL's text group (W16A16) + vision group "
+                        "(ReaLB, modality-isolated) on one token batch")
     p.add_argument("--tokens", type=int, default=8192, help="local tokens per GPU")
     p.add_argument("--vision-frac", type=float, default=0.7)
     p.add_argument("--cpu-sample-tokens", type=int, default=1024,
@@ -92,6 +95,8 @@ def run_ours(args):
     from paper_2604_19503_b200.policy import RealbParams
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config == "ernie_split":
+        return run_split(args, world)
     if world > 1:
         from paper_2604_19503_b200 import ep
 
@@ -241,6 +246,201 @@ def run_ours(args):
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, sample=args.cpu_sample_tokens)
     print(json.dumps(out), flush=True)
+
+
+def run_split(args, world: int):
+    """BASELINE configs[3]: the ERNIE-4.5-VL modality-split MoE layer. Text tokens go
+    through the text group (64 experts, I = 1536, W16A16), vision tokens through the
+    vision group (64 experts, I = 512) under the modality-isolated ReaLB policy
+    (balancers.py:105-106). N = 1: moe.ModalitySplitMoELayer (the split is boolean
+    indexing on the token-type mask, a host sync, as in the model), eager, CUDA
+    events. N > 1: two expert-parallel layers (ep.EPMoELayer, NCCL path) over the
+    rank's text and vision tokens, max over ranks."""
+    import numpy as np
+    import torch
+
+    from paper_2604_19503_b200.clocks import ClockSampler, measured_peaks
+    from paper_2604_19503_b200.moe import SHAPES, ModalitySplitMoELayer, MoELayer, MoEWeights
+    from paper_2604_19503_b200.policy import ClusterConfig, RealbParams
+    from paper_2604_19503_b200.workload import WorkloadSpec, make_experts, make_split_batch
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    st, sv = SHAPES["ernie_text"], SHAPES["ernie_vision"]
+    T = args.tokens
+    if world > 1:
+        import torch.distributed as dist
+
+        staged = torch.cuda.device_count() < world
+        torch.cuda.set_device(0 if staged else local)
+        if staged:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    x, mod, rt, rv, _, _ = make_split_batch(st, sv, WorkloadSpec(tokens=T, vision_frac=args.vision_frac,
+                                                                 num_ranks=8, rank=rank))
+    gt, dt = make_experts(st, seed=11)
+    gv, dv = make_experts(sv, seed=12)
+    params = RealbParams()
+    vis = mod.bool()
+    n_vis = int(vis.sum())
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    flush = (lambda: None) if args.no_l2_flush else (lambda: flush_buf.zero_())
+    marks = {}
+
+    class Marks:  # gate_up events of the text group (the dominant launch), eager
+        def mark(self, name, stream=None):
+            if name in ("gate_up_start", "gate_up_end"):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks[name] = e
+
+    if world == 1:
+        cl = lambda iso: ClusterConfig(1, 1, 64, 1, iso)  # R = 1, as the main bench: plan inactive
+        text = MoELayer(MoEWeights.from_hf(st, rt, gt, dt), max_tokens=T - n_vis, cluster=cl(False))
+        vision = MoELayer(MoEWeights.from_hf(sv, rv, gv, dv), max_tokens=n_vis, cluster=cl(True))
+        layer = ModalitySplitMoELayer(text, vision)
+
+        def step(strategy="realb", timer=None):
+            it = (~vis).nonzero().squeeze(1)
+            iv = vis.nonzero().squeeze(1)
+            y = torch.empty_like(x)
+            rt_ = text.forward(x.index_select(0, it), mod.index_select(0, it), "baseline", timer=timer)
+            y.index_copy_(0, it, rt_.y)
+            rv_ = vision.forward(x.index_select(0, iv), mod.index_select(0, iv), strategy, params)
+            y.index_copy_(0, iv, rv_.y)
+            return y, rt_, rv_
+    else:
+        from paper_2604_19503_b200.ep import CudaEPOps, EPComm, EPMoELayer, split_weights
+
+        comm = EPComm(staged=torch.cuda.device_count() < world)
+        nt_max = T - int(vis.sum())
+        layers = {}
+        for name, shape, router, gu, dn, n in (("text", st, rt, gt, dt, T - n_vis), ("vision", sv, rv, gv, dv, n_vis)):
+            loc = split_weights(shape, router, gu, dn, rank, world)
+            ops = CudaEPOps(shape, router.contiguous(), None, loc, world, max(n, 1) * 2)
+            layers[name] = EPMoELayer(shape, comm, ops, fp4_dispatch=True)
+        del nt_max
+
+        def step(strategy="realb", timer=None):
+            it = (~vis).nonzero().squeeze(1)
+            iv = vis.nonzero().squeeze(1)
+            y = torch.empty_like(x)
+            yt, _, _ = layers["text"].forward(x.index_select(0, it).contiguous(), mod.index_select(0, it), "baseline",
+                                              timer=timer)
+            y.index_copy_(0, it, yt)
+            yv, plan_v, _ = layers["vision"].forward(x.index_select(0, iv).contiguous(), mod.index_select(0, iv),
+                                                     strategy, params)
+            y.index_copy_(0, iv, yv)
+            return y, None, plan_v
+
+    def timed(strategy, steps, warmup, timer=None):
+        for _ in range(warmup):
+            step(strategy)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            step(strategy, timer)
+            b.record()
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in ts]))
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda" if not comm.staged else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    from paper_2604_19503_b200 import _lib
+
+    step("realb")
+    torch.cuda.synchronize()
+    _lib.launch_count = 0
+    step("realb")
+    launches = _lib.launch_count
+    with ClockSampler(0 if world == 1 else local) as clk:
+        ms = timed("realb", args.steps, args.warmup, timer=Marks())
+    if world == 1:
+        gate_up_ms = marks["gate_up_start"].elapsed_time(marks["gate_up_end"])
+        gu_timing = "CUDA events around the launch in the last timed step"
+    else:  # the text group's local gate_up over this rank's received rows, timed after the run
+        step("realb")
+        torch.cuda.synchronize()
+        gate_up_ms, F_gu, _ = layers["text"].ops.time_gate_up()
+        gu_timing = "the text group's local gate_up launch re-timed after the run (median of 5)"
+    rounds = {"realb": [], "bf16": []}
+    for _ in range(3):
+        rounds["realb"].append(timed("realb", max(2, args.steps // 3), 1))
+        rounds["bf16"].append(timed("baseline", max(2, args.steps // 3), 1))
+    # e2e through the public call with host buffers: H2D of x / modality, D2H of y
+    xh, mh = x.cpu().pin_memory(), mod.cpu().pin_memory()
+    yh = torch.empty(T, x.shape[1], dtype=torch.bfloat16).pin_memory()
+    xd, md = torch.empty_like(x), torch.empty_like(mod)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        md.copy_(mh, non_blocking=True)
+        x.copy_(xd)
+        mod.copy_(md)
+        y, _, _ = step("realb")
+        yh.copy_(y, non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    ms_e2e = a.elapsed_time(b) / args.steps
+    _, _, res_v = step("realb")
+    torch.cuda.synchronize()
+    peaks, src = measured_peaks()
+    n_text = T - n_vis
+    F_text = float(n_text * st.top_k) * 2 * (2 * st.intermediate) * st.hidden  # gate_up flops of the text group
+    if world == 1:
+        F_gu = F_text
+    F = float(n_text * st.top_k) * 6 * st.hidden * st.intermediate + float(n_vis * sv.top_k) * 6 * sv.hidden * sv.intermediate
+    peak = float(peaks.get("bf16_tflops", 1641.1))
+    if rank == 0:
+        plan_v = res_v.plan if world == 1 else res_v
+        out = {"metric": METRIC, "value": world * T / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "bf16 (nvfp4 on W4A4 vision ranks)",
+               "data": "synthetic",
+               "config": {"workload": f"ernie-4.5-vl-a3b modality-split MoE layer prefill, {T} tokens/GPU, "
+                                      f"{args.vision_frac:.0%} vision: text group E=64 I=1536, vision group E=64 "
+                                      f"I=512, top-6, H=2560", "strategy": "realb (vision group, modality-isolated)",
+                          "ep_ranks": world, "tokens_per_gpu": T,
+                          "l2": "flushed between timed steps (256 MB write, untimed)",
+                          "execution": "eager (the modality split is a host-synchronising boolean index, as in the "
+                                       "model); " + ("one GPU (R = 1: the plan is inactive)" if world == 1 else
+                                                     "two EP layers (text / vision tokens), NCCL path")},
+               "speedup_vs_bf16": float(np.sum(rounds["bf16"]) / np.sum(rounds["realb"])),
+               "speedup_timing": "3 interleaved rounds of realb / all-BF16 steps (ratio of sums)",
+               "plan_w4a4_vision_ranks": sorted(plan_v.accelerated_ranks),
+               "e2e": {"value": world * T / (ms_e2e / 1e3), "unit": "tokens/s",
+                       "h2d_bytes_per_step": int(world * (x.numel() * 2 + mod.numel())),
+                       "d2h_bytes_per_step": int(world * T * x.shape[1] * 2), "pipeline": "serial per step"},
+               "roofline": {"kernel": "realb_grouped_gemm_bf16 (text-group K5 gate_up, SwiGLU epilogue)",
+                            "bound": "tensor", "achieved": F_gu / (gate_up_ms / 1e3) / 1e12, "peak": peak,
+                            "unit": "TFLOP/s", "frac": F_gu / (gate_up_ms / 1e3) / 1e12 / peak, "traffic": None,
+                            "peak_source": f"{src} bf16_tflops (burst)", "launch_ms": gate_up_ms,
+                            "launch_timing": gu_timing,
+                            "layer": {"t_roof_ms": F / (peak * 1e12) * 1e3, "t_meas_ms": ms,
+                                      "frac": F / (peak * 1e12) * 1e3 / ms}},
+               "clocks": clk.summary(), "gpu_launches": int(launches * args.steps)}
+        if not args.no_cpu_baseline and world == 1:
+            out["cpu_baseline"] = {"skipped": "no CPU arm for the split layer; the vision / text groups' CPU "
+                                              "baseline is --config ernie_vision"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
 
 
 def run_e2e(torch, layer, x, mod, params, args):
