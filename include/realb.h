@@ -335,6 +335,28 @@ REALB_API int realb_p2p_pack_direct(const void* d_x, const int32_t* d_topk_idx, 
                                     const void* d_plan, int32_t* d_pair_pos, int32_t* d_nonfinite_flag,
                                     void* stream);
 
+/* Rank-partial return. realb_p2p_pack_direct_partial is
+ * realb_p2p_pack_direct plus, for every row bound for a W4A4 owner d (device
+ * plan), the grouped row g in d's unit table h_peer_units[d] (int32
+ * [R][ustride][k], entry (me, t, j); -1 = no row) and the routing weight
+ * d_topk_w[t][j] in h_peer_wts[d][g] (fp32 [rows_cap]). After its down GEMM has
+ * stored its W4A4 rows locally (d_rows, grouped order), a W4A4 owner calls
+ * realb_p2p_partial_return: per (source s, token t) with rows here, the fma chain
+ * over t's slots in order, rounded once to bf16, goes to row unit_base + me *
+ * ustride + t of s's return window (h_ret_bases[s]); the unit table is reset to
+ * -1 behind it. A W16A16 owner's call is a no-op. The source then combines with
+ * realb_combine_partial(unit_base, ustride). */
+REALB_API int realb_p2p_pack_direct_partial(const void* d_x, const int32_t* d_topk_idx, const float* d_topk_w,
+                                            int T, int H, int E, int k, const int32_t* d_layout, int nchunks,
+                                            int R, const uint64_t* h_peer_a, const uint64_t* h_peer_codes,
+                                            const uint64_t* h_peer_sf, const uint64_t* h_peer_units,
+                                            const uint64_t* h_peer_wts, int me, int64_t ustride,
+                                            const void* d_plan, int32_t* d_pair_pos, int32_t* d_nonfinite_flag,
+                                            void* stream);
+REALB_API int realb_p2p_partial_return(const void* d_rows, int32_t* d_units, const float* d_wts, int R,
+                                       int64_t ustride, int k, int H, int me, const uint64_t* h_ret_bases,
+                                       int64_t unit_base, const void* d_plan, void* stream);
+
 /* Row-major NVFP4 scales [rows][K/16] -> the MMA 128x4 scale layout, for the valid
  * rows of the groups of precision class `prec` in d_layout (E groups). */
 REALB_API int realb_sf_rows_to_mma(const uint8_t* d_sf_rows, int64_t rows_cap, int K, const int32_t* d_layout,
@@ -422,6 +444,20 @@ REALB_API int realb_grouped_gemm_nvfp4_scatter(const uint8_t* d_a_codes, const u
  *   the shared-expert output of models that have one (Kimi-VL, ERNIE-4.5-VL). */
 REALB_API int realb_combine(const void* d_rows, const int32_t* d_pair_pos, const float* d_topk_w,
                   int T, int H, int k, const void* d_addend, void* d_y, void* stream);
+
+/* Combine with the rank-partial return: W16A16 slots as realb_combine;
+ * for a W4A4 owner rank d (d_expert_prec[e] == REALB_PREC_W4A4, owner = e / El) the
+ * rows of t's slots on d enter as ONE bf16 partial P_d(t) (their fma chain in slot
+ * order, rounded once) at t's first slot on d:
+ *   unit_base == -1 : P_d formed here from the rows at d_pos (single-GPU layer, and the
+ *                     collective EP path that gets every slot's row back)
+ *   unit_base >= 0  : P_d read from row unit_base + d * unit_stride + t of d_rows (the
+ *                     return window the owners wrote with realb_p2p_partial_return)
+ * Both forms are bit-identical for identical rows. */
+REALB_API int realb_combine_partial(const void* d_rows, const int32_t* d_pair_pos, const float* d_topk_w,
+                                    const int32_t* d_topk_idx, const uint8_t* d_expert_prec, int El, int T,
+                                    int H, int k, const void* d_addend, int64_t unit_base, int64_t unit_stride,
+                                    void* d_y, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * P1 — host precision policy, identical fp64 operation order to

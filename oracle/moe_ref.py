@@ -16,7 +16,9 @@ reference (moesim) pins only the policy and the quantiser; everything else is
                       h = bf16(silu(g) * u); y = bf16(h . Wd^T)
               W4A4:   same with x, W and h replaced by their reference-block-rule
                       fake-quantised values (fp4.py:108-122, along K, D3)
-  combine     out[t] = bf16( sum_j w[t,j] * y[t,j] )  (fp32 accumulate)
+  combine     out[t] = bf16( sum_j w[t,j] * y[t,j] )  (fp32 accumulate); with the
+              rank-partial return (partial_el = experts per rank), the slots of a W4A4
+              owner rank enter as one bf16-rounded partial sum per (token, rank)
 """
 
 from __future__ import annotations
@@ -93,7 +95,7 @@ def expert_mlp(xe, w_gate, w_up, w_down, w4a4: bool):
 
 
 def moe_layer(x, modality, wg, gate_up, down, k, scoring, expert_prec=None, bias=None,
-              routed_scaling=1.0, norm_min=1e-12, logits=None, shared=None):
+              routed_scaling=1.0, norm_min=1e-12, logits=None, shared=None, partial_el=None):
     """x [T,H] bf16 values (float32); gate_up [E,2I,H] (HF: gate rows first);
     down [E,H,I]; expert_prec [E] 0/1; shared: (gate_up [2Is,H], down [H,Is]) of a
     shared-expert MLP added to every token (BF16 path, bf16 output, summed with the
@@ -111,7 +113,18 @@ def moe_layer(x, modality, wg, gate_up, down, k, scoring, expert_prec=None, bias
             continue
         ye = expert_mlp(x[tok], gate_up[e, :I], gate_up[e, I:], down[e], bool(prec[e]))
         y_pairs[tok, slot] = ye
-    acc = (w[:, :, None] * y_pairs).sum(axis=1, dtype=np.float32)
+    if partial_el:
+        # rank-partial return: the slots of a W4A4 owner rank d (expert e on
+        # rank e // partial_el) enter as ONE bf16-rounded partial sum per (token, d)
+        owner = idx // partial_el
+        w4 = prec[idx].astype(bool)
+        acc = (np.where(w4, 0.0, w)[:, :, None] * y_pairs).sum(axis=1, dtype=np.float32)
+        for d in np.unique(owner[w4]):
+            m = (w4 & (owner == d)).astype(np.float32)
+            part = bf16_round(((m * w)[:, :, None] * y_pairs).sum(axis=1, dtype=np.float32))
+            acc = acc + part
+    else:
+        acc = (w[:, :, None] * y_pairs).sum(axis=1, dtype=np.float32)
     if shared is not None:
         Is = shared[1].shape[1]
         acc = acc + expert_mlp(x, shared[0][:Is], shared[0][Is:], shared[1], False)

@@ -73,6 +73,7 @@ SIGNATURES: dict[str, tuple] = {
     "realb_grouped_gemm_nvfp4": (
         _i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _vp]),
     "realb_combine": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "realb_combine_partial": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i64, _i64, _vp, _vp]),
     "realb_plan": (_i32, [_vp, _i32, _f64, _f64, _i64, _i32, _vp, _vp]),
     "realb_ep_pack": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp]),
@@ -86,6 +87,9 @@ SIGNATURES: dict[str, tuple] = {
     "realb_p2p_return_dev": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "realb_p2p_pack_direct": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                      _vp, _vp]),
+    "realb_p2p_pack_direct_partial": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp,
+                                             _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
+    "realb_p2p_partial_return": (_i32, [_vp, _vp, _vp, _i32, _i64, _i32, _i32, _i32, _vp, _i64, _vp, _vp]),
     "realb_ipc_alloc": (_i32, [_i64, _vp, _vp]),
     "realb_ipc_open": (_i32, [_vp, _vp]),
     "realb_ipc_close": (_i32, [_vp]),
@@ -107,12 +111,13 @@ LAUNCHES_KERNEL = {
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_bf16_gather": 1, "realb_grouped_gemm_nvfp4": 1,
     "realb_grouped_gemm_bf16_copyin": 1, "realb_grouped_gemm_bf16_scatter": 1, "realb_grouped_gemm_nvfp4_scatter": 1, "realb_p2p_return_map": 1, "realb_sf_rows_to_mma": 1,
     "realb_dispatch_index": 1,  # + 1 when NVFP4 rows are quantised (call() adds it)
-    "realb_combine": 1, "realb_quantize_tensor_nvfp4": 1, "realb_dequantize_blocks": 1,
+    "realb_combine": 1, "realb_combine_partial": 1, "realb_quantize_tensor_nvfp4": 1, "realb_dequantize_blocks": 1,
     "realb_gather_rows": 1, "realb_ep_regroup": 2, "realb_index_rows": 1,
     "realb_ep_pack": 2, "realb_gather_rows_nvfp4_packed": 1,
     "realb_p2p_pack": 2, "realb_p2p_return": 1, "realb_p2p_signal": 1, "realb_p2p_wait": 1,
     "realb_p2p_publish": 1, "realb_p2p_plan_offsets": 1, "realb_p2p_pack_dev": 2, "realb_p2p_return_dev": 1,
-    "realb_p2p_wait_next": 1, "realb_p2p_pack_direct": 2,
+    "realb_p2p_wait_next": 1, "realb_p2p_pack_direct": 2, "realb_p2p_pack_direct_partial": 2,
+    "realb_p2p_partial_return": 1,
 }
 launch_count = 0  # kernels launched through this binding (bench.py's gpu_launches)
 

@@ -417,6 +417,98 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
   }
 }
 
+// ----------------------------------------------------------------- rank-partial combine
+// The EP return with a per-rank partial sum ("rank-partial return"): a
+// W4A4 owner rank d sums token t's rows over ITS slots before the return,
+//   P_d(t) = bf16( fma-chain over t's slots j (ascending) with owner(e_j) = d of w_j * y_j ),
+// and returns one row per (token, owner) instead of one per (token, slot). The combine
+//   y(t) = bf16( addend + slots j ascending: W16A16 slot -> fma(w_j, y_j, acc);
+//                first slot of a W4A4 owner d -> acc + P_d(t) )
+// is the same arithmetic whether P_d is formed here from the local rows (REMOTE = false:
+// the single-GPU layer, and the EP collective path that gets every slot's row back) or
+// read from the owner's returned row (REMOTE = true: unit row d * unit_stride + t past
+// unit_base of the return window), so the EP layer equals the single-GPU layer exactly.
+template <int K, bool REMOTE>
+__global__ void __launch_bounds__(256) combine_partial_kernel(
+    const __nv_bfloat16* __restrict__ rows, const int32_t* __restrict__ pos, const float* __restrict__ w,
+    const int32_t* __restrict__ topk_idx, const uint8_t* __restrict__ prec, int El, int T, int H,
+    const __nv_bfloat16* __restrict__ addend, int64_t unit_base, int64_t unit_stride, __nv_bfloat16* __restrict__ y) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  int own[K];
+  bool w4[K], first[K];
+  float wt[K];
+  const uint4* src[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int e = topk_idx[(int64_t)t * K + j];
+    own[j] = e / El;
+    w4[j] = prec[e] == REALB_PREC_W4A4;
+    wt[j] = w[(int64_t)t * K + j];
+    first[j] = true;
+#pragma unroll
+    for (int i = 0; i < j; ++i) first[j] = first[j] && own[i] != own[j];
+    const int64_t row = (REMOTE && w4[j]) ? unit_base + (int64_t)own[j] * unit_stride + t
+                                          : (int64_t)pos[(int64_t)t * K + j];
+    src[j] = reinterpret_cast<const uint4*>(rows + row * H);
+  }
+  for (int c = lane; c < H / 8; c += 32) {
+    uint4 u[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (!(REMOTE && w4[j] && !first[j])) u[j] = __ldg(src[j] + c);  // every needed row in flight
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (addend) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(addend + (int64_t)t * H) + c);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] = bf16lo(av[i]);
+        acc[2 * i + 1] = bf16hi(av[i]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (!w4[j]) {
+        const uint32_t v[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[2 * i] = fmaf(wt[j], bf16lo(v[i]), acc[2 * i]);
+          acc[2 * i + 1] = fmaf(wt[j], bf16hi(v[i]), acc[2 * i + 1]);
+        }
+      } else if (first[j]) {
+        uint32_t pv[4];
+        if constexpr (REMOTE) {
+          pv[0] = u[j].x; pv[1] = u[j].y; pv[2] = u[j].z; pv[3] = u[j].w;
+        } else {  // the owner's partial: its slots in ascending order, one bf16 rounding
+          float p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+          for (int jj = j; jj < K; ++jj) {
+            if (own[jj] != own[j]) continue;
+            const uint32_t v[4] = {u[jj].x, u[jj].y, u[jj].z, u[jj].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              p[2 * i] = fmaf(wt[jj], bf16lo(v[i]), p[2 * i]);
+              p[2 * i + 1] = fmaf(wt[jj], bf16hi(v[i]), p[2 * i + 1]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pv[i] = pack_bf16x2(p[2 * i], p[2 * i + 1]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[2 * i] += bf16lo(pv[i]);
+          acc[2 * i + 1] += bf16hi(pv[i]);
+        }
+      }
+    }
+    reinterpret_cast<uint4*>(y + (int64_t)t * H)[c] =
+        make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                   pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+  }
+}
+
 // ----------------------------------------------------------------- EP pack (send side, C2)
 // One warp per (token, slot) pair: the row goes to destination rank d = e / El,
 // at byte offset byte0[d] + (pos - row0[d]) * row_bytes(fmt[d]) of the send
@@ -637,6 +729,46 @@ extern "C" int realb_combine(const void* d_rows, const int32_t* d_pos, const flo
       return REALB_EUNSUPPORTED;
   }
   return check_launch("realb_combine");
+}
+
+extern "C" int realb_combine_partial(const void* d_rows, const int32_t* d_pos, const float* d_w,
+                                     const int32_t* d_topk_idx, const uint8_t* d_expert_prec, int El, int T, int H,
+                                     int k, const void* d_addend, int64_t unit_base, int64_t unit_stride, void* d_y,
+                                     void* stream) {
+  if (T == 0 && H > 0 && H % 8 == 0 && k >= 1 && k <= 8 && El >= 1) return REALB_OK;
+  if (!d_rows || !d_pos || !d_w || !d_topk_idx || !d_expert_prec || !d_y || T < 0 || H <= 0 || H % 8 || k < 1 ||
+      k > 8 || El < 1 || unit_base < -1 || (unit_base >= 0 && unit_stride < T)) {
+    set_error("realb_combine_partial: bad arguments (T=%d H=%d k=%d El=%d)", T, H, k, El);
+    return REALB_EINVAL;
+  }
+  if (T == 0) return REALB_OK;
+  const dim3 grid((T + 7) / 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto r = reinterpret_cast<const __nv_bfloat16*>(d_rows);
+  auto ad = reinterpret_cast<const __nv_bfloat16*>(d_addend);
+  auto y = reinterpret_cast<__nv_bfloat16*>(d_y);
+  const bool remote = unit_base >= 0;
+#define REALB_CP(KK)                                                                                              \
+  case KK:                                                                                                        \
+    if (remote)                                                                                                   \
+      combine_partial_kernel<KK, true><<<grid, 256, 0, st>>>(r, d_pos, d_w, d_topk_idx, d_expert_prec, El, T, H, \
+                                                             ad, unit_base, unit_stride, y);                       \
+    else                                                                                                          \
+      combine_partial_kernel<KK, false><<<grid, 256, 0, st>>>(r, d_pos, d_w, d_topk_idx, d_expert_prec, El, T, H, \
+                                                              ad, 0, 0, y);                                         \
+    break;
+  switch (k) {
+    REALB_CP(1)
+    REALB_CP(2)
+    REALB_CP(4)
+    REALB_CP(6)
+    REALB_CP(8)
+    default:
+      set_error("realb_combine_partial: top-k must be one of 1,2,4,6,8 (k=%d)", k);
+      return REALB_EUNSUPPORTED;
+  }
+#undef REALB_CP
+  return check_launch("realb_combine_partial");
 }
 
 extern "C" int realb_gather_rows(const void* d_x, const int32_t* d_expert, const int32_t* d_pos,

@@ -281,6 +281,14 @@ struct PeerOperands {
   uint8_t* codes[kMaxPeers];    // peer d's NVFP4 operand codes [rows_cap][H/2]
   uint8_t* sf[kMaxPeers];       // peer d's NVFP4 scales, ROW-MAJOR staging [rows_cap][H/16]
   int R, El;
+  // rank-partial return (realb_p2p_pack_direct_partial): for a W4A4 destination d the
+  // sender also records, per (me, token t, slot j), the grouped row g in d's unit table
+  // units[d][(me * ustride + t) * k + j] and the routing weight in wts[d][g]
+  int32_t* units[kMaxPeers];
+  float* wts[kMaxPeers];
+  const float* topk_w;
+  int me;
+  int64_t ustride;
 };
 
 // Direct dispatch: every (token, slot) row is written straight into its
@@ -306,6 +314,10 @@ __global__ void __launch_bounds__(256) p2p_pack_direct_kernel(const __nv_bfloat1
     const int d = e / ops.El;
     const int64_t g = (int64_t)plan->gpos0[e] + (pair_pos[p] - send_start[e]);
     const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+    if (ops.topk_w && plan->fmt[d] == 1 && lane == 0) {  // rank-partial metadata (W4A4 owner)
+      ops.units[d][((int64_t)ops.me * ops.ustride + t) * k + (p - t * k)] = (int32_t)g;
+      ops.wts[d][g] = ops.topk_w[p];
+    }
     if (plan->fmt[d] == 0) {
       uint4* o = reinterpret_cast<uint4*>(ops.a[d] + g * H);
       for (int i = lane; i < H / 8; i += 32) o[i] = __ldg(src + i);
@@ -366,6 +378,59 @@ __global__ void __launch_bounds__(256) p2p_return_dev_kernel(const __nv_bfloat16
     uint4* dst = reinterpret_cast<uint4*>(win.base[s] + ((int64_t)plan->ret_row0[s] + (i - plan->recv0[s])) *
                                                             (2 * (int64_t)H));
     for (int c = lane; c < H / 8; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+// Rank-partial return: a W4A4 owner sums each (source s, token t)'s
+// rows over ITS slots, in slot order (fma chain, fp32), rounds once to bf16 and stores
+// ONE row into s's return window (row unit_base + me * ustride + t) instead of one row
+// per slot; realb_combine_partial at the source adds it at t's first slot on this rank.
+// Warp per unit (s, t); the unit table is reset to -1 behind itself for the next call.
+// A W16A16 owner (device plan) does nothing here: its rows went back with the down GEMM.
+__global__ void __launch_bounds__(256) p2p_partial_return_kernel(const __nv_bfloat16* __restrict__ rows,
+                                                                 int32_t* __restrict__ units,
+                                                                 const float* __restrict__ wts, int R,
+                                                                 int64_t ustride, int k, int H, int me,
+                                                                 const PeerRows win, int64_t unit_base,
+                                                                 const P2PPlan* __restrict__ plan) {
+  if (!plan->w4a4) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nunits = (int64_t)R * ustride;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nunits;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t gl = lane < k ? units[u * k + lane] : -1;
+    if (!__any_sync(0xffffffffu, gl >= 0)) continue;
+    int32_t g[8];
+    float w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      g[j] = __shfl_sync(0xffffffffu, gl, j);
+      w[j] = (j < k && g[j] >= 0) ? wts[g[j]] : 0.f;
+    }
+    const int s = (int)(u / ustride);
+    const int64_t t = u - (int64_t)s * ustride;
+    uint4* dst = reinterpret_cast<uint4*>(win.base[s] + (unit_base + (int64_t)me * ustride + t) * (2 * (int64_t)H));
+    for (int c = lane; c < H / 8; c += 32) {
+      uint4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k && g[j] >= 0) v[j] = __ldg(reinterpret_cast<const uint4*>(rows + (int64_t)g[j] * H) + c);
+      float p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!(j < k && g[j] >= 0)) continue;
+        const uint32_t vv[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          p[2 * i] = fmaf(w[j], __uint_as_float(vv[i] << 16), p[2 * i]);
+          p[2 * i + 1] = fmaf(w[j], __uint_as_float(vv[i] & 0xFFFF0000u), p[2 * i + 1]);
+        }
+      }
+      dst[c] = make_uint4(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]), pack_bf16x2(p[4], p[5]),
+                          pack_bf16x2(p[6], p[7]));
+    }
+    __syncwarp();
+    if (lane < k) units[u * k + lane] = -1;
   }
 }
 
@@ -655,10 +720,65 @@ extern "C" int realb_p2p_plan_layout(int64_t* out5) {
   return REALB_OK;
 }
 
+static int pack_direct_impl(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                            const int32_t* d_layout, int nchunks, int R, const uint64_t* h_peer_a,
+                            const uint64_t* h_peer_codes, const uint64_t* h_peer_sf, const void* d_plan,
+                            int32_t* d_pair_pos, int32_t* d_flag, const float* d_topk_w, const uint64_t* h_peer_units,
+                            const uint64_t* h_peer_wts, int me, int64_t ustride, void* stream);
+
 extern "C" int realb_p2p_pack_direct(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
                                      const int32_t* d_layout, int nchunks, int R, const uint64_t* h_peer_a,
                                      const uint64_t* h_peer_codes, const uint64_t* h_peer_sf,
                                      const void* d_plan, int32_t* d_pair_pos, int32_t* d_flag, void* stream) {
+  return pack_direct_impl(d_x, d_topk_idx, T, H, E, k, d_layout, nchunks, R, h_peer_a, h_peer_codes, h_peer_sf,
+                          d_plan, d_pair_pos, d_flag, nullptr, nullptr, nullptr, 0, 0, stream);
+}
+
+extern "C" int realb_p2p_pack_direct_partial(const void* d_x, const int32_t* d_topk_idx, const float* d_topk_w,
+                                             int T, int H, int E, int k, const int32_t* d_layout, int nchunks, int R,
+                                             const uint64_t* h_peer_a, const uint64_t* h_peer_codes,
+                                             const uint64_t* h_peer_sf, const uint64_t* h_peer_units,
+                                             const uint64_t* h_peer_wts, int me, int64_t ustride, const void* d_plan,
+                                             int32_t* d_pair_pos, int32_t* d_flag, void* stream) {
+  if (!d_topk_w || !h_peer_units || !h_peer_wts || me < 0 || me >= R || ustride < T) {
+    set_error("realb_p2p_pack_direct_partial: bad arguments (me=%d R=%d ustride=%lld T=%d)", me, R,
+              (long long)ustride, T);
+    return REALB_EINVAL;
+  }
+  return pack_direct_impl(d_x, d_topk_idx, T, H, E, k, d_layout, nchunks, R, h_peer_a, h_peer_codes, h_peer_sf,
+                          d_plan, d_pair_pos, d_flag, d_topk_w, h_peer_units, h_peer_wts, me, ustride, stream);
+}
+
+extern "C" int realb_p2p_partial_return(const void* d_rows, int32_t* d_units, const float* d_wts, int R,
+                                        int64_t ustride, int k, int H, int me, const uint64_t* h_ret_bases,
+                                        int64_t unit_base, const void* d_plan, void* stream) {
+  if (!d_rows || !d_units || !d_wts || !h_ret_bases || !d_plan || R < 1 || R > kMaxPeers || me < 0 || me >= R ||
+      ustride < 1 || k < 1 || k > 8 || H <= 0 || H % 8 || unit_base < 0) {
+    set_error("realb_p2p_partial_return: bad arguments (R=%d me=%d k=%d H=%d)", R, me, k, H);
+    return REALB_EINVAL;
+  }
+  PeerRows win{};
+  win.R = R;
+  for (int s = 0; s < R; ++s) {
+    if (h_ret_bases[s] & 15) {
+      set_error("realb_p2p_partial_return: return window %d misaligned", s);
+      return REALB_EINVAL;
+    }
+    win.base[s] = reinterpret_cast<uint8_t*>(h_ret_bases[s]);
+  }
+  int64_t grid = ((int64_t)R * ustride + 7) / 8;
+  if (grid > (int64_t)num_sms() * 16) grid = (int64_t)num_sms() * 16;
+  p2p_partial_return_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(d_rows), d_units, d_wts, R, ustride, k, H, me, win, unit_base,
+      reinterpret_cast<const P2PPlan*>(d_plan));
+  return check_launch("realb_p2p_partial_return");
+}
+
+static int pack_direct_impl(const void* d_x, const int32_t* d_topk_idx, int T, int H, int E, int k,
+                            const int32_t* d_layout, int nchunks, int R, const uint64_t* h_peer_a,
+                            const uint64_t* h_peer_codes, const uint64_t* h_peer_sf, const void* d_plan,
+                            int32_t* d_pair_pos, int32_t* d_flag, const float* d_topk_w, const uint64_t* h_peer_units,
+                            const uint64_t* h_peer_wts, int me, int64_t ustride, void* stream) {
   if (T == 0 && nchunks == 0) return REALB_OK;
   if (!d_x || !d_topk_idx || !d_layout || !d_plan || !d_pair_pos || !h_peer_a || !h_peer_codes || !h_peer_sf ||
       T < 0 || H <= 0 || H % 64 || E < 1 || E > 256 || k < 1 || k > 8 || R < 1 || R > kMaxPeers || E % R ||
@@ -677,7 +797,14 @@ extern "C" int realb_p2p_pack_direct(const void* d_x, const int32_t* d_topk_idx,
     o.a[d] = reinterpret_cast<__nv_bfloat16*>(h_peer_a[d]);
     o.codes[d] = reinterpret_cast<uint8_t*>(h_peer_codes[d]);
     o.sf[d] = reinterpret_cast<uint8_t*>(h_peer_sf[d]);
+    if (d_topk_w) {
+      o.units[d] = reinterpret_cast<int32_t*>(h_peer_units[d]);
+      o.wts[d] = reinterpret_cast<float*>(h_peer_wts[d]);
+    }
   }
+  o.topk_w = d_topk_w;
+  o.me = me;
+  o.ustride = ustride;
   int rc = ep_positions(d_topk_idx, T, E, k, d_layout, nchunks, d_pair_pos, stream);
   if (rc) return rc;
   const int64_t P = (int64_t)T * k;

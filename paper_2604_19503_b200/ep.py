@@ -258,7 +258,12 @@ class CudaEPOps:
 
         R, H, T, k, E = self.R, self.H, self.T, self.k, self.E
         rc = self.rows_cap
-        sizes = {"recv": R * T * k * 2 * H, "ret": T * k * 2 * H, "ctr": 256, "cnt": R * E * 2 * 4,
+        # return window: T*k pair rows, then R*T unit rows of the rank-partial return
+        # (owner d's partial for my token t at row T*k + d*T + t)
+        sizes = {"recv": R * T * k * 2 * H, "ret": (T * k + R * T) * 2 * H, "ctr": 256, "cnt": R * E * 2 * 4,
+                 # rank-partial return: unit table [R sources][T][k] (grouped row or -1) and
+                 # the routing weight of every grouped row, written by the senders
+                 "units": R * T * k * 4, "wts": rc * 4,
                  # the GEMM operands themselves, written directly by the senders (device-plan path)
                  "opa": rc * H * 2, "opc": rc * (H // 2), "ops": rc * (H // 16),
                  # NVFP4 scales as sent (row-major); converted to "ops" (MMA layout) locally
@@ -308,7 +313,7 @@ class CudaEPOps:
         self.p2p_epoch = 0
         self.p2p_rank = comm.rank
         # peers' operand bases (kept alive: the ABI reads them through a host pointer)
-        self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "opsr")]
+        self.op_bases = [np.array(self.p2p[n], np.uint64) for n in ("opa", "opc", "opsr", "units", "wts")]
         self.ret_bases = np.array(self.p2p["ret"], np.uint64)
         # my operand windows (written by the senders) start as in-distribution values,
         # not the allocation's zeros: their padding rows are multiplied too (moe.operand_noise_)
@@ -321,6 +326,7 @@ class CudaEPOps:
             va[i:i + n].copy_(nb[:n])
         operand_noise_(_device_view(own["opc"], sizes["opc"], torch.uint8), "codes")
         operand_noise_(_device_view(own["ops"], sizes["ops"], torch.uint8), "sf")
+        _device_view(own["units"], sizes["units"] // 4, torch.int32).fill_(-1)  # no rows yet
         del noise, nb
         torch.cuda.synchronize()
         # fused down-GEMM + return: grouped row -> (source, row of its return window)
@@ -384,7 +390,7 @@ class CudaEPOps:
                   self.p2p_err.data_ptr(), sp)
 
     def forward_device(self, x, mod, strategy: str, params: RealbParams, fp4_dispatch: bool,
-                       timer=None):
+                       timer=None, rank_partial: bool = False):
         """The whole EP layer with no host synchronisation (CUDA-graph capturable):
         C1 through peer memory, the plan and every window offset derived on the
         device (realb_moe_align_plan over the gathered [R][E][2] counts,
@@ -432,11 +438,18 @@ class CudaEPOps:
                       self.flag.data_ptr(), self.quant_max_ctas, ssp)
         # C2, direct: every row lands in its destination's GEMM operand at its final
         # grouped row (bf16, or NVFP4 + MMA-layout scales for a W4A4 destination)
-        _lib.call("realb_p2p_pack_direct", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
-                  self.send_layout.data_ptr(), (T + 63) // 64, R,
-                  self.op_bases[0].ctypes.data, self.op_bases[1].ctypes.data, self.op_bases[2].ctypes.data,
-                  self.d_plan.data_ptr(),
-                  self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
+        if rank_partial:  # + each W4A4-bound row's (token, slot) -> grouped row and its weight
+            _lib.call("realb_p2p_pack_direct_partial", x.data_ptr(), self.topk_idx.data_ptr(),
+                      self.topk_w.data_ptr(), T, H, E, k, self.send_layout.data_ptr(), (T + 63) // 64, R,
+                      self.op_bases[0].ctypes.data, self.op_bases[1].ctypes.data, self.op_bases[2].ctypes.data,
+                      self.op_bases[3].ctypes.data, self.op_bases[4].ctypes.data, r, self.T,
+                      self.d_plan.data_ptr(), self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
+        else:
+            _lib.call("realb_p2p_pack_direct", x.data_ptr(), self.topk_idx.data_ptr(), T, H, E, k,
+                      self.send_layout.data_ptr(), (T + 63) // 64, R,
+                      self.op_bases[0].ctypes.data, self.op_bases[1].ctypes.data, self.op_bases[2].ctypes.data,
+                      self.d_plan.data_ptr(),
+                      self.send_pos.data_ptr(), self.flag.data_ptr(), sp)
         self._signal_wait_dev(_DEV_CTR_DISPATCH, 0)
         mark("dispatch")
         # receive side: only the grouped layout and the row map for the return (no row copies)
@@ -463,15 +476,29 @@ class CudaEPOps:
         _lib.call("realb_grouped_gemm_nvfp4", a_codes, a_sf,
                   ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(), self.rows_cap, 2 * I, H, El, lay,
                   _lib.EPI_SWIGLU, None, ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(), 0, sp)
-        _lib.call("realb_grouped_gemm_nvfp4_scatter", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
-                  ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
-                  self.row_map.data_ptr(), R, rb, 0, sp)
+        if rank_partial:
+            # a W4A4 owner: down GEMM rows stay local, then ONE partial row per (source,
+            # token) goes back (no-op kernels on a W16A16 owner: no W4A4 groups, gate off)
+            _lib.call("realb_grouped_gemm_nvfp4", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+                      ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
+                      _lib.EPI_STORE, self.rows_out.data_ptr(), None, None, 0, sp)
+            _lib.call("realb_p2p_partial_return", self.rows_out.data_ptr(), self._p2p_own["units"],
+                      self._p2p_own["wts"], R, self.T, k, H, r, rb, self.T * k, pl, sp)
+        else:
+            _lib.call("realb_grouped_gemm_nvfp4_scatter", ws["h_codes"].data_ptr(), ws["h_sf"].data_ptr(),
+                      ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(), self.rows_cap, H, I, El, lay,
+                      self.row_map.data_ptr(), R, rb, 0, sp)
         mark("compute")
         self._signal_wait_dev(_DEV_CTR_RETURN, 1)
         y = torch.empty(T, H, dtype=torch.bfloat16, device=self.dev)
         addend = self.shared.join() if self.shared is not None and T > 0 else None
-        _lib.call("realb_combine", self.p2p["ret"][r], self.send_pos.data_ptr(), self.topk_w.data_ptr(),
-                  T, H, k, addend, y.data_ptr(), sp)
+        if rank_partial:
+            _lib.call("realb_combine_partial", self.p2p["ret"][r], self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+                      self.topk_idx.data_ptr(), self.prec_global.data_ptr(), El, T, H, k, addend, self.T * k,
+                      self.T, y.data_ptr(), sp)
+        else:
+            _lib.call("realb_combine", self.p2p["ret"][r], self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+                      T, H, k, addend, y.data_ptr(), sp)
         mark("combine")
         if torch.cuda.is_current_stream_capturing():
             return y, None
@@ -540,13 +567,22 @@ class CudaEPOps:
         if self.shared is not None and x.shape[0] > 0:
             self.shared.start(x)
 
-    def combine(self, ret_buf, send_pos, topk_w):
+    def combine(self, ret_buf, send_pos, topk_w, partial_prec=None):
+        """Weighted top-k combine of the returned rows (send order). partial_prec (uint8 [E]
+        expert precisions, host): the rank-partial return's arithmetic, formed here from
+        every slot's returned row — equal to the device path's owner-side partials."""
         T = send_pos.shape[0]
         y = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.dev)
         ret_ptr = ret_buf if isinstance(ret_buf, int) else ret_buf.data_ptr()
         addend = self.shared.join() if self.shared is not None and T > 0 else None
-        _lib.call("realb_combine", ret_ptr, self.send_pos.data_ptr(), self.topk_w.data_ptr(),
-                  T, self.H, self.k, addend, y.data_ptr(), _lib.stream_ptr())
+        if partial_prec is not None:
+            self.prec_partial = torch.as_tensor(np.asarray(partial_prec, np.uint8)).to(self.dev)
+            _lib.call("realb_combine_partial", ret_ptr, self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+                      self.topk_idx.data_ptr(), self.prec_partial.data_ptr(), self.El, T, self.H, self.k, addend,
+                      -1, 0, y.data_ptr(), _lib.stream_ptr())
+        else:
+            _lib.call("realb_combine", ret_ptr, self.send_pos.data_ptr(), self.topk_w.data_ptr(),
+                      T, self.H, self.k, addend, y.data_ptr(), _lib.stream_ptr())
         return y
 
 
@@ -559,7 +595,7 @@ class EPMoELayer:
     phase boundaries of engine.py's RankPhases (schedule / transform /
     dispatch / compute / combine)."""
 
-    def __init__(self, shape: MoEShape, comm: EPComm, ops, fp4_dispatch: bool = False):
+    def __init__(self, shape: MoEShape, comm: EPComm, ops, fp4_dispatch: bool = False, rank_partial: bool = False):
         if shape.num_experts % comm.world:
             raise ValueError("experts must divide evenly over the EP ranks")
         self.shape, self.comm, self.ops = shape, comm, ops
@@ -567,6 +603,9 @@ class EPMoELayer:
         self.El = shape.num_experts // self.R
         self.cluster = ClusterConfig(self.R, 1, self.El, 1, shape.modality_isolated)
         self.fp4_dispatch = fp4_dispatch
+        # rank_partial: a W4A4 owner returns ONE bf16 partial row per (token, owner) — its
+        # slots pre-summed — instead of one row per (token, slot)
+        self.rank_partial = rank_partial
 
     def forward_device(self, x, mod, strategy: str = "realb", params: RealbParams | None = None, timer=None):
         """Host-sync-free EP layer (peer-memory transport only): -> (y, DevicePlanResult
@@ -580,7 +619,8 @@ class EPMoELayer:
             # owner's precision: a W4A4 owner always receives NVFP4 rows
             raise ValueError("the device-plan EP layer always sends NVFP4 rows to W4A4 ranks "
                              "(fp4_dispatch=True); use forward() for bf16 dispatch")
-        return self.ops.forward_device(x, mod, strategy, params or RealbParams(), self.fp4_dispatch, timer)
+        return self.ops.forward_device(x, mod, strategy, params or RealbParams(), self.fp4_dispatch, timer,
+                                       rank_partial=self.rank_partial)
 
     def forward(self, x, mod, strategy: str = "realb", params: RealbParams | None = None, timer=None):
         R, r, El, E = self.R, self.rank, self.El, self.shape.num_experts
@@ -615,7 +655,13 @@ class EPMoELayer:
             back = self.ops.expert_compute(recv_buf, cnt, w4a4, fp4_rows[r])
             mark("compute")
             ret = self.comm.all_to_all_rows(self.ops.ret_buffer(), back, send_counts, recv_counts)  # C3
-        y = self.ops.combine(ret, send_pos, topk_w)
+        if self.rank_partial:
+            from .policy import place_experts_static
+
+            y = self.ops.combine(ret, send_pos, topk_w,
+                                 partial_prec=plan.expert_precision(place_experts_static(self.cluster)))
+        else:
+            y = self.ops.combine(ret, send_pos, topk_w)
         mark("combine")
         return y, plan, vt_all
 

@@ -344,6 +344,10 @@ class MoELayer:
         #   "copyin" K5's spare warps copy them into a_bf16 while its mainloop runs,
         #            gated per expert (realb_grouped_gemm_bf16_copyin)
         self.dispatch_mode = "copy"
+        # rank_partial: combine with the EP rank-partial return's arithmetic (the slots of a
+        # W4A4 rank enter as one bf16 partial per (token, rank); ep.py), so
+        # the single-GPU layer with the EP cluster reproduces that EP layer bit for bit
+        self.rank_partial = False
         self.row_src = torch.zeros(R, dtype=i32, device=dev)
         self.ready = torch.zeros(E, dtype=i32, device=dev)     # copy-in per-expert row counters
         self.copy_err = torch.zeros(1, dtype=i32, device=dev)  # copy-in wait timeout flag
@@ -515,8 +519,13 @@ class MoELayer:
         mark("down_end", main)
         y = self.y_buf[:T] if out is None else out
         addend = self.shared.join() if shared else None
-        _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
-                  self.topk_w.data_ptr(), T, H, k, addend, y.data_ptr(), sp)
+        if self.rank_partial:  # the EP rank-partial return's numerics (W4A4 ranks' slots pre-summed)
+            _lib.call("realb_combine_partial", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
+                      self.topk_w.data_ptr(), self.topk_idx.data_ptr(), self.prec_dev.data_ptr(),
+                      self.cluster.experts_per_rank, T, H, k, addend, -1, 0, y.data_ptr(), sp)
+        else:
+            _lib.call("realb_combine", self.rows_out.data_ptr(), self.pair_pos.data_ptr(),
+                      self.topk_w.data_ptr(), T, H, k, addend, y.data_ptr(), sp)
         mark("combine_end", main)
         if torch.cuda.is_current_stream_capturing():
             return LayerResult(y, self, self.plan_host, self.expert_vt_host, None, self.placement,

@@ -39,7 +39,8 @@ def _setup(shape_name, E, T, world, rank, device="cuda"):
     return shape, x, mod, router, gu, dn, sh
 
 
-def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir, p2p=False, device_plan=False):
+def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir, p2p=False, device_plan=False,
+            rank_partial=False):
     import sys
     from pathlib import Path
 
@@ -59,7 +60,7 @@ def _worker(rank, world, port, shape_name, E, T, strategy, fp4_dispatch, outdir,
     comm = EPComm(staged=True, p2p=p2p)
     if p2p:
         ops.setup_p2p(comm)
-    layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch)
+    layer = EPMoELayer(shape, comm, ops, fp4_dispatch=fp4_dispatch, rank_partial=rank_partial)
     params = RealbParams(global_batch_threshold=0)
     if device_plan:
         # host-sync-free layer: eager twice, then captured as a CUDA graph and replayed
@@ -142,6 +143,27 @@ def test_ep1_host_sync_free_layer_own_windows(tmp_path, strategy):
     _run_and_compare(tmp_path, "kimi", 16, 333, strategy, True, p2p=True, device_plan=True, world=1)
 
 
+@pytest.mark.parametrize("world,shape_name,E,T,strategy", [
+    (2, "kimi", 16, 384, "realb"), (2, "qwen", 16, 256, "fp4all"), (2, "kimi_shared", 16, 384, "realb"),
+    (2, "kimi", 16, 203, "fp4all"), (4, "kimi", 16, 256, "realb"), (2, "tiny", 8, 512, "baseline")])
+def test_ep_rank_partial_return_host_sync_free(tmp_path, world, shape_name, E, T, strategy):
+    """Rank-partial return (realb_p2p_pack_direct_partial -> local K6 down ->
+    realb_p2p_partial_return -> realb_combine_partial): a W4A4 owner sends ONE bf16
+    partial row per (token, owner). Equal, bit for bit, to the single-GPU layer with the
+    same arithmetic (MoELayer.rank_partial), eager and as a CUDA graph, and within the
+    layer bar of the oracle's emulation of the rule."""
+    _run_and_compare(tmp_path, shape_name, E, T, strategy, True, p2p=True, device_plan=True, world=world,
+                     rank_partial=True)
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+def test_ep_rank_partial_collective_path(tmp_path, p2p):
+    """The host-plan EP paths (collective all-to-alls / peer-memory windows) with the
+    rank-partial arithmetic formed at the source from every slot's returned row: equal to
+    the single-GPU layer (and so to the host-sync-free path, which the bench checks)."""
+    _run_and_compare(tmp_path, "kimi", 16, 384, "realb", True, p2p=p2p, world=2, rank_partial=True)
+
+
 def test_device_plan_layer_rejects_bf16_dispatch():
     """The host-sync-free layer always sends NVFP4 rows to W4A4 owners; asking it
     for bf16 dispatch is an error (not a silently different measurement)."""
@@ -217,9 +239,10 @@ def _check_direct_dispatch_operands(tmp_path, world):
     assert checked > 0
 
 
-def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False, world=2):
+def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, device_plan=False, world=2,
+                     rank_partial=False):
     mp.spawn(_worker, args=(world, _free_port(), shape_name, E, T, strategy, fp4_dispatch, str(tmp_path), p2p,
-                            device_plan), nprocs=world)
+                            device_plan, rank_partial), nprocs=world)
     from paper_2604_19503_b200 import _lib
     from paper_2604_19503_b200.moe import MoELayer, MoEWeights
     from paper_2604_19503_b200.policy import ClusterConfig, RealbParams
@@ -231,6 +254,7 @@ def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, de
     bias = torch.zeros(E, device="cuda") if shape.scoring == _lib.SCORE_SIGMOID_RENORM else None
     single = MoELayer(MoEWeights.from_hf(shape, router, gu, dn, bias=bias, shared=sh), max_tokens=world * T,
                       cluster=ClusterConfig(world, 1, E // world, 1, shape.modality_isolated))
+    single.rank_partial = rank_partial
     res = single.forward(x, mod, strategy, RealbParams(global_batch_threshold=0))
     ref = res.y.float().cpu().numpy()
     r = [np.load(tmp_path / f"r{i}.npz") for i in range(world)]
@@ -245,7 +269,8 @@ def _run_and_compare(tmp_path, shape_name, E, T, strategy, fp4_dispatch, p2p, de
                              gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
                              expert_prec=prec, routed_scaling=shape.routed_scaling,
                              logits=single.logits[:world * T].cpu().numpy(),
-                             shared=None if sh is None else (sh[0].float().cpu().numpy(), sh[1].float().cpu().numpy()))
+                             shared=None if sh is None else (sh[0].float().cpu().numpy(), sh[1].float().cpu().numpy()),
+                             partial_el=(E // world) if rank_partial else None)
     assert (single.topk_idx[:world * T].cpu().numpy() == oref["idx"]).all()
     err = float(np.linalg.norm(y - oref["y"]) / np.linalg.norm(oref["y"]))
     bar = 1e-3 if (strategy == "fp4all" and sh is None) else 2e-3  # tests/test_layer_gpu.py BAR

@@ -607,3 +607,32 @@ def test_full_size_ernie_modality_split_ep8(parity_log):
         assert (codes[e * rows:(e + 1) * rows].cpu().numpy() == c_ref).all()
         s = sf.view(-1)[e * rows * cols // 16:(e + 1) * rows * cols // 16].cpu().numpy()
         assert (sf_mma_to_flat(s, rows, cols) == s_ref).all()
+
+
+@pytest.mark.parametrize("name,E,T,strategy,R", [("kimi", 64, 2048, "realb", 8), ("qwen", 32, 512, "fp4all", 4),
+                                                  ("tiny", None, 1024, "baseline", 2)])
+def test_layer_rank_partial_combine_vs_oracle(name, E, T, strategy, R, parity_log):
+    """The rank-partial return's arithmetic (realb_combine_partial, local form): W4A4
+    ranks' slots enter as one bf16 partial per (token, rank) — vs the oracle's
+    emulation of the same rule; with no W4A4 rank it is the plain combine, bit for bit."""
+    shape = small(SHAPES[name], E)
+    layer, x, mod, router, gu, dn, _ = build_layer(shape, T, R=R)
+    params = RealbParams(global_batch_threshold=0)
+    y_plain = layer.forward(x, mod, strategy, params).y.clone()
+    layer.rank_partial = True
+    res = layer.forward(x, mod, strategy, params)
+    torch.cuda.synchronize()
+    prec = res.plan.expert_precision(layer.placement)
+    El = shape.num_experts // R
+    ref = moe_ref.moe_layer(x.float().cpu().numpy(), mod.cpu().numpy(), router.float().cpu().numpy(),
+                            gu.float().cpu().numpy(), dn.float().cpu().numpy(), shape.top_k, shape.scoring,
+                            expert_prec=prec, routed_scaling=shape.routed_scaling,
+                            logits=layer.logits[:T].cpu().numpy(), partial_el=El)
+    y = res.y.float().cpu().numpy()
+    err = rel_err(y, ref["y"])
+    parity_log(f"layer_rank_partial_{strategy}", err, BAR[strategy])
+    assert err < BAR[strategy], err
+    if not prec.any():
+        assert torch.equal(res.y, y_plain)
+    else:  # the partial rounding is real: the result differs from the plain combine somewhere
+        assert not torch.equal(res.y, y_plain)
