@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(256, 1)
   };
   // arrive on a barrier of the pair leader (local barrier in a 1-CTA launch)
   auto arrive_leader = [&](uint64_t* bar) {
-    if constexpr (CL == 2) mbar_arrive_cluster(mapa_shared(bar, 0));
-    else mbar_arrive(bar);
+    // relaxed: these arrives only signal "slot value read" / "TMEM drained" (no memory
+    // writes to publish); a release arrive waits for the warp's outstanding stores
+    if constexpr (CL == 2) mbar_arrive_cluster_relaxed(mapa_shared(bar, 0));
+    else mbar_arrive_relaxed(bar);
   };
 
   // Producer and MMA roles run on their whole warp with warp-uniform values and
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
       const int t = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
       __syncwarp();
-      if (leader) mbar_arrive(&slot_empty[slot]);
+      if (leader) mbar_arrive_relaxed(&slot_empty[slot]);
       if (t < 0) break;
       const int acc = i & 1;
       mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&slot_full[slot], (i / kTileRing) & 1);
       const int t = slot_tile[slot];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&slot_empty[slot]);
+      if (lane == 0) mbar_arrive_relaxed(&slot_empty[slot]);
       if (t < 0) break;
       bool dummy;
       const TileCoord c = tile_of(t, 0, dummy);

@@ -74,7 +74,10 @@ struct Fp4Args {
   uint8_t* out_sf;      // SWIGLU: MMA-layout scales of the [rows][N/2] result
   uint32_t sf_lbo, sf_sbo;
   uint32_t dbg;  // REALB_DBG_FP4 bits: 1 skip epilogue math/stores, 2 skip scale copies, 4 skip MMAs,
-                 // 8 release the accumulator without reading it
+                 // 8 release the accumulator without reading it, 16 no accumulator hand-off at
+                 // all (MMA never waits, epilogue idle; wrong results: the mainloop alone), 32 STORE
+                 // epilogue stages its chunks but issues no TMA store, 64 every TMA store writes
+                 // output tile 0 (L2-resident: no HBM write-back)
   RowScatter scat;  // kEpiScatter: per-row destinations (down GEMM fused with the EP return)
 };
 
@@ -160,8 +163,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
     return sched.coord(mu * n_tiles);
   };
   auto arrive_leader = [&](uint64_t* bar) {
-    if constexpr (CL == 2) mbar_arrive_cluster(mapa_shared(bar, 0));
-    else mbar_arrive(bar);
+    // relaxed: these arrives only signal "slot value read" / "TMEM drained" (no memory
+    // writes to publish); a release arrive waits for the warp's outstanding stores
+    if constexpr (CL == 2) mbar_arrive_cluster_relaxed(mapa_shared(bar, 0));
+    else mbar_arrive_relaxed(bar);
   };
 
   // Producer and MMA roles run on their WHOLE warp: every lane computes the same
@@ -281,14 +286,14 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       mbar_wait(&slot_full[slot], (it / kF4Ring) & 1);
       const int u = __shfl_sync(0xffffffffu, slot_tile[slot], 0);
       __syncwarp();
-      if (leader) mbar_arrive(&slot_empty[slot]);
+      if (leader) mbar_arrive_relaxed(&slot_empty[slot]);
       if (u < 0) break;
       const int mu = u / nchunks, nt0 = (u - mu * nchunks) * kNPerUnit;
       const int nt1 = min(n_tiles, nt0 + kNPerUnit);
       for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
         // previous n-tile drained by the epilogue(s) => every earlier MMA completed,
         // so the resident A scales may be rewritten at the start of a new unit
-        mbar_wait(tempty, (tile_it & 1) ^ 1);
+        if (!(args.dbg & 16u)) mbar_wait(tempty, (tile_it & 1) ^ 1);  // dbg 16: no accumulator hand-off
         tc_fence_after();
         const bool load_a_sf = nt == nt0;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -323,12 +328,20 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           sfsel ^= 1;
           if (++stage == kF4Stages) { stage = 0; phase ^= 1; }
         }
-        if (leader) {
+        if (leader && !(args.dbg & 16u)) {
           if constexpr (CL == 2) tc_commit_2sm_mc(tfull, kBoth);
           else tc_commit(tfull);
         }
         __syncwarp();
       }
+    }
+    if (args.dbg & 16u) {  // debug: nobody else waited for the MMAs; drain them before the TMEM dealloc
+      if (leader) {
+        if constexpr (CL == 2) tc_commit_2sm_mc(tfull, kBoth);
+        else tc_commit(tfull);
+      }
+      __syncwarp();
+      mbar_wait(tfull, 0);
     }
   } else if (warp >= 4) {  // ---------------- epilogue (8 warps per CTA)
     const int q = warp & 3, half = (warp - 4) >> 2;
@@ -349,6 +362,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       for (int nt = nt0; nt < nt1; ++nt, ++tile_it) {
       TileCoord c = cm;
       c.n0 = nt * kF4BN;
+      if (args.dbg & 16u) continue;  // debug: no accumulator hand-off (mainloop alone)
       mbar_wait(tfull, tile_it & 1);
       tc_fence_after();
       const uint32_t tb = tmem_base + kTmemAcc + ((uint32_t)(q * 32) << 16);
@@ -446,9 +460,10 @@ __global__ void __launch_bounds__(kF4Threads, 1)
                          p[4 * cc + 2], p[4 * cc + 3]);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(args.dbg & 32u)) {  // dbg 32: staged, never stored; 64: every store to tile 0
+            const bool same = args.dbg & 64u;
             tma_store_2d(&tmOut, smem + S::EPI_OFF + wi * (kF4EpiBufs * 2048) + sbuf * 2048,
-                         c.n0 + half * 128 + 32 * i, c.a_row + q * 32);
+                         same ? 32 * i : c.n0 + half * 128 + 32 * i, same ? q * 32 : c.a_row + q * 32);
             bulk_commit_group();
           }
           sbuf = sbuf + 1 == kF4EpiBufs ? 0 : sbuf + 1;
@@ -470,6 +485,12 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   }
   if (threadIdx.x == 0) GroupedSched::finish(args.layout, REALB_PREC_W4A4);
 }
+
+// gemm_fp4_pair.cu
+int fp4_pair_supported(int epilogue, int N, int K);
+int fp4_pair(int epilogue, const uint8_t* a, const uint8_t* a_sf, const uint8_t* w, const uint8_t* w_sf,
+             int64_t rows_cap, int N, int K, int E, const int32_t* layout, void* out, uint8_t* out_codes,
+             uint8_t* out_sf, int max_ctas, uint32_t sf_lbo, uint32_t sf_sbo, uint32_t dbg, cudaStream_t st);
 
 static uint32_t env_u32(const char* name, uint32_t dflt) {
   const char* s = getenv(name);
@@ -567,14 +588,31 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
     return REALB_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // 1-CTA tiles by default: the 2-CTA pair form (same results) measured slower on the
-  // EP8 hot rank (scripts/bench_fp4.py, interleaved: gate_up 0.44 vs 0.37 ms) — its
-  // TMA-only pipeline time did not drop with the halved W bytes, so the 1-CTA kernel
-  // is not feed-bound. REALB_GEMM_CLUSTER=2 selects the pair kernel.
+  // Kernel choice (all forms give bit-identical results; tests/test_gemm_fp4_gpu.py):
+  //  * STORE (down GEMM): K6 v2 (gemm_fp4_pair.cu: 2-SM pairs, the A operand resident in
+  //    smem for a unit of n-tiles), measured 0.224 vs 0.257 ms (v1 1-CTA) on the EP8 hot
+  //    rank (scripts/bench_k6_v2.py);
+  //  * SWIGLU (gate_up): v1 in its 2-CTA pair form. The v2 form has no edge there (the
+  //    128 KB A reload per unit stalls as much as the streamed A costs).
+  // REALB_K6_VERSION=1 forces v1 (REALB_GEMM_CLUSTER=1|2 then picks its form),
+  // REALB_K6_VERSION=2 forces v2 where it is supported.
   const char* cl_env = getenv("REALB_GEMM_CLUSTER");
-  const bool pair = cl_env && cl_env[0] == '2';
+  const char* ver = getenv("REALB_K6_VERSION");
+  const bool cl_set = cl_env && cl_env[0];
+  const bool v1_forced = (ver && ver[0] == '1') || cl_set;
+  auto use_v2 = [&](int epi) {
+    if (!fp4_pair_supported(epi, N, K) || v1_forced) return false;
+    return epi == REALB_EPI_STORE || (ver && ver[0] == '2');
+  };
+  // v1 form: pair unless REALB_GEMM_CLUSTER=1, or REALB_K6_VERSION=1 without a cluster
+  // choice (the 1-CTA kernel, as in round 1)
+  const bool pair = cl_set ? cl_env[0] == '2' : !(ver && ver[0] == '1');
   if (epilogue == REALB_EPI_STORE) {
     if (!d_out) { set_error("realb_grouped_gemm_nvfp4: STORE needs d_out"); return REALB_EINVAL; }
+    if (use_v2(REALB_EPI_STORE))
+      return fp4_pair(REALB_EPI_STORE, d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E, d_layout, d_out,
+                      nullptr, nullptr, max_ctas, env_u32("REALB_DBG_SF_LBO", 128), env_u32("REALB_DBG_SF_SBO", 128),
+                      env_u32("REALB_DBG_FP4", 0), st);
     const char* xst = getenv("REALB_DBG_FP4_STORE4");
     if (xst && xst[0] == '1' && !pair) {
       if (!(env_u32("REALB_DBG_FP4", 0) & 1u)) {
@@ -595,6 +633,10 @@ extern "C" int realb_grouped_gemm_nvfp4(const uint8_t* d_a_codes, const uint8_t*
       return REALB_EINVAL;
     }
     // d_out (optional, SWIGLU): also store the bf16 SwiGLU values the re-quantisation consumed
+    if (use_v2(REALB_EPI_SWIGLU))
+      return fp4_pair(REALB_EPI_SWIGLU, d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E, d_layout, d_out,
+                      d_out_codes, d_out_sf, max_ctas, env_u32("REALB_DBG_SF_LBO", 128),
+                      env_u32("REALB_DBG_SF_SBO", 128), env_u32("REALB_DBG_FP4", 0), st);
     return pair ? launch_fp4<REALB_EPI_SWIGLU, 2>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,
                                                   d_layout, d_out, d_out_codes, d_out_sf, max_ctas, st)
                 : launch_fp4<REALB_EPI_SWIGLU, 1>(d_a_codes, d_a_sf, d_w_codes, d_w_sf, rows_cap, N, K, E,

@@ -40,11 +40,18 @@ def make_problem(E, N, K, counts, seed, a_scale=1.0):
     return lay, rows, A, W, ac, asf, wc, wsf
 
 
-@pytest.fixture(params=["1", "2"], ids=["cta1", "pair"])
+@pytest.fixture(params=["1", "2", "v2"], ids=["cta1", "pair", "pair_a_resident"])
 def cluster(request, monkeypatch):
-    """Both kernel forms: one CTA per tile, and 2-CTA pairs (cta_group::2, M = 256,
-    odd m-tile counts give the rank-1 CTA a dummy slot)."""
-    monkeypatch.setenv("REALB_GEMM_CLUSTER", request.param)
+    """Every kernel form: v1 with one CTA per tile, v1 with 2-CTA pairs (cta_group::2,
+    M = 256, odd m-tile counts give the rank-1 CTA a dummy slot), and the v2 STORE
+    kernel (gemm_fp4_pair.cu: pairs, A resident, N = 128 double-buffered; the default
+    for STORE with K <= 1536, other shapes fall back to v1)."""
+    if request.param == "v2":
+        monkeypatch.delenv("REALB_GEMM_CLUSTER", raising=False)
+        monkeypatch.setenv("REALB_K6_VERSION", "2")
+    else:
+        monkeypatch.setenv("REALB_GEMM_CLUSTER", request.param)
+        monkeypatch.setenv("REALB_K6_VERSION", "1")
     return request.param
 
 
@@ -167,3 +174,53 @@ def test_fp4_scatter_equals_store(E, N, K, counts, n_dst):
         assert torch.equal(got[d][j], refc[g]), (g, d, j)
     for d, s in enumerate(sizes):
         assert (got[d][s:].float() == 7.0).all()
+
+
+@pytest.mark.parametrize("E,N,K,counts,epi", [
+    (8, 2048, 1408, None, "store"),             # Kimi EP8 hot rank, down GEMM
+    (8, 2816, 2048, None, "swiglu"),            # Kimi EP8 hot rank, gate_up GEMM (+ K4 epilogue)
+    (5, 512, 768, [1, 0, 383, 129, 1000], "store"),   # Qwen down K, odd / empty / 1-row experts
+    (5, 1536, 2048, [1, 0, 383, 129, 1000], "swiglu"),  # Qwen gate_up
+    (2, 2560, 512, [700, 300], "store"),        # ERNIE-vision down K
+    (3, 1024, 1024, [256, 255, 257], "swiglu"),
+])
+def test_fp4_v2_equals_v1(E, N, K, counts, epi, monkeypatch):
+    """K6 v2 (pair, A resident) and v1 (1-CTA) give bit-identical outputs (bf16 for
+    STORE; NVFP4 codes, scales and the bf16 SwiGLU hook for SWIGLU): the same K=64
+    block-scaled MMAs in the same k order; only tiling and feed differ."""
+    if counts is None:
+        counts = ((np.random.default_rng(0).random(E) * 0.2 + 0.9) * 17134).astype(np.int64).tolist()
+    lay, rows, A, W, ac, asf, wc, wsf = make_problem(E, N, K, counts, seed=7 + K)
+    lt = torch.from_numpy(lay).cuda()
+    outs = []
+    monkeypatch.delenv("REALB_GEMM_CLUSTER", raising=False)
+    for ver in ("1", "2", "2"):  # v2 twice: the tile counters re-arm between launches
+        monkeypatch.setenv("REALB_K6_VERSION", ver)
+        if epi == "store":
+            out = torch.full((rows, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+            _lib.call("realb_grouped_gemm_nvfp4", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(),
+                      rows, N, K, E, lt.data_ptr(), _lib.EPI_STORE, out.data_ptr(), None, None, 0,
+                      _lib.stream_ptr())
+            res = [out.view(torch.int16)]
+        else:
+            I = N // 2
+            hc = torch.zeros(rows, I // 2, dtype=torch.uint8, device="cuda")
+            hsf = torch.zeros(rows * I // 16, dtype=torch.uint8, device="cuda")
+            hbf = torch.zeros(rows, I, dtype=torch.bfloat16, device="cuda")
+            _lib.call("realb_grouped_gemm_nvfp4", ac.data_ptr(), asf.data_ptr(), wc.data_ptr(), wsf.data_ptr(),
+                      rows, N, K, E, lt.data_ptr(), _lib.EPI_SWIGLU, hbf.data_ptr(), hc.data_ptr(), hsf.data_ptr(),
+                      0, _lib.stream_ptr())
+            res = [hbf.view(torch.int16), hc, hsf]  # scales: MMA layout, compared whole
+        torch.cuda.synchronize()
+        outs.append(res)
+    valid = torch.zeros(rows, dtype=torch.bool)
+    for e in range(E):
+        rs = int(lay[8 + e])
+        valid[rs:rs + counts[e]] = True
+    valid = valid.cuda()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            if a.dim() == 1:
+                assert torch.equal(a, b), int((a != b).sum())
+            else:
+                assert torch.equal(a[valid], b[valid]), int((a[valid] != b[valid]).sum())
