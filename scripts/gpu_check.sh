@@ -1,5 +1,5 @@
 set -u
-O=gpurun_out/r02b; mkdir -p $O
+O=gpurun_out/${1:-r02c}; mkdir -p $O
 rm -f gpurun_out/parity_log.jsonl
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $O/gputest.log 2>&1; tail -3 $O/gputest.log
