@@ -100,6 +100,18 @@ REALB_API int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows_
                                            int32_t* d_nonfinite_flag, int max_ctas,
                                            void* stream);
 
+/* K3 over two weight matrices of the same experts in ONE launch (an expert's
+ * gate_up [E*rows0_per_expert, cols0] and down [E*rows1_per_expert, cols1]):
+ * the W4A4 experts' tiles of both matrices form one contiguous range split over
+ * a persistent grid, so the pair pays one ramp-up and one tail. Same rule, codes
+ * and MMA scale layout as realb_quantize_experts_nvfp4 on each matrix
+ * (replaces fp4.py:173-227 per rank-layer). */
+REALB_API int realb_quantize_experts2_nvfp4(const void* d_w0, int64_t rows0_per_expert, int64_t cols0,
+                                            uint8_t* d_codes0, uint8_t* d_sf0, const void* d_w1,
+                                            int64_t rows1_per_expert, int64_t cols1, uint8_t* d_codes1,
+                                            uint8_t* d_sf1, int E, const uint8_t* d_expert_prec,
+                                            int32_t* d_nonfinite_flag, int max_ctas, void* stream);
+
 /* Q5 — quantize_tensor + ErrorSummary (fp4.py:130-170) on the device.
  *   d_x        : n flat values (dtype REALB_DT_BF16 / F32 / F64), n > 0; the
  *                last block is zero-padded

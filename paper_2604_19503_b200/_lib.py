@@ -49,6 +49,8 @@ SIGNATURES: dict[str, tuple] = {
     "realb_layout_words": (_i64, [_i32, _i32]),
     "realb_moe_align_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _f64, _f64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "realb_quantize_experts_nvfp4": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "realb_quantize_experts2_nvfp4": (
+        _i32, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _i32, _vp]),
     "realb_quantize_tensor_nvfp4": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
     "realb_dequantize_blocks": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "realb_moe_align": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
@@ -107,7 +109,7 @@ _lib: C.CDLL | None = None
 LAUNCHES_KERNEL = {
     "realb_dispatch_permute": 2,
     "realb_quantize_nvfp4": 1, "realb_router_topk_stats": 1, "realb_moe_align": 1,
-    "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1,
+    "realb_moe_align_plan": 1, "realb_quantize_experts_nvfp4": 1, "realb_quantize_experts2_nvfp4": 1,
     "realb_grouped_gemm_bf16": 1, "realb_grouped_gemm_bf16_gather": 1, "realb_grouped_gemm_nvfp4": 1,
     "realb_grouped_gemm_bf16_copyin": 1, "realb_grouped_gemm_bf16_scatter": 1, "realb_grouped_gemm_nvfp4_scatter": 1, "realb_p2p_return_map": 1, "realb_sf_rows_to_mma": 1,
     "realb_dispatch_index": 1,  # + 1 when NVFP4 rows are quantised (call() adds it)

@@ -161,12 +161,25 @@ __device__ __forceinline__ void ldg_nc_v8(uint32_t (&v)[8], const void* p) {
                : "l"(p));
 }
 
+// A K3 segment: one [G x rows_per_group, cols] bf16 matrix and its NVFP4 outputs. A
+// launch covers up to two segments (an expert's gate_up and down weights) as ONE
+// contiguous tile range, so the two matrices share one ramp-up and one tail.
+struct QSeg {
+  const __nv_bfloat16* x;
+  int64_t rows, cols;
+  int mt_per_group;
+  uint8_t* codes;
+  uint8_t* sf;
+};
+constexpr int kQMaxSegs = 2;
+struct QSegs {
+  QSeg s[kQMaxSegs];
+  int n;
+};
+
 template <int LAYOUT>
-__global__ void __launch_bounds__(256) quant_tiles_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
-                                                          int64_t cols, int mt_per_group, int G,
-                                                          const uint8_t* __restrict__ prec,
-                                                          uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
-                                                          int32_t* flag) {
+__global__ void __launch_bounds__(256) quant_tiles_kernel(const __grid_constant__ QSegs segs, int G,
+                                                          const uint8_t* __restrict__ prec, int32_t* flag) {
   __shared__ float2 tab[128];
   __shared__ int s_list[256];
   __shared__ int s_n;
@@ -178,40 +191,51 @@ __global__ void __launch_bounds__(256) quant_tiles_kernel(const __nv_bfloat16* _
     s_n = n;
   }
   __syncthreads();
-  const int64_t nkb = cols >> 4;
-  const int tiles_k = (int)(cols >> 6);
-  const int per_group = mt_per_group * tiles_k;
-  const int64_t tiles = (int64_t)s_n * per_group;
+  static_assert(kQMaxSegs == 2, "the walk below handles two segments");
+  const int64_t tiles0 = (int64_t)s_n * segs.s[0].mt_per_group * (segs.s[0].cols >> 6);
+  const int64_t tiles = tiles0 + (segs.n > 1 ? (int64_t)s_n * segs.s[1].mt_per_group * (segs.s[1].cols >> 6) : 0);
   const int64_t q = tiles / gridDim.x, rem = tiles % gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * q + min((int64_t)blockIdx.x, rem);
   const int64_t t1 = t0 + q + ((int64_t)blockIdx.x < rem ? 1 : 0);
   if (t0 >= t1) return;
   const int row_in = threadIdx.x >> 1, half = threadIdx.x & 1;
-  int g = (int)(t0 / per_group);
-  const int w0 = (int)(t0 - (int64_t)g * per_group);
-  int mt = w0 / tiles_k, kt = w0 - (w0 / tiles_k) * tiles_k;
-  auto row_of = [&](int gg, int mm) { return ((int64_t)s_list[gg] * mt_per_group + mm) * 128 + row_in; };
-  int64_t r = row_of(g, mt);
-  bool ok = r < rows;
+  // walk state: segment si, group g, m-tile mt, k-tile kt
+  int64_t w0 = t0;
+  const QSeg* S = &segs.s[0];
+  if (w0 >= tiles0) { w0 -= tiles0; S = &segs.s[1]; }
+  int tiles_k = (int)(S->cols >> 6);
+  int per_group = S->mt_per_group * tiles_k;
+  int g = (int)(w0 / per_group);
+  const int wg = (int)(w0 - (int64_t)g * per_group);
+  int mt = wg / tiles_k, kt = wg - (wg / tiles_k) * tiles_k;
+  auto row_of = [&](const QSeg* s_, int gg, int mm) {
+    return ((int64_t)s_list[gg] * s_->mt_per_group + mm) * 128 + row_in;
+  };
+  int64_t r = row_of(S, g, mt);
+  bool ok = r < S->rows;
   uint32_t cur[2][8], nxt[2][8];
   if (ok) {
-    const uint8_t* p = reinterpret_cast<const uint8_t*>(x + r * cols + kt * 64 + half * 32);
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(S->x + r * S->cols + kt * 64 + half * 32);
     ldg_nc_v8(cur[0], p);
     ldg_nc_v8(cur[1], p + 32);
   }
   for (int64_t t = t0; t < t1; ++t) {
+    const QSeg* S2 = S;
     int g2 = g, mt2 = mt, kt2 = kt + 1;
     if (kt2 == tiles_k) {
       kt2 = 0;
-      if (++mt2 == mt_per_group) { mt2 = 0; ++g2; }
+      if (++mt2 == S->mt_per_group) {
+        mt2 = 0;
+        if (++g2 == s_n) { g2 = 0; S2 = S + 1; }  // next segment (only reached if t + 1 < t1)
+      }
     }
     int64_t r2 = 0;
     bool ok2 = false;
     if (t + 1 < t1) {
-      r2 = row_of(g2, mt2);
-      ok2 = r2 < rows;
+      r2 = row_of(S2, g2, mt2);
+      ok2 = r2 < S2->rows;
       if (ok2) {
-        const uint8_t* p = reinterpret_cast<const uint8_t*>(x + r2 * cols + kt2 * 64 + half * 32);
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(S2->x + r2 * S2->cols + kt2 * 64 + half * 32);
         ldg_nc_v8(nxt[0], p);
         ldg_nc_v8(nxt[1], p + 32);
       }
@@ -222,15 +246,21 @@ __global__ void __launch_bounds__(256) quant_tiles_kernel(const __nv_bfloat16* _
       const uint2 ca = quant_block16_bf16_x2(cur[0], sa, nfa, tab);
       const uint2 cb = quant_block16_bf16_x2(cur[1], sb, nfb, tab);
       if (nfa || nfb) flag_nonfinite(flag);
-      *reinterpret_cast<uint4*>(codes + r * (cols >> 1) + kt * 32 + half * 16) = make_uint4(ca.x, ca.y, cb.x, cb.y);
+      const int64_t cols = S->cols, nkb = cols >> 4;
+      *reinterpret_cast<uint4*>(S->codes + r * (cols >> 1) + kt * 32 + half * 16) =
+          make_uint4(ca.x, ca.y, cb.x, cb.y);
       const int64_t kb0 = (int64_t)kt * 4 + half * 2;
       const int64_t so = LAYOUT == REALB_SF_FLAT ? r * nkb + kb0 : sf_mma_offset(r, kb0, nkb);
-      *reinterpret_cast<uint16_t*>(sf + so) = (uint16_t)(sa | (sb << 8));
+      *reinterpret_cast<uint16_t*>(S->sf + so) = (uint16_t)(sa | (sb << 8));
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       cur[0][i] = nxt[0][i];
       cur[1][i] = nxt[1][i];
+    }
+    if (S2 != S) {
+      S = S2;
+      tiles_k = (int)(S->cols >> 6);
     }
     g = g2; mt = mt2; kt = kt2; r = r2; ok = ok2;
   }
@@ -525,8 +555,10 @@ extern "C" int realb_quantize_nvfp4(const void* d_x, int dtype, int64_t rows, in
         const int64_t mt = (rows + 127) / 128;
         auto kern = flat ? quant_tiles_kernel<REALB_SF_FLAT> : quant_tiles_kernel<REALB_SF_MMA128x4>;
         const int grid = quant_grid(reinterpret_cast<const void*>(kern), mt * (cols / 64), max_ctas);
-        kern<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(d_x), rows, cols, (int)mt, 1, nullptr,
-                                   d_codes, d_sf, d_flag);
+        QSegs sg{};
+        sg.s[0] = QSeg{reinterpret_cast<const __nv_bfloat16*>(d_x), rows, cols, (int)mt, d_codes, d_sf};
+        sg.n = 1;
+        kern<<<grid, 256, 0, st>>>(sg, 1, nullptr, d_flag);
         return check_launch("realb_quantize_nvfp4");
       }
       return flat ? launch_quant(quant_kernel_bf16<REALB_SF_FLAT>, d_x, rows, cols, d_codes,
@@ -566,9 +598,11 @@ extern "C" int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows
     auto kern = quant_tiles_kernel<REALB_SF_MMA128x4>;
     const int grid = quant_grid(reinterpret_cast<const void*>(kern),
                                (int64_t)E * (rows_per_expert / 128) * (cols / 64), max_ctas);
-    kern<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(d_w),
-                                                 (int64_t)E * rows_per_expert, cols, (int)(rows_per_expert / 128), E,
-                                                 d_expert_prec, d_codes, d_sf, d_flag);
+    QSegs sg{};
+    sg.s[0] = QSeg{reinterpret_cast<const __nv_bfloat16*>(d_w), (int64_t)E * rows_per_expert, cols,
+                   (int)(rows_per_expert / 128), d_codes, d_sf};
+    sg.n = 1;
+    kern<<<grid, 256, 0, (cudaStream_t)stream>>>(sg, E, d_expert_prec, d_flag);
     return check_launch("realb_quantize_experts_nvfp4");
   }
   const int grid = quant_grid(reinterpret_cast<const void*>(quant_experts_kernel),
@@ -577,4 +611,37 @@ extern "C" int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows
       reinterpret_cast<const __nv_bfloat16*>(d_w), rows_per_expert, cols, E, d_expert_prec,
       d_codes, d_sf, d_flag);
   return check_launch("realb_quantize_experts_nvfp4");
+}
+
+extern "C" int realb_quantize_experts2_nvfp4(const void* d_w0, int64_t rows0_per_expert, int64_t cols0,
+                                             uint8_t* d_codes0, uint8_t* d_sf0, const void* d_w1,
+                                             int64_t rows1_per_expert, int64_t cols1, uint8_t* d_codes1,
+                                             uint8_t* d_sf1, int E, const uint8_t* d_expert_prec,
+                                             int32_t* d_flag, int max_ctas, void* stream) {
+  if (!d_w0 || !d_w1 || !d_expert_prec || !d_codes0 || !d_sf0 || !d_codes1 || !d_sf1 || E < 1 || E > 256 ||
+      rows0_per_expert <= 0 || rows0_per_expert % 128 || cols0 <= 0 || cols0 % 64 || rows1_per_expert <= 0 ||
+      rows1_per_expert % 128 || cols1 <= 0 || cols1 % 64 || rows0_per_expert / 128 > INT32_MAX / 64 ||
+      rows1_per_expert / 128 > INT32_MAX / 64) {
+    set_error("realb_quantize_experts2_nvfp4: bad arguments (E=%d rows/expert=%lld,%lld cols=%lld,%lld)", E,
+              (long long)rows0_per_expert, (long long)rows1_per_expert, (long long)cols0, (long long)cols1);
+    return REALB_EINVAL;
+  }
+  if (k3_version() != 2) {  // A/B forms (v1 / v3) quantise the two matrices in two launches
+    int rc = realb_quantize_experts_nvfp4(d_w0, E, rows0_per_expert, cols0, d_expert_prec, d_codes0, d_sf0, d_flag,
+                                          max_ctas, stream);
+    if (rc) return rc;
+    return realb_quantize_experts_nvfp4(d_w1, E, rows1_per_expert, cols1, d_expert_prec, d_codes1, d_sf1, d_flag,
+                                        max_ctas, stream);
+  }
+  auto kern = quant_tiles_kernel<REALB_SF_MMA128x4>;
+  const int64_t tiles = (int64_t)E * ((rows0_per_expert / 128) * (cols0 / 64) + (rows1_per_expert / 128) * (cols1 / 64));
+  const int grid = quant_grid(reinterpret_cast<const void*>(kern), tiles, max_ctas);
+  QSegs sg{};
+  sg.s[0] = QSeg{reinterpret_cast<const __nv_bfloat16*>(d_w0), (int64_t)E * rows0_per_expert, cols0,
+                 (int)(rows0_per_expert / 128), d_codes0, d_sf0};
+  sg.s[1] = QSeg{reinterpret_cast<const __nv_bfloat16*>(d_w1), (int64_t)E * rows1_per_expert, cols1,
+                 (int)(rows1_per_expert / 128), d_codes1, d_sf1};
+  sg.n = 2;
+  kern<<<grid, 256, 0, (cudaStream_t)stream>>>(sg, E, d_expert_prec, d_flag);
+  return check_launch("realb_quantize_experts2_nvfp4");
 }

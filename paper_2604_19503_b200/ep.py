@@ -430,12 +430,10 @@ class CudaEPOps:
         self.side.wait_stream(main)
         with torch.cuda.stream(self.side):
             ssp = _lib.stream_ptr(self.side)
-            _lib.call("realb_quantize_experts_nvfp4", self.local.w_gu.data_ptr(), El, 2 * I, H,
-                      self.prec_local.data_ptr(), ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
-                      self.flag.data_ptr(), self.quant_max_ctas, ssp)
-            _lib.call("realb_quantize_experts_nvfp4", self.local.w_d.data_ptr(), El, H, I,
-                      self.prec_local.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
-                      self.flag.data_ptr(), self.quant_max_ctas, ssp)
+            _lib.call("realb_quantize_experts2_nvfp4",
+                      self.local.w_gu.data_ptr(), 2 * I, H, ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
+                      self.local.w_d.data_ptr(), H, I, ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
+                      El, self.prec_local.data_ptr(), self.flag.data_ptr(), self.quant_max_ctas, ssp)
         # C2, direct: every row lands in its destination's GEMM operand at its final
         # grouped row (bf16, or NVFP4 + MMA-layout scales for a W4A4 destination)
         if rank_partial:  # + each W4A4-bound row's (token, slot) -> grouped row and its weight

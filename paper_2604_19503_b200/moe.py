@@ -472,12 +472,11 @@ class MoELayer:
             with torch.cuda.stream(k3_stream):
                 ssp = _lib.stream_ptr(k3_stream)
                 mark("k3_start", k3_stream)
-                _lib.call("realb_quantize_experts_nvfp4", self.w.w_gu.data_ptr(), E, 2 * I, H,
-                          self.prec_dev.data_ptr(), ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
-                          self.flag.data_ptr(), self.quant_max_ctas, ssp)
-                _lib.call("realb_quantize_experts_nvfp4", self.w.w_d.data_ptr(), E, H, I,
-                          self.prec_dev.data_ptr(), ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
-                          self.flag.data_ptr(), self.quant_max_ctas, ssp)
+                # gate_up and down weights of the W4A4 experts in one launch
+                _lib.call("realb_quantize_experts2_nvfp4",
+                          self.w.w_gu.data_ptr(), 2 * I, H, ws["wgu_codes"].data_ptr(), ws["wgu_sf"].data_ptr(),
+                          self.w.w_d.data_ptr(), H, I, ws["wd_codes"].data_ptr(), ws["wd_sf"].data_ptr(),
+                          E, self.prec_dev.data_ptr(), self.flag.data_ptr(), self.quant_max_ctas, ssp)
                 mark("k3_end", k3_stream)
         else:
             ws = None

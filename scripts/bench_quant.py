@@ -77,6 +77,27 @@ t = timed(lambda: b8.copy_(a8))
 out["same_size_copy_gate_up"] = dict(us=t * 1e6, GBps=2 * nb / t / 1e9)
 for ver in VERS:
     out[f"k3_{ver}_gate_up"]["frac_of_same_size_copy"] = out["same_size_copy_gate_up"]["us"] / out[f"k3_{ver}_gate_up"]["us"]
+# gate_up + down of the hot rank: one realb_quantize_experts2_nvfp4 launch vs the two
+# single-matrix launches back to back; a copy moving the same total bytes beside them
+os.environ["REALB_K3_VERSION"] = "2"
+both = lambda: _lib.call("realb_quantize_experts2_nvfp4", wgu.data_ptr(), 2 * I, H, cg.data_ptr(), sg.data_ptr(),
+                         wd.data_ptr(), H, I, cd.data_ptr(), sd.data_ptr(), E, prec.data_ptr(), flag.data_ptr(), 0,
+                         _lib.stream_ptr())
+def two():
+    for name, w, rpe, cols, c, s in shapes:
+        _lib.call("realb_quantize_experts_nvfp4", w.data_ptr(), E, rpe, cols, prec.data_ptr(), c.data_ptr(),
+                  s.data_ptr(), flag.data_ptr(), 0, _lib.stream_ptr())
+nb_all = int(8 * (2 * I * H + H * I) * 2.5625)
+a_all = torch.empty(nb_all // 2, dtype=torch.uint8, device="cuda")
+b_all = torch.empty_like(a_all)
+tb, tt, tc = [], [], []
+for rnd in range(5):
+    tb.append(timed(both, 11)); tt.append(timed(two, 11)); tc.append(timed(lambda: b_all.copy_(a_all), 11))
+tb, tt, tc = sorted(tb)[2], sorted(tt)[2], sorted(tc)[2]
+out["k3_v2_gate_up_and_down_one_launch"] = dict(us=tb * 1e6, GBps=nb_all / tb / 1e9, algorithmic_bytes=nb_all,
+                                                frac_of_same_size_copy=tc / tb)
+out["k3_v2_gate_up_and_down_two_launches"] = dict(us=tt * 1e6, GBps=nb_all / tt / 1e9, frac_of_same_size_copy=tc / tt)
+out["same_size_copy_gate_up_and_down"] = dict(us=tc * 1e6, GBps=nb_all / tc / 1e9)
 # parity spot check v1 == v2 (bit-exact codes / scales)
 outs = []
 for ver in VERS:

@@ -220,3 +220,43 @@ def test_weight_error_summary_bf16_weights(q):
     s = q.summary_from_sums(r["sums"], r["n"])
     assert abs(s.relative_rmse - rel) <= 1e-12 * rel and abs(s.rmse - rmse) <= 1e-12 * rmse
     assert 0.09 < s.relative_rmse < 0.12  # subnormal-scale regime (0.103)
+
+
+@pytest.mark.parametrize("max_ctas", [0, 7])
+def test_experts2_one_launch_bit_exact(q, max_ctas):
+    """realb_quantize_experts2_nvfp4: an expert set's gate_up [E*2I, H] and down
+    [E*H, I] weights in ONE launch (the tile range crosses from one matrix to the
+    other inside CTAs) == the oracle on each W4A4 expert's rows; W16A16 experts'
+    outputs untouched. Kimi-like I = 1408 (22 k-tiles) next to H = 2048 (32)."""
+    import torch
+    from paper_2604_19503_b200 import _lib
+
+    E, H, I = 5, 256, 1408
+    g = torch.Generator(device="cpu").manual_seed(11)
+    wgu = (torch.randn(E * 2 * I, H, generator=g) * 0.02).to(torch.bfloat16)
+    wd = (torch.randn(E * H, I, generator=g) * 0.02).to(torch.bfloat16)
+    prec = np.array([1, 0, 1, 1, 0], np.uint8)
+    dev = {k: v.cuda() for k, v in dict(wgu=wgu, wd=wd).items()}
+    cg = torch.full((E * 2 * I, H // 2), 0xAB, dtype=torch.uint8, device="cuda")
+    sg = torch.full((E * 2 * I * H // 16,), 0xAB, dtype=torch.uint8, device="cuda")
+    cd = torch.full((E * H, I // 2), 0xAB, dtype=torch.uint8, device="cuda")
+    sd = torch.full((E * H * I // 16,), 0xAB, dtype=torch.uint8, device="cuda")
+    pd = torch.from_numpy(prec).cuda()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("realb_quantize_experts2_nvfp4", dev["wgu"].data_ptr(), 2 * I, H, cg.data_ptr(), sg.data_ptr(),
+              dev["wd"].data_ptr(), H, I, cd.data_ptr(), sd.data_ptr(), E, pd.data_ptr(), flag.data_ptr(),
+              max_ctas, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0
+    for w, c, sfm, rpe, cols in ((wgu, cg, sg, 2 * I, H), (wd, cd, sd, H, I)):
+        c = c.cpu().numpy()
+        sfm = sfm.cpu().numpy().reshape(E, -1)
+        for e in range(E):
+            rows = slice(e * rpe, (e + 1) * rpe)
+            if prec[e]:
+                bits = w[rows].view(torch.int16).numpy().view(np.uint16)
+                oc, osf = oracle.quantize_bf16(bits)
+                assert (c[rows] == oc).all()
+                assert (q.sf_mma_to_flat(sfm[e], rpe, cols) == osf).all()
+            else:
+                assert (c[rows] == 0xAB).all() and (sfm[e] == 0xAB).all()
