@@ -246,10 +246,14 @@ __global__ void __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
           if constexpr (CL == 2) {
             const uint32_t fb = full0 + (uint32_t)stage * 8u;
-            if (crank == 0)
-              mbar_arrive_expect_tx(&full[stage], 2 * S::B_BYTES + S::A_BYTES + (dummy1 ? 0 : S::A_BYTES));
-            if (!dummy) tma_load_2d_2sm(sa, &tmA, fb, kb * kBK, a_row);
-            tma_load_2d_2sm(sa + S::A_BYTES, &tmB, fb, kb * kBK, brow + (int)crank * (BN / 2));
+            if (dbg & 2u) {  // debug: no operand loads (MMA + epilogue only)
+              if (crank == 0) mbar_arrive(&full[stage]);
+            } else {
+              if (crank == 0)
+                mbar_arrive_expect_tx(&full[stage], 2 * S::B_BYTES + S::A_BYTES + (dummy1 ? 0 : S::A_BYTES));
+              if (!dummy) tma_load_2d_2sm(sa, &tmA, fb, kb * kBK, a_row);
+              tma_load_2d_2sm(sa + S::A_BYTES, &tmB, fb, kb * kBK, brow + (int)crank * (BN / 2));
+            }
           } else if (dbg & 2u) {  // debug: no operand loads (MMA + epilogue only)
             mbar_arrive(&full[stage]);
           } else {
