@@ -29,23 +29,20 @@ struct PlanParams {
 __device__ void plan_on_device(const int32_t* ev, int E, const PlanParams& pp, uint8_t* prec,
                                int32_t* plan_out) {  // ev, prec: shared memory
   const int R = pp.R, epr = E / R;
-  long long rv[256], rt[256];
-  long long total = 0;
-  for (int r = 0; r < R; ++r) {
-    long long v = 0, t = 0;
-    for (int e = r * epr; e < (r + 1) * epr; ++e) { v += ev[2 * e]; t += ev[2 * e + 1]; }
-    rv[r] = v; rt[r] = v + t;
-    total += v + t;
-  }
+  long long total = 0;  // integer sums: exact in any order
+  for (int e = 0; e < E; ++e) total += (long long)ev[2 * e] + ev[2 * e + 1];
   int active = 0, nacc = 0;
-  for (int r = 0; r < R; ++r) {
+  for (int r = 0; r < R; ++r) {  // per-rank (v, v + t), recomputed: no per-rank arrays on the stack
+    long long v = 0, tt = 0;
+    for (int e = r * epr; e < (r + 1) * epr; ++e) { v += ev[2 * e]; tt += ev[2 * e + 1]; }
+    const long long rv_r = v, rt_r = v + tt;
     uint32_t flags = 0;
     if (pp.strategy == 1) {
       flags = 7u;
     } else if (pp.strategy == 2 && !(total < pp.thr || total == 0)) {
       const double ideal = (double)total / (double)R;
-      const bool hot = (double)rt[r] / ideal > pp.C;
-      const bool vis = pp.isolated ? rt[r] > 0 : (rt[r] > 0 && (double)rv[r] / (double)rt[r] > pp.Md);
+      const bool hot = (double)rt_r / ideal > pp.C;
+      const bool vis = pp.isolated ? rt_r > 0 : (rt_r > 0 && (double)rv_r / (double)rt_r > pp.Md);
       flags = (hot ? 1u : 0u) | (vis ? 2u : 0u) | ((hot && vis) ? 4u : 0u);
     }
     if (flags & 4u) ++nacc;
@@ -74,11 +71,17 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
   // chunk range of group g (contiguous, for the offset scan)
   const int per = (nchunks + G - 1) / G;
   const int c0 = act ? min(nchunks, g * per) : 0, c1 = act ? min(nchunks, c0 + per) : 0;
+  // chunk counts in blocks of 8 (all loads of a block in flight; one 8-B load per
+  // (chunk, expert) pair of counts)
+  constexpr int kAB = 8;
+  const int2* cc2 = reinterpret_cast<const int2*>(cc);
   int v = 0, t = 0;
-#pragma unroll 4
-  for (int c = c0; c < c1; ++c) {
-    v += cc[((int64_t)c * E + e) * 2];
-    t += cc[((int64_t)c * E + e) * 2 + 1];
+  for (int cb = c0; cb < c1; cb += kAB) {
+    int2 q[kAB];
+#pragma unroll
+    for (int i = 0; i < kAB; ++i) q[i] = cb + i < c1 ? __ldg(cc2 + (int64_t)(cb + i) * E + e) : make_int2(0, 0);
+#pragma unroll
+    for (int i = 0; i < kAB; ++i) { v += q[i].x; t += q[i].y; }
   }
   s_v[threadIdx.x] = v;
   s_t[threadIdx.x] = t;
@@ -111,23 +114,29 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
     // 4 scanned quantities: padded rows, and for p in {0,1}: (flag, m-tiles, pairs)
     int v[7] = {padded, pe == 0, pe == 0 ? m : 0, pe == 0 ? (m + 1) / 2 : 0,
                 pe == 1, pe == 1 ? m : 0, pe == 1 ? (m + 1) / 2 : 0};
+    // inclusive scans: within each warp by shuffles, then the warps' totals
     int incl[7];
+    const int ln = e & 31, wp = e >> 5;
 #pragma unroll
-    for (int j = 0; j < 7; ++j) incl[j] = v[j];
-    for (int off = 1; off < 256; off <<= 1) {
-      if (e < 256) {
+    for (int j = 0; j < 7; ++j) {
+      int x = v[j];
 #pragma unroll
-        for (int j = 0; j < 7; ++j) s_scan[j * 256 + e] = incl[j];
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (ln >= off) x += y;
       }
-      __syncthreads();
-      if (e < 256 && e >= off) {
+      incl[j] = x;
+      if (e < 256 && ln == 31) s_scan[j * 8 + wp] = x;  // warp totals
+    }
+    __syncthreads();
+    if (e < 256) {
 #pragma unroll
-        for (int j = 0; j < 7; ++j) incl[j] += s_scan[j * 256 + e - off];
-      }
-      __syncthreads();
+      for (int j = 0; j < 7; ++j)
+        for (int w = 0; w < wp; ++w) incl[j] += s_scan[j * 8 + w];
     }
     if (in) {
       s_start[e] = incl[0] - v[0];
+#pragma unroll
       for (int p = 0; p < 2; ++p) {
         if (pe != p) continue;
         const int g = incl[1 + 3 * p] - 1;  // exclusive rank among experts of class p
@@ -139,6 +148,7 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
     if (e == E - 1) {
       layout[0] = incl[0];
       for (int w = 3; w < 8; ++w) layout[w] = 0;  // GEMM tile counters (grouped.cuh)
+#pragma unroll
       for (int p = 0; p < 2; ++p) {
         const int G = incl[1 + 3 * p];
         layout[1 + p] = G;
@@ -158,9 +168,16 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
     int run = s_start[e];
     for (int j = 0; j < g; ++j) run += s_v[j * E + e] + s_t[j * E + e];
     int32_t* co = layout + LayoutView::off_chunk(E);
-    for (int c = c0; c < c1; ++c) {
-      co[(int64_t)c * E + e] = run;
-      run += cc[((int64_t)c * E + e) * 2] + cc[((int64_t)c * E + e) * 2 + 1];
+    for (int cb = c0; cb < c1; cb += kAB) {  // loads of a block first, then its offsets
+      int2 q[kAB];
+#pragma unroll
+      for (int i = 0; i < kAB; ++i) q[i] = cb + i < c1 ? __ldg(cc2 + (int64_t)(cb + i) * E + e) : make_int2(0, 0);
+#pragma unroll
+      for (int i = 0; i < kAB; ++i)
+        if (cb + i < c1) {
+          co[(int64_t)(cb + i) * E + e] = run;
+          run += q[i].x + q[i].y;
+        }
     }
   }
 }
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(256) index_rows_kernel(const __nv_bfloat16* __
 
 // ----------------------------------------------------------------- combine
 template <int K>
-__global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ rows,
+__global__ void __launch_bounds__(256, 1) combine_kernel(const __nv_bfloat16* __restrict__ rows,
                                                       const int32_t* __restrict__ pos,
                                                       const float* __restrict__ w, int T, int H,
                                                       const __nv_bfloat16* __restrict__ addend,
