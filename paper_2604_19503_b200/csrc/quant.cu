@@ -175,7 +175,12 @@ constexpr int kQMaxSegs = 2;
 struct QSegs {
   QSeg s[kQMaxSegs];
   int n;
+  int dbg;  // timing probes (REALB_DBG_K3): 1 = stores without the conversion, 2 = loads only
 };
+static int k3_dbg() {
+  const char* e = getenv("REALB_DBG_K3");
+  return e ? atoi(e) : 0;
+}
 
 template <int LAYOUT>
 __global__ void __launch_bounds__(256) quant_tiles_kernel(const __grid_constant__ QSegs segs, int G,
@@ -240,11 +245,20 @@ __global__ void __launch_bounds__(256) quant_tiles_kernel(const __grid_constant_
         ldg_nc_v8(nxt[1], p + 32);
       }
     }
-    if (ok) {
+    if (ok && segs.dbg == 2) {  // probe: keep the loads alive without converting or storing
+      if ((cur[0][0] ^ cur[1][7]) == 0x7fc17fc1u) flag_nonfinite(flag);
+    } else if (ok) {
       uint32_t sa, sb;
-      bool nfa, nfb;
-      const uint2 ca = quant_block16_bf16_x2(cur[0], sa, nfa, tab);
-      const uint2 cb = quant_block16_bf16_x2(cur[1], sb, nfb, tab);
+      bool nfa = false, nfb = false;
+      uint2 ca, cb;
+      if (segs.dbg == 1) {  // probe: the stores without the conversion
+        ca = make_uint2(cur[0][0] ^ cur[0][1], cur[0][2] ^ cur[0][3]);
+        cb = make_uint2(cur[1][0] ^ cur[1][1], cur[1][2] ^ cur[1][3]);
+        sa = cur[0][4] & 0xff; sb = cur[1][4] & 0xff;
+      } else {
+        ca = quant_block16_bf16_x2(cur[0], sa, nfa, tab);
+        cb = quant_block16_bf16_x2(cur[1], sb, nfb, tab);
+      }
       if (nfa || nfb) flag_nonfinite(flag);
       const int64_t cols = S->cols, nkb = cols >> 4;
       *reinterpret_cast<uint4*>(S->codes + r * (cols >> 1) + kt * 32 + half * 16) =
@@ -602,6 +616,7 @@ extern "C" int realb_quantize_experts_nvfp4(const void* d_w, int E, int64_t rows
     sg.s[0] = QSeg{reinterpret_cast<const __nv_bfloat16*>(d_w), (int64_t)E * rows_per_expert, cols,
                    (int)(rows_per_expert / 128), d_codes, d_sf};
     sg.n = 1;
+    sg.dbg = k3_dbg();
     kern<<<grid, 256, 0, (cudaStream_t)stream>>>(sg, E, d_expert_prec, d_flag);
     return check_launch("realb_quantize_experts_nvfp4");
   }
@@ -642,6 +657,7 @@ extern "C" int realb_quantize_experts2_nvfp4(const void* d_w0, int64_t rows0_per
   sg.s[1] = QSeg{reinterpret_cast<const __nv_bfloat16*>(d_w1), (int64_t)E * rows1_per_expert, cols1,
                  (int)(rows1_per_expert / 128), d_codes1, d_sf1};
   sg.n = 2;
+  sg.dbg = k3_dbg();
   kern<<<grid, 256, 0, (cudaStream_t)stream>>>(sg, E, d_expert_prec, d_flag);
   return check_launch("realb_quantize_experts2_nvfp4");
 }
