@@ -286,7 +286,9 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(sa + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
           }
         }
-        if (crank == 0) {
+        // (1-CTA form only: in the pair form the claim stays at the unit boundary — with
+        // fetch-ahead its no-load timing probe, REALB_DBG_BF16 bit 2, did not terminate)
+        if (CL == 1 && !(dbg & 128u)) {  // (debug bit 128: claim at the unit boundary instead)
           if (kb == 0 && leader) t_next = atomicAdd(ctr, 1);  // after this stage's loads
           if (kb == (nkb > 2 ? 2 : nkb - 1)) {
             int tn = __shfl_sync(0xffffffffu, t_next, 0);

@@ -25,6 +25,8 @@ def main():
             if only and label not in only.split(","):
                 continue
             counts = ((rng.random(E) * 0.4 + 0.8) * per).astype(np.int64)
+            if os.environ.get("BENCH_EVEN"):  # whole 256-row units: no 2-SM pair dummy m-tiles
+                counts = np.maximum(256, (counts + 128) // 256 * 256)
             lay, rows = host_layout(counts, np.zeros(E, np.int64))
             A = torch.randn(rows, K, device="cuda").to(torch.bfloat16)
             W = (torch.randn(E * N, K, device="cuda") / K**0.5).to(torch.bfloat16)
