@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmOut);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], GATHER ? 1 + 32 * kGatherWarps : 1);  // gather: + one noinc arrive per loader lane
+      // gather: + one noinc arrive per loader lane; the pair's no-load probe: one arrive
+      // from each CTA's producer, so neither producer can be lapped by the MMA (a waiter
+      // two phases behind an mbarrier never sees its phase complete)
+      mbar_init(&full[s], GATHER ? 1 + 32 * kGatherWarps : (CL == 2 && (dbg & 2u)) ? 2 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -270,8 +273,8 @@ __global__ void __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
           if constexpr (CL == 2) {
             const uint32_t fb = full0 + (uint32_t)stage * 8u;
-            if (dbg & 2u) {  // debug: no operand loads (MMA + epilogue only)
-              if (crank == 0) mbar_arrive(&full[stage]);
+            if (dbg & 2u) {  // debug: no operand loads (MMA + epilogue only); both producers arrive
+              mbar_arrive_cluster(fb);
             } else {
               if (crank == 0)
                 mbar_arrive_expect_tx(&full[stage], 2 * S::B_BYTES + S::A_BYTES + (dummy1 ? 0 : S::A_BYTES));
@@ -286,8 +289,7 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(sa + S::A_BYTES, &tmB, &full[stage], kb * kBK, brow);
           }
         }
-        // (1-CTA form only: in the pair form the claim stays at the unit boundary — with
-        // fetch-ahead its no-load timing probe, REALB_DBG_BF16 bit 2, did not terminate)
+        // (1-CTA form only; the pair form claims at the unit boundary as before)
         if (CL == 1 && !(dbg & 128u)) {  // (debug bit 128: claim at the unit boundary instead)
           if (kb == 0 && leader) t_next = atomicAdd(ctr, 1);  // after this stage's loads
           if (kb == (nkb > 2 ? 2 : nkb - 1)) {
