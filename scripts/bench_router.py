@@ -1,5 +1,6 @@
 """Router microbenchmark with debug variants (REALB_DBG_ROUTER: 1 no epilogue, 4 no loads,
-16 no logits stores; REALB_ROUTER_NACC=1 forces one K-loop accumulator)."""
+16 no logits stores, 32 in-kernel phase cycles written into topk_w; REALB_ROUTER_STAGES caps
+the ring depth). BENCH_T / BENCH_STAGES / BENCH_DBG select the runs."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -15,11 +16,9 @@ for T in [int(t) for t in os.environ.get("BENCH_T", "8192,65536").split(",")]:
     bias = torch.zeros(E, device="cuda")
     f = lambda: _lib.call("realb_router_topk_stats", x.data_ptr(), router.data_ptr(), bias.data_ptr(), mod.data_ptr(), T, H, E, k, 1, 2.446, 1e-12, logits.data_ptr(), idx.data_ptr(), w.data_ptr(), cc.data_ptr(), _lib.stream_ptr())
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
-    for stages, nacc, dbg in [(s_, n_, d_) for s_ in os.environ.get("BENCH_STAGES", "4,8").split(",")
-                              for n_ in os.environ.get("BENCH_NACC", "0,1").split(",")
-                              for d_ in os.environ.get("BENCH_DBG", "0,1,4,5,13").split(",")]:
+    for stages, dbg in [(s_, d_) for s_ in os.environ.get("BENCH_STAGES", "12").split(",")
+                        for d_ in os.environ.get("BENCH_DBG", "0,1,4,5").split(",")]:
         os.environ["REALB_ROUTER_STAGES"] = stages
-        os.environ["REALB_ROUTER_NACC"] = nacc
         if True:
             os.environ["REALB_DBG_ROUTER"] = str(dbg)
             for _ in range(3): f()
@@ -34,4 +33,4 @@ for T in [int(t) for t in os.environ.get("BENCH_T", "8192,65536").split(",")]:
                 st = w.view(torch.int32)[::64, :6].cpu()
                 print("phase cycles (done, pass1+b1, merge+b2, pass2+b3, select, out+bar): median",
                       st.median(dim=0).values.tolist(), "max", st.max(dim=0).values.tolist())
-            print(f"T={T} stages={stages} nacc={nacc} dbg={dbg} {t*1e3:8.1f} us  {T*H*2/t/1e9:8.1f} GB/s", flush=True)
+            print(f"T={T} stages={stages} dbg={dbg} {t*1e3:8.1f} us  {T*H*2/t/1e6:8.1f} GB/s (x only, event-timed)", flush=True)
