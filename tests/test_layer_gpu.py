@@ -48,7 +48,9 @@ def build_layer(shape, T, R=1, seed=2024):
 
 
 @pytest.mark.parametrize("name,E,T", [("tiny", None, 1024), ("kimi", None, 1000), ("qwen", None, 777),
-                                      ("ernie_vision", None, 512)])
+                                      ("ernie_vision", None, 512),
+                                      ("kimi", 22, 300),     # E % 4 != 0: logits stored per element, not by TMA
+                                      ("qwen", 256, 333)])   # the widest router tile (EPAD 256, 8 logit boxes)
 def test_router_d1_contract(name, E, T):
     shape = small(SHAPES[name], E)
     layer, x, mod, router, *_ , planned = build_layer(shape, T)
