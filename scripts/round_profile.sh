@@ -8,6 +8,7 @@ R=${1:-r02}
 O=gpurun_out/$R
 mkdir -p "$O"
 rm -f gpurun_out/parity_log.jsonl
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > "$O/smoke.log" 2>&1; tail -2 "$O/smoke.log"
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > "$O/gputest.log" 2>&1; tail -3 "$O/gputest.log"
 cp gpurun_out/parity_log.jsonl "$O/parity_log.jsonl" 2>/dev/null
 timeout 600 python bench.py --steps 20 --warmup 5 > "$O/bench.json" 2> "$O/bench.err"; tail -c 300 "$O/bench.json"
