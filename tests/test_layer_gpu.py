@@ -638,3 +638,40 @@ def test_layer_rank_partial_combine_vs_oracle(name, E, T, strategy, R, parity_lo
         assert torch.equal(res.y, y_plain)
     else:  # the partial rounding is real: the result differs from the plain combine somewhere
         assert not torch.equal(res.y, y_plain)
+
+
+@pytest.mark.parametrize("E,k", [(40, 1), (48, 4), (200, 8), (64, 2)])
+@pytest.mark.parametrize("scoring", [_lib.SCORE_SOFTMAX_RENORM, _lib.SCORE_SIGMOID_RENORM, _lib.SCORE_SOFTMAX_CLAMPNORM])
+def test_router_kernel_shapes_and_scorings(E, k, scoring):
+    """realb_router_topk_stats on shapes the model configs do not use: padding columns
+    (E = 40 -> 48-wide tile), an odd number of 16-column groups (E = 48), E = 200, every
+    top-k the kernel supports next to the scoring families, and a nonzero score bias
+    for the sigmoid family. Against the oracle on the device's own logits (D1)."""
+    T, H = 700, 256
+    g = torch.Generator(device="cuda").manual_seed(E * 10 + k + scoring)
+    x = torch.randn(T, H, generator=g, device="cuda").to(torch.bfloat16)
+    wg = (torch.randn(E, H, generator=g, device="cuda") / H ** 0.5).to(torch.bfloat16)
+    mod = torch.randint(0, 2, (T,), generator=g, device="cuda").to(torch.uint8)
+    bias = (torch.randn(E, generator=g, device="cuda") * 0.1) if scoring == _lib.SCORE_SIGMOID_RENORM else None
+    nch = (T + 63) // 64
+    logits = torch.empty(T, E, device="cuda")
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(T, k, device="cuda")
+    cc = torch.empty(nch, E, 2, dtype=torch.int32, device="cuda")
+    rs, nm = 2.5, 1e-12
+    _lib.call("realb_router_topk_stats", x.data_ptr(), wg.data_ptr(), bias.data_ptr() if bias is not None else 0,
+              mod.data_ptr(), T, H, E, k, scoring, rs, nm, logits.data_ptr(), idx.data_ptr(), w.data_ptr(),
+              cc.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    lg = logits.cpu().numpy()
+    _, idx_ref, w_ref = moe_ref.route(None, None, k, scoring, bias=bias.cpu().numpy() if bias is not None else None,
+                                      routed_scaling=rs if scoring == _lib.SCORE_SIGMOID_RENORM else 1.0,
+                                      norm_min=nm, logits=lg)
+    assert (idx.cpu().numpy() == idx_ref).all()
+    np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=2e-5, atol=2e-6)
+    lref = x.float().cpu().numpy() @ wg.float().cpu().numpy().T
+    assert np.abs(lg - lref).max() <= 1e-3 * max(1.0, np.abs(lref).max())
+    m = mod.cpu().numpy()
+    for c in range(nch):
+        sl = slice(64 * c, min(T, 64 * c + 64))
+        assert (cc[c].cpu().numpy() == moe_ref.expert_counts(idx_ref[sl], m[sl], E)).all()
