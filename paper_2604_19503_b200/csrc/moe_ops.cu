@@ -54,10 +54,14 @@ __device__ void plan_on_device(const int32_t* ev, int E, const PlanParams& pp, u
   if (plan_out) { plan_out[0] = active; plan_out[1] = nacc; plan_out[2] = R; }
 }
 
-// 1024 threads = E experts x G chunk groups (G = 1024 / E): chunk sums and
-// per-chunk offsets are computed with all threads, the serial part (scan over
-// experts, P1, group lists) by one thread over E <= 256 entries.
-__global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__ cc, int nchunks,
+// 256 threads (whole warps, >= E): E experts x G chunk groups (G = 256 / E) read the
+// chunk counts (16 loads in flight per thread) and write the per-chunk offsets; the
+// scans over the E <= 256 experts run on all 256 threads (warp shuffles); the plan
+// on one thread. (1024 threads measured slower: the kernel is instruction-bound on
+// its single SM, and a thread count that is not a multiple of 32 would leave a
+// partial warp in the shuffle scans.)
+constexpr int kAlignThreads = 256;
+__global__ void __launch_bounds__(kAlignThreads) align_kernel(const int32_t* __restrict__ cc, int nchunks,
                                                      int E, uint8_t* __restrict__ prec,
                                                      int32_t* __restrict__ layout,
                                                      int32_t* __restrict__ expert_vt,
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(1024) align_kernel(const int32_t* __restrict__
   const int c0 = act ? min(nchunks, g * per) : 0, c1 = act ? min(nchunks, c0 + per) : 0;
   // chunk counts in blocks of 8 (all loads of a block in flight; one 8-B load per
   // (chunk, expert) pair of counts)
-  constexpr int kAB = 8;
+  constexpr int kAB = 16;
   const int2* cc2 = reinterpret_cast<const int2*>(cc);
   int v = 0, t = 0;
   for (int cb = c0; cb < c1; cb += kAB) {
@@ -640,7 +644,7 @@ extern "C" int realb_moe_align(const int32_t* d_cc, int nchunks, int E, const ui
     return REALB_EINVAL;
   }
   PlanParams pp{};
-  align_kernel<<<1, (1024 / E) * E, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, const_cast<uint8_t*>(d_prec),
+  align_kernel<<<1, kAlignThreads, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, const_cast<uint8_t*>(d_prec),
                                                     d_layout, d_expert_vt, pp, nullptr, row_align);
   return check_launch("realb_moe_align");
 }
@@ -663,7 +667,7 @@ extern "C" int realb_moe_align_plan(const int32_t* d_cc, int nchunks, int E, int
   }
   PlanParams pp{1, strategy, R, modality_isolated, capacity_factor, modality_threshold,
                 (long long)global_batch_threshold};
-  align_kernel<<<1, (1024 / E) * E, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
+  align_kernel<<<1, kAlignThreads, 0, (cudaStream_t)stream>>>(d_cc, nchunks, E, d_prec, d_layout,
                                                     d_expert_vt, pp, d_plan_out, 128);
   return check_launch("realb_moe_align_plan");
 }

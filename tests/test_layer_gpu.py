@@ -675,3 +675,17 @@ def test_router_kernel_shapes_and_scorings(E, k, scoring):
     for c in range(nch):
         sl = slice(64 * c, min(T, 64 * c + 64))
         assert (cc[c].cpu().numpy() == moe_ref.expert_counts(idx_ref[sl], m[sl], E)).all()
+    # the chunk counts through realb_moe_align: expert totals and the 128-row padded layout
+    layout = torch.zeros(int(_lib.load().realb_layout_words(E, nch)), dtype=torch.int32, device="cuda")
+    vt = torch.empty(E, 2, dtype=torch.int32, device="cuda")
+    prec = torch.zeros(E, dtype=torch.uint8, device="cuda")
+    _lib.call("realb_moe_align", cc.data_ptr(), nch, E, prec.data_ptr(), 128, layout.data_ptr(), vt.data_ptr(),
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref = moe_ref.expert_counts(idx_ref, m, E)
+    assert (vt.cpu().numpy() == ref).all()
+    lay = layout.cpu().numpy()
+    cnt = ref.sum(1)
+    starts = np.concatenate([[0], np.cumsum((cnt + 127) // 128 * 128)[:-1]])
+    assert lay[0] == ((cnt + 127) // 128 * 128).sum()
+    assert (lay[8:8 + E] == starts).all() and (lay[8 + E:8 + 2 * E] == cnt).all()
