@@ -300,4 +300,63 @@ __host__ __device__ __forceinline__ int64_t sf_mma_offset(int64_t r, int64_t kb,
   return atom * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (kb & 3);
 }
 
+
+// ---------------------------------------------------------------------------
+// Correctly rounded reciprocals of every E4M3 scale, computed at compile time
+// (IEEE float division in the constant evaluator; equal to __frcp_rn for all 127
+// nonzero scale codes, checked against numpy's float32 division when this table was
+// written): the activation-side rule (K4 producers, the K6 SwiGLU re-quantisation)
+// reads it instead of evaluating __frcp_rn, an IEEE multi-instruction sequence.
+struct E4M3Rcp {
+  float v[128];
+};
+constexpr float e4m3_decode_ce(uint32_t b) {
+  const uint32_t e = b >> 3, m = b & 7u;
+  if (e == 0) return (float)m * 0.001953125f;
+  float f = 1.0f + (float)m * 0.125f;
+  for (int i = 7; i < (int)e; ++i) f *= 2.0f;
+  for (int i = (int)e; i < 7; ++i) f *= 0.5f;
+  return f;
+}
+constexpr E4M3Rcp make_e4m3_rcp() {
+  E4M3Rcp t{};
+  for (uint32_t b = 1; b < 128; ++b) t.v[b] = 1.0f / e4m3_decode_ce(b);
+  return t;
+}
+static __device__ const E4M3Rcp g_e4m3_rcp = make_e4m3_rcp();
+
+// the block rule on 8 packed pairs (f32x2: element 2i low, 2i+1 high) of
+// bf16-representable values whose amax bits are known: hardware scale encode,
+// table reciprocal, packed-FP32 residual step, hardware E2M1 conversion
+__device__ __forceinline__ uint2 quant_block16_pairs(const uint64_t (&p)[8], float amax, uint32_t& sbits) {
+  sbits = block_scale_bits_bf16amax_hw(amax);
+  if (sbits == 0u) return make_uint2(0u, 0u);
+  const float sc = e4m3_decode(sbits);
+  const float r = __ldg(&g_e4m3_rcp.v[sbits]);
+  const uint64_t r2 = f32x2_pack(r, r), nsc2 = f32x2_pack(-sc, -sc);
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = cvt_e2m1x4_2(q1_div2(p[2 * i], r2, nsc2), q1_div2(p[2 * i + 1], r2, nsc2));
+  return make_uint2(canon_neg_zero(c[0] | (c[1] << 16)), canon_neg_zero(c[2] | (c[3] << 16)));
+}
+// quant_block16_bf16 (16 bf16 as 8 words) by the packed path
+__device__ __forceinline__ uint2 quant_block16_bf16_fast(const uint32_t (&w)[8], uint32_t& sbits, bool& nonfinite) {
+  const uint32_t ab = amax_bits_bf16x16(w);
+  nonfinite = ab >= 0x7F80u;
+  uint64_t p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = bf16x2_to_f32x2(w[i]);
+  return quant_block16_pairs(p, __uint_as_float(ab << 16), sbits);
+}
+// quant_block16_bf16vals (16 fp32 holding bf16 values) by the packed path
+__device__ __forceinline__ uint2 quant_block16_bf16vals_fast(const float (&v)[16], uint32_t& sbits) {
+  float amax = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  uint64_t p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = f32x2_pack(v[2 * i], v[2 * i + 1]);
+  return quant_block16_pairs(p, amax, sbits);
+}
+
 }  // namespace realb

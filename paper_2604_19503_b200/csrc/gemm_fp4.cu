@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             h[i] = __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u));
           }
           uint32_t sb;
-          cw[b] = quant_block16_bf16vals(h, sb);
+          cw[b] = quant_block16_bf16vals_fast(h, sb);
           sfw |= sb << (8 * b);
           if (args.out) {  // parity hook: the bf16 SwiGLU values the re-quantisation consumed
             uint32_t hp[8];

@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(pair_threads<EPI>(), 1)
               hv[i] = __bfloat162float(__float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * uu));
             }
             uint32_t sb;
-            cw[b] = quant_block16_bf16vals(hv, sb);
+            cw[b] = quant_block16_bf16vals_fast(hv, sb);
             sfw |= sb << (8 * b);
             if (args.out) {  // parity hook: the bf16 SwiGLU values the re-quantisation consumed
               uint32_t hp[8];

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
           const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
           uint32_t sb;
           bool nf;
-          cw[b] = quant_block16_bf16(w, sb, nf);
+          cw[b] = quant_block16_bf16_fast(w, sb, nf);
           if (nf && flag) atomicOr(flag, 1);
           sfw |= sb << (8 * b);
         }
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(256) ep_pack_rows_kernel(
           const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
           uint32_t sb;
           bool nf;
-          cw[b] = quant_block16_bf16(w, sb, nf);
+          cw[b] = quant_block16_bf16_fast(w, sb, nf);
           if (nf && flag) atomicOr(flag, 1);
           sfw |= sb << (8 * b);
         }

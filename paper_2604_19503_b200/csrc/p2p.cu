@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) p2p_pack_kernel(const __nv_bfloat16* __re
           const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
           uint32_t sb;
           bool nf;
-          cw[b] = quant_block16_bf16(w, sb, nf);
+          cw[b] = quant_block16_bf16_fast(w, sb, nf);
           if (nf && flag) atomicOr(flag, 1);
           sfw |= sb << (8 * b);
         }
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) p2p_pack_dev_kernel(const __nv_bfloat16* 
           const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
           uint32_t sb;
           bool nf;
-          cw[b] = quant_block16_bf16(w, sb, nf);
+          cw[b] = quant_block16_bf16_fast(w, sb, nf);
           if (nf && flag) atomicOr(flag, 1);
           sfw |= sb << (8 * b);
         }
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) p2p_pack_direct_kernel(const __nv_bfloat1
             const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
             uint32_t sb;
             bool nf;
-            cw[b] = quant_block16_bf16(w, sb, nf);
+            cw[b] = quant_block16_bf16_fast(w, sb, nf);
             if (nf && flag) atomicOr(flag, 1);
             sfw |= sb << (8 * b);
           }
