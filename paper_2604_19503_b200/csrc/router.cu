@@ -399,21 +399,21 @@ __global__ void __launch_bounds__(256, 1)
       // routing weights from the selected logits
       float w[KK];
       float wsum = 0.f;
-      const float inv_sum = __frcp_rn(run_sum);
+      const float inv_sum = __fdividef(1.0f, run_sum);  // MUFU.RCP (the IEEE __frcp_rn is a long sequence)
 #pragma unroll
       for (int j = 0; j < KK; ++j) {
         float p;
         if (scoring == REALB_SCORE_SIGMOID_RENORM)
-          p = __frcp_rn(1.0f + __expf(-ls[j]));
+          p = __fdividef(1.0f, 1.0f + __expf(-ls[j]));
         else
           p = __expf(ls[j] - run_max) * inv_sum;  // softmax probability
         w[j] = p;
         wsum += p;
       }
       float scale;
-      if (scoring == REALB_SCORE_SOFTMAX_RENORM) scale = __frcp_rn(wsum);
-      else if (scoring == REALB_SCORE_SIGMOID_RENORM) scale = routed_scaling * __frcp_rn(wsum);
-      else scale = __frcp_rn(fmaxf(wsum, norm_min));
+      if (scoring == REALB_SCORE_SOFTMAX_RENORM) scale = __fdividef(1.0f, wsum);
+      else if (scoring == REALB_SCORE_SIGMOID_RENORM) scale = __fdividef(routed_scaling, wsum);
+      else scale = __fdividef(1.0f, fmaxf(wsum, norm_min));
       ts[4] = clock64();
       if (valid) {
         const int vis = modality[t] ? 0 : 1;  // hist[e][0] vision, [e][1] text
