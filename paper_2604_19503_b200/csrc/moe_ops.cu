@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(256) permute_kernel(
   int32_t* s_base = sm;                       // [E]
   int32_t* s_cnt = s_base + E;                // [kPermWarps][E]
   int32_t* s_pos = s_cnt + kPermWarps * E;    // [REALB_CHUNK_TOKENS * k]
+  int32_t* s_eid = s_pos + REALB_CHUNK_TOKENS * k;  // [REALB_CHUNK_TOKENS * k] expert ids (read once)
   const int chunk = blockIdx.x;
   const int t0 = chunk * REALB_CHUNK_TOKENS;
   const int ntok = min(REALB_CHUNK_TOKENS, T - t0);
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(256) permute_kernel(
     const unsigned am = __ballot_sync(0xffffffffu, act);
     if (!act) continue;
     const int e = topk_idx[(int64_t)t0 * k + p];
+    s_eid[p] = e;
     const unsigned grp = __match_any_sync(am, e);
     const int before = __popc(grp & ((1u << lane) - 1u));
     const int base = s_cnt[warp * E + e];
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(256) permute_kernel(
   __syncthreads();
   // phase 3: final positions
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    const int e = topk_idx[(int64_t)t0 * k + p];
+    const int e = s_eid[p];
     const int pos = s_cnt[(p / seg) * E + e] + s_pos[p];
     s_pos[p] = pos;
     pair_pos[(int64_t)t0 * k + p] = pos;
@@ -617,7 +619,7 @@ __global__ void __launch_bounds__(256) gather_packed_fp4_kernel(const uint8_t* _
 // dispatch, the EP pack and the peer-memory pack)
 int ep_positions(const int32_t* topk_idx, int T, int E, int k, const int32_t* layout, int nchunks,
                  int32_t* pair_pos, void* stream) {
-  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  const int smem = (E + kPermWarps * E + 2 * REALB_CHUNK_TOKENS * k) * 4;
   permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(topk_idx, T, E, k, layout, pair_pos);
   return check_launch("pair positions");
 }
@@ -685,7 +687,7 @@ extern "C" int realb_dispatch_permute(const void* d_x, const int32_t* d_topk_idx
     return REALB_EINVAL;
   }
   if (T == 0) return REALB_OK;
-  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  const int smem = (E + kPermWarps * E + 2 * REALB_CHUNK_TOKENS * k) * 4;
   permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout,
                                                                 d_pair_pos);
   int rc = check_launch("realb_dispatch_permute (positions)");
@@ -711,7 +713,7 @@ extern "C" int realb_dispatch_index(const void* d_x, const int32_t* d_topk_idx, 
     return REALB_EINVAL;
   }
   if (T == 0) return REALB_OK;
-  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  const int smem = (E + kPermWarps * E + 2 * REALB_CHUNK_TOKENS * k) * 4;
   permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout, d_pair_pos,
                                                                 d_row_src);
   int rc = check_launch("realb_dispatch_index (positions)");
@@ -866,7 +868,7 @@ extern "C" int realb_ep_pack(const void* d_x, const int32_t* d_topk_idx, int T, 
     m.byte0[d] = h_rank_byte0[d];
   }
   if (T == 0) return REALB_OK;
-  const int smem = (E + kPermWarps * E + REALB_CHUNK_TOKENS * k) * 4;
+  const int smem = (E + kPermWarps * E + 2 * REALB_CHUNK_TOKENS * k) * 4;
   permute_kernel<<<nchunks, 256, smem, (cudaStream_t)stream>>>(d_topk_idx, T, E, k, d_layout,
                                                                 d_pair_pos);
   int rc = check_launch("realb_ep_pack (positions)");
